@@ -1,0 +1,91 @@
+"""Online stage of Polar Express in fp64 -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+``polar_express`` is Listing 2 written out in numpy fp64 with no
+rounding: normalise by ||X||_F * 1.01 + 1e-7 (reading R1), transpose
+when rows > cols (reading R10), then for each tuple
+A = X X^T; B = b A + c A A; X = a X + B X, repeating the last
+tuple past the table (reading R11), transpose back.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .coeffs import odd_poly
+
+
+def schedule(table, T):
+    """Listing 2 ``hs``: the first T tuples, last one repeated."""
+    table = [tuple(t) for t in table]
+    return table[:T] + [table[-1]] * max(0, T - len(table))
+
+
+def normalize(M, mode="listing2"):
+    """X_0 = M / (||M||_F * 1.01 + 1e-7) (Listing 2) -- reading R1;
+    mode 'alg1' gives Alg. 1 line 9's M / (||M||_F + 1e-2)."""
+    M = np.asarray(M, dtype=np.float64)
+    nrm = np.sqrt(np.sum(M * M))
+    if mode == "listing2":
+        return M / (nrm * 1.01 + 1e-7)
+    if mode == "alg1":
+        return M / (nrm + 1e-2)
+    raise ValueError(mode)
+
+
+def polar_express(M, table, T, norm="listing2", return_all=False):
+    """Listing 2 in fp64.  M: (rows, cols) array; table: list of
+    (a, b, c) (or (a, b) for degree 3) tuples; T: iterations."""
+    M = np.asarray(M, dtype=np.float64)
+    assert M.ndim == 2
+    tall = M.shape[0] > M.shape[1]                     # P:493 (strict, R10)
+    X = M.T if tall else M
+    X = normalize(X, norm) if norm else X.copy()
+    iterates = [X]
+    for tup in schedule(table, T):
+        A = X @ X.T
+        if len(tup) == 3:
+            a, b, c = tup
+            B = b * A + c * (A @ A)
+        else:
+            a, b = tup                                 # degree 3: B = b A
+            B = b * A
+        X = a * X + B @ X
+        iterates.append(X)
+    if tall:
+        X = X.T
+        iterates = [Y.T for Y in iterates]
+    return (X, iterates) if return_all else X
+
+
+def exact_polar(M, rtol=1e-13):
+    """polar(M) = U V^T from the rank-reduced SVD (eq. (matrixsign), P:51-53;
+    notation P:107), singular values below rtol * sigma_max dropped."""
+    M = np.asarray(M, dtype=np.float64)
+    U, s, Vt = np.linalg.svd(M, full_matrices=False)
+    if s.size == 0 or s[0] == 0:
+        return np.zeros_like(M)
+    keep = s > rtol * s[0]
+    return U[:, keep] @ Vt[keep, :]
+
+
+def composite(x, table, T):
+    """Scalar composite p* = p_T o ... o p_1 (eq. (composition))."""
+    y = np.asarray(x, dtype=np.float64)
+    for tup in schedule(table, T):
+        y = odd_poly(tup, y)
+    return y
+
+
+def via_scalar_map(M, table, T, norm="listing2"):
+    """X_T = U p*(Sigma_hat) V^T with Sigma_hat the normalised singular values
+    (definition of p(M); odd monomials via Gram).  An
+    independent route to polar_express's result, used as a pin."""
+    M = np.asarray(M, dtype=np.float64)
+    U, s, Vt = np.linalg.svd(M, full_matrices=False)
+    nrm = np.sqrt(np.sum(s * s))
+    if norm == "listing2":
+        sh = s / (nrm * 1.01 + 1e-7)
+    elif norm == "alg1":
+        sh = s / (nrm + 1e-2)
+    else:
+        sh = s
+    return (U * composite(sh, table, T)) @ Vt
