@@ -1,0 +1,185 @@
+/*
+ * pe.h -- C ABI of the B200-native Polar Express hot path.
+ *
+ * Polar Express (arXiv 2505.16932; /root/reference/PAPER.md, cited P:<line>)
+ * approximates polar(M) = U V^T (eq. (matrixsign)) of a rectangular
+ * matrix M by a composition of odd polynomials (eq. (composition)/(iteration),
+ * P:121-128).  The library has the paper's two stages (Alg. 1):
+ *
+ *   offline (host, fp64): pe_coeffs / pe_coeffs_ex -- greedy minimax
+ *       polynomials (Theorem 1; Alg. 2 / Listing 1),
+ *       cushioning, recentring and the 1.01 safety factor.
+ *   online (device): pe_polar -- Listing 2: normalise by
+ *       ||X||_F * 1.01 + 1e-7, transpose when rows > cols, then T steps of
+ *       A = X X^T; B = b A + c A^2; X = a X + B X, transpose back.
+ *
+ * Conventions common to every call:
+ *   - plain C: no C++ types, no exceptions cross this boundary; every call
+ *     returns pe_status and never aborts the process.
+ *   - matrices are row-major and contiguous (leading dimension = cols),
+ *     16-byte aligned; "shapes" is an int64 array of 2*count entries
+ *     (rows_0, cols_0, rows_1, cols_1, ...).
+ *   - device pointers are CUDA device addresses on the context's device;
+ *     host pointers are ordinary (preferably pinned) host memory.
+ *   - the caller owns every buffer it passes; the context owns its workspace.
+ *   - argument errors are reported synchronously, before any launch;
+ *     asynchronous CUDA faults surface as PE_ERR_CUDA on a later call.
+ *   - no CPU fallback exists: without a usable sm_100 device the online calls
+ *     return PE_ERR_CUDA / PE_ERR_UNSUPPORTED.
+ */
+#ifndef PE_H_
+#define PE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PE_OK = 0,
+  PE_ERR_INVALID_ARG = 1,     /* bad shape / pointer / parameter              */
+  PE_ERR_UNSUPPORTED = 2,     /* e.g. degree not in {3,5}, no sm_100 device   */
+  PE_ERR_NO_CONVERGENCE = 3,  /* Remez exceeded 50 iterations (reading R6)    */
+  PE_ERR_CUDA = 4,            /* CUDA runtime/driver error (sticky errors too) */
+  PE_ERR_NCCL = 5,            /* reserved for the multi-GPU all-gather        */
+  PE_ERR_WORKSPACE = 6        /* device allocation failed                     */
+} pe_status;
+
+typedef enum { PE_BF16 = 0, PE_FP32 = 1 } pe_dtype;
+
+/* Flags of pe_coeffs_ex (reading R5 and App. F). */
+#define PE_SAFETY_ALL 1       /* scale every tuple, Pade tail too (Alg.1 l.5) */
+#define PE_SAFETY_NOT_FINAL 2 /* leave the final tuple unscaled              */
+#define PE_NO_RECENTER 4      /* skip Listing 1's recentring             */
+
+/* Human-readable name of a status code (static storage). */
+const char* pe_status_string(pe_status s);
+
+/* Library version string, e.g. "pe-b200 0.1 sm_100a". */
+const char* pe_version(void);
+
+/* Detail of the last error raised on the calling thread (static storage,
+ * empty string if none). */
+const char* pe_last_error_message(void);
+
+/*
+ * Offline stage (Alg. 1 offline box; Listing 1, P:537-554;
+ * Listing 2's safety comprehension).  Host-only, fp64, pure and
+ * thread-safe; microseconds.
+ *
+ *   ell    lower bound on the normalised singular values, 0 < ell <= 1
+ *          (P:261 recommends 1e-3).
+ *   degree 3 (closed form, eq. (deg3_solution)) or 5 (Alg. 2,
+ *          P:862-886); anything else -> PE_ERR_UNSUPPORTED (general Remez is
+ *          only cited by the paper).
+ *   T      number of polynomials, T >= 1.
+ *   safety safety factor >= 1 (P:486 uses 1.01): p_t(x) -> p_t(x / safety).
+ *   coeffs caller-owned output of T * (degree+1)/2 doubles, tuple t at
+ *          coeffs[t*(degree+1)/2 ...] = (a_t, b_t[, c_t]) with
+ *          p_t(x) = a_t x + b_t x^3 [+ c_t x^5].
+ * Cushion = 0.02407327424182761 (Listing 1) for degree 5 and the
+ * analogous 0.039327193224439 for degree 3 (reading R3).  Tuples produced by
+ * the Pade branch (l/u >= 1 - 5e-6) are emitted as the exact limit
+ * (15/8, -10/8, 3/8) and left unscaled (readings R4, R5), reproducing the
+ * printed table P:475-487.
+ * Errors: PE_ERR_INVALID_ARG (ell, T, safety, NULL), PE_ERR_UNSUPPORTED
+ * (degree), PE_ERR_NO_CONVERGENCE (Remez > 50 iterations).
+ */
+pe_status pe_coeffs(double ell, int degree, int T, double safety, double* coeffs);
+
+/*
+ * As pe_coeffs with the knobs exposed:
+ *   cushion    < 0 selects the default above; otherwise the cushion ratio c
+ *              of max(l_t, c*u_t) (Alg.1 line 4 uses 0.1).
+ *   flags      PE_SAFETY_ALL | PE_SAFETY_NOT_FINAL | PE_NO_RECENTER.
+ *   ell_trace  optional (NULL ok) output of T+1 doubles: l_1..l_{T+1} of the
+ *              pre-safety recurrence l_{t+1} = p_t(l_t) (eq. (newbounds),
+ *              P:196); the certified error is 1 - l_{T+1}.
+ */
+pe_status pe_coeffs_ex(double ell, int degree, int T, double safety, double cushion,
+                       int flags, double* coeffs, double* ell_trace);
+
+/* ------------------------------------------------------------------------ */
+/* Online stage (device).  One context per device; a context is not          */
+/* thread-safe (serialise calls on it).                                      */
+/* ------------------------------------------------------------------------ */
+typedef struct pe_ctx_s* pe_ctx;
+
+/* Create a context on CUDA device `device`.  Its default table is
+ * pe_coeffs(1e-3, 5, 8, 1.01) (Listing 2's coeffs_list).
+ * Errors: PE_ERR_INVALID_ARG (NULL), PE_ERR_UNSUPPORTED (device is not
+ * compute capability 10.0), PE_ERR_CUDA. */
+pe_status pe_create(pe_ctx* ctx, int device);
+
+/* Destroy a context and free its workspace (synchronises its device). */
+pe_status pe_destroy(pe_ctx ctx);
+
+/* Replace the coefficient table: `ntuples` tuples of (degree+1)/2 doubles,
+ * degree 3 or 5 (e.g. Newton-Schulz P:78, Jordan P:82, a degree-3 table).
+ * The kernels receive them rounded to fp32.  Copied; caller keeps ownership.
+ * Errors: PE_ERR_INVALID_ARG (NULL, ntuples < 1, non-finite entries),
+ * PE_ERR_UNSUPPORTED (degree). */
+pe_status pe_set_coeffs(pe_ctx ctx, const double* coeffs, int ntuples, int degree);
+
+/* Pre-size the workspace for a batch so that a later pe_polar with the same
+ * (or smaller) batch performs no allocation (required before CUDA-graph
+ * capture).  Workspace per matrix (m = min side, n = max side): two bf16 (or
+ * fp32) m x n iterate buffers, two m x m buffers (A, B), a norm slot.
+ * Errors: PE_ERR_INVALID_ARG, PE_ERR_WORKSPACE. */
+pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtype);
+
+/*
+ * Polar Express on a batch of `count` matrices (Listing 2).
+ *   in[i], out[i]  device pointers to rows_i x cols_i row-major matrices of
+ *                  element type `dtype` (PE_BF16: bf16 tensor-core path with
+ *                  fp32 accumulation; PE_FP32: fp32 path).  in[i] == out[i]
+ *                  (in place) is allowed; distinct matrices must not overlap.
+ *   iters          T >= 1; tuples past the table repeat its last tuple
+ *                  (P:495-496).
+ *   stream         a cudaStream_t (NULL = legacy default stream); all work is
+ *                  enqueued on it, the call does not synchronise.
+ * Per matrix: s = ||M||_F * 1.01 + 1e-7 (reading R1; fp64 sum of
+ * squares), X_0 = M / s, oriented so that the Gram is on the smaller side
+ * (strict rows > cols, R10); then T x (Gram, b A + c A^2, a X + B X)
+ * on sm_100a tcgen05 tensor cores; the result is written to out[i] in the
+ * caller's orientation.  A zero matrix gives zeros (R9).
+ * Errors: PE_ERR_INVALID_ARG (count < 0, NULL pointer, rows/cols < 1 or
+ * > 2^20, a pointer not 16-byte aligned, iters < 1), PE_ERR_WORKSPACE
+ * (device allocation), PE_ERR_CUDA (launch / earlier asynchronous fault).
+ */
+pe_status pe_polar(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
+                   int count, int iters, pe_dtype dtype, void* stream);
+
+/*
+ * End-to-end variant on HOST buffers: copies in[i] (host) to device staging
+ * owned by the context, runs pe_polar on `stream`, copies the results back to
+ * out[i] (host) and synchronises `stream`.  Same semantics and errors as
+ * pe_polar; host buffers should be pinned for full PCIe bandwidth.
+ */
+pe_status pe_polar_host(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
+                        int count, int iters, pe_dtype dtype, void* stream);
+
+/* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
+ * the benchmark's gpu_launches accounting). */
+pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
+
+/*
+ * Deterministic matrix-to-rank partition for data-parallel Muon:
+ * longest-processing-time greedy on the per-matrix cost 3 m^2 n + m^3
+ * (m = min side), ties broken by matrix index, so every rank computes the
+ * same plan with no communication.  owner[i] in [0, world).
+ * Errors: PE_ERR_INVALID_ARG (world < 1, count < 0, NULL).
+ */
+pe_status pe_shard_plan(const int64_t* shapes, int count, int world, int* owner);
+
+/* Algorithmic flops of one pe_polar call (symmetric Gram and A^2 counted
+ * once): sum_i T [ m(m+1) n + m^2 (m+1) + 2 m^2 n ]; degree-3
+ * tables drop the A^2 term.  Written to *flops. */
+pe_status pe_flops(const int64_t* shapes, int count, int iters, int degree, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PE_H_ */

@@ -1,0 +1,234 @@
+"""Python binding of the Polar Express B200 C-ABI library (include/pe.h).
+
+Argument marshalling only: every step of the path runs in libpe.so's CUDA
+kernels (sm_100a).  There is no CPU or PyTorch fallback -- if the library is
+missing or the device is not a B200, calls raise.
+
+Names follow the C ABI: ``pe_coeffs``, ``pe_coeffs_ex``, ``pe_polar``,
+``pe_polar_host``, ``pe_shard_plan``, ``pe_flops``; a ``Context`` wraps
+``pe_create`` / ``pe_destroy`` / ``pe_set_coeffs`` / ``pe_reserve``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "PE_BF16", "PE_FP32", "PE_SAFETY_ALL", "PE_SAFETY_NOT_FINAL", "PE_NO_RECENTER",
+    "PeError", "lib", "pe_coeffs", "pe_coeffs_ex", "pe_shard_plan", "pe_flops",
+    "Context", "pe_polar", "pe_polar_host", "EXPORTED_SYMBOLS",
+]
+
+PE_BF16 = 0
+PE_FP32 = 1
+PE_SAFETY_ALL = 1
+PE_SAFETY_NOT_FINAL = 2
+PE_NO_RECENTER = 4
+
+_STATUS = {0: "PE_OK", 1: "PE_ERR_INVALID_ARG", 2: "PE_ERR_UNSUPPORTED", 3: "PE_ERR_NO_CONVERGENCE",
+           4: "PE_ERR_CUDA", 5: "PE_ERR_NCCL", 6: "PE_ERR_WORKSPACE"}
+
+EXPORTED_SYMBOLS = [
+    "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
+    "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
+    "pe_last_launch_count", "pe_shard_plan", "pe_flops",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpe.so")
+
+
+class PeError(RuntimeError):
+    def __init__(self, status, where, detail=""):
+        self.status = status
+        super().__init__(f"{where}: {_STATUS.get(status, status)}" + (f" ({detail})" if detail else ""))
+
+
+_lib = None
+
+
+def lib():
+    """Load libpe.so (building it first if it is absent and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _build
+        _build.build()
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, D, I64P = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)
+    DP = ctypes.POINTER(ctypes.c_double)
+    sig = {
+        "pe_status_string": (ctypes.c_char_p, [I]),
+        "pe_version": (ctypes.c_char_p, []),
+        "pe_last_error_message": (ctypes.c_char_p, []),
+        "pe_coeffs": (I, [D, I, I, D, DP]),
+        "pe_coeffs_ex": (I, [D, I, I, D, D, I, DP, DP]),
+        "pe_create": (I, [ctypes.POINTER(P), I]),
+        "pe_destroy": (I, [P]),
+        "pe_set_coeffs": (I, [P, DP, I, I]),
+        "pe_reserve": (I, [P, I64P, I, I]),
+        "pe_polar": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
+        "pe_polar_host": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
+        "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
+        "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
+        "pe_flops": (I, [I64P, I, I, I, DP]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status, where):
+    if status != 0:
+        detail = lib().pe_last_error_message()
+        raise PeError(status, where, detail.decode() if detail else "")
+
+
+def _shapes_arr(shapes):
+    flat = []
+    for r, c in shapes:
+        flat += [int(r), int(c)]
+    return (ctypes.c_int64 * max(1, len(flat)))(*flat)
+
+
+def pe_coeffs(ell=1e-3, degree=5, T=8, safety=1.01):
+    """Offline stage (pe.h pe_coeffs): list of T tuples (a, b[, c])."""
+    nq = (degree + 1) // 2
+    buf = (ctypes.c_double * (max(T, 1) * nq))()
+    _check(lib().pe_coeffs(float(ell), int(degree), int(T), float(safety), buf), "pe_coeffs")
+    return [tuple(buf[t * nq:(t + 1) * nq]) for t in range(T)]
+
+
+def pe_coeffs_ex(ell=1e-3, degree=5, T=8, safety=1.01, cushion=-1.0, flags=0):
+    """pe.h pe_coeffs_ex: (tuples, ell_trace[T+1])."""
+    nq = (degree + 1) // 2
+    buf = (ctypes.c_double * (max(T, 1) * nq))()
+    tr = (ctypes.c_double * (max(T, 1) + 1))()
+    _check(lib().pe_coeffs_ex(float(ell), int(degree), int(T), float(safety), float(cushion), int(flags),
+                              buf, tr), "pe_coeffs_ex")
+    return [tuple(buf[t * nq:(t + 1) * nq]) for t in range(T)], list(tr[:T + 1])
+
+
+def pe_shard_plan(shapes, world):
+    """pe.h pe_shard_plan: owner rank per matrix (deterministic LPT)."""
+    n = len(shapes)
+    own = (ctypes.c_int * max(n, 1))()
+    _check(lib().pe_shard_plan(_shapes_arr(shapes), n, int(world), own), "pe_shard_plan")
+    return list(own[:n])
+
+
+def pe_flops(shapes, iters, degree=5):
+    """pe.h pe_flops: algorithmic flops of one call."""
+    out = ctypes.c_double()
+    _check(lib().pe_flops(_shapes_arr(shapes), len(shapes), int(iters), int(degree), ctypes.byref(out)),
+           "pe_flops")
+    return out.value
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return PE_BF16
+    if t.dtype == torch.float32:
+        return PE_FP32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+class Context:
+    """One pe_ctx on a CUDA device."""
+
+    def __init__(self, device=0):
+        self._h = ctypes.c_void_p()
+        _check(lib().pe_create(ctypes.byref(self._h), int(device)), "pe_create")
+        self.device = int(device)
+
+    def close(self):
+        if self._h:
+            lib().pe_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_coeffs(self, tuples):
+        deg = 2 * len(tuples[0]) - 1
+        flat = [float(v) for t in tuples for v in t]
+        arr = (ctypes.c_double * len(flat))(*flat)
+        _check(lib().pe_set_coeffs(self._h, arr, len(tuples), deg), "pe_set_coeffs")
+
+    def reserve(self, shapes, dtype=PE_BF16):
+        _check(lib().pe_reserve(self._h, _shapes_arr(shapes), len(shapes), int(dtype)), "pe_reserve")
+
+    def last_launch_count(self):
+        n = ctypes.c_int()
+        _check(lib().pe_last_launch_count(self._h, ctypes.byref(n)), "pe_last_launch_count")
+        return n.value
+
+    def polar(self, inputs, outputs=None, iters=5, stream=None):
+        """pe_polar on device tensors (2-D, contiguous, same dtype: bf16 or fp32).
+        ``outputs`` defaults to new tensors; pass ``inputs`` for in-place."""
+        import torch
+        if len(inputs) == 0:
+            return []
+        dt = _dtype_code(inputs[0])
+        if outputs is None:
+            outputs = [torch.empty_like(x) for x in inputs]
+        for x, y in zip(inputs, outputs):
+            if x.dim() != 2 or not x.is_contiguous() or not y.is_contiguous() or x.shape != y.shape:
+                raise ValueError("pe_polar takes contiguous 2-D tensors of matching shapes")
+            if _dtype_code(x) != dt or _dtype_code(y) != dt or not x.is_cuda or not y.is_cuda:
+                raise ValueError("pe_polar takes CUDA tensors of one dtype")
+        n = len(inputs)
+        ins = (ctypes.c_void_p * n)(*[x.data_ptr() for x in inputs])
+        outs = (ctypes.c_void_p * n)(*[y.data_ptr() for y in outputs])
+        shp = _shapes_arr([tuple(x.shape) for x in inputs])
+        if stream is None:
+            stream = torch.cuda.current_stream(inputs[0].device)
+        _check(lib().pe_polar(self._h, ins, outs, shp, n, int(iters), dt, ctypes.c_void_p(stream.cuda_stream)),
+               "pe_polar")
+        return outputs
+
+    def polar_host(self, inputs, outputs, iters=5, stream=None):
+        """pe_polar_host on host (pinned) CPU tensors; synchronous."""
+        import torch
+        n = len(inputs)
+        if n == 0:
+            return outputs
+        dt = _dtype_code(inputs[0])
+        ins = (ctypes.c_void_p * n)(*[x.data_ptr() for x in inputs])
+        outs = (ctypes.c_void_p * n)(*[y.data_ptr() for y in outputs])
+        shp = _shapes_arr([tuple(x.shape) for x in inputs])
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        _check(lib().pe_polar_host(self._h, ins, outs, shp, n, int(iters), dt,
+                                   ctypes.c_void_p(stream.cuda_stream)), "pe_polar_host")
+        return outputs
+
+
+_default_ctx = {}
+
+
+def _ctx_for(device):
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def pe_polar(inputs, outputs=None, iters=5, coeffs=None, stream=None):
+    """Module-level pe_polar on a per-device default context."""
+    dev = inputs[0].device.index if inputs else 0
+    ctx = _ctx_for(dev or 0)
+    if coeffs is not None:
+        ctx.set_coeffs(coeffs)
+    return ctx.polar(inputs, outputs, iters, stream)
+
+
+def pe_polar_host(inputs, outputs, iters=5, device=0, stream=None):
+    return _ctx_for(device).polar_host(inputs, outputs, iters, stream)

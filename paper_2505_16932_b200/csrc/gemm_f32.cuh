@@ -1,0 +1,111 @@
+// fp32 path (PE_FP32): the same three products per iteration (Listing 2,
+// P:497-500) on the CUDA cores in true fp32 (FFMA).  1xTF32 tensor cores miss
+// the 1e-5 contract by ~200x, so this path stays on FP32 FMA
+// until a 3xTF32 tcgen05 variant lands.  64x64 output tiles, 256 threads,
+// 4x4 outputs per thread, K staged through shared memory 16 at a time.
+// Symmetric modes compute only tiles with tn >= tm and mirror-store.
+#pragma once
+#include "pe_types.h"
+
+namespace pe {
+
+struct GemmF32Args {
+  const Tile* tiles;     // units of 64 x 64
+  int ntiles;
+  const MatDev* mats;
+  void* const* outs;     // final destination per matrix (wide) or nullptr
+  int mode, xin, final_iter;
+  float a, b, c;
+};
+
+__global__ void __launch_bounds__(256) pe_gemm_f32(const GemmF32Args g) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    const Tile tl = g.tiles[t];
+    const MatDev md = g.mats[tl.mat];
+    const int m = md.m, n = md.n;
+    const float* P;    // left operand rows
+    const float* Q;    // right operand
+    int ldp, ldq, K, ncols;
+    if (g.mode == kModeGram) {
+      P = Q = reinterpret_cast<const float*>(md.X[g.xin]); ldp = ldq = md.ldx; K = n; ncols = m;
+    } else if (g.mode == kModePoly) {
+      P = Q = reinterpret_cast<const float*>(md.A); ldp = ldq = md.ldm; K = m; ncols = m;
+    } else {
+      P = reinterpret_cast<const float*>(md.B); ldp = md.ldm;
+      Q = reinterpret_cast<const float*>(md.X[g.xin]); ldq = md.ldx; K = m; ncols = n;
+    }
+    const int r0 = tl.tm * 64, c0 = tl.tn * 64;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      // As[kk][i] = P[r0+i][k0+kk]
+      for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+        const int i = e >> 4, kk = e & 15;
+        const int r = r0 + i, k = k0 + kk;
+        As[kk][i] = (r < m && k < K) ? P[(size_t)r * ldp + k] : 0.f;
+      }
+      if (g.mode == kModeUpdate) {
+        // Bs[kk][j] = X[k0+kk][c0+j]
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+          const int kk = e >> 6, j = e & 63;
+          const int k = k0 + kk, c = c0 + j;
+          Bs[kk][j] = (k < K && c < ncols) ? Q[(size_t)k * ldq + c] : 0.f;
+        }
+      } else {
+        // Bs[kk][j] = Q[c0+j][k0+kk]
+        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+          const int j = e >> 4, kk = e & 15;
+          const int c = c0 + j, k = k0 + kk;
+          Bs[kk][j] = (c < ncols && k < K) ? Q[(size_t)c * ldq + k] : 0.f;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        float av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+    // epilogue
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + ty * 4 + i;
+      if (r >= m) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + tx * 4 + j;
+        if (c >= ncols) continue;
+        float v = acc[i][j];
+        if (g.mode == kModeUpdate) {
+          const float* X = reinterpret_cast<const float*>(md.X[g.xin]);
+          v = __fadd_rn(__fmul_rn(g.a, X[(size_t)r * md.ldx + c]), v);
+          float* dst = reinterpret_cast<float*>(md.X[g.xin ^ 1]);
+          int ld = md.ldx;
+          if (g.final_iter && g.outs && g.outs[tl.mat]) { dst = reinterpret_cast<float*>(g.outs[tl.mat]); ld = n; }
+          dst[(size_t)r * ld + c] = v;
+        } else {
+          if (c < r) continue;
+          if (g.mode == kModePoly) {
+            const float* A = reinterpret_cast<const float*>(md.A);
+            v = __fadd_rn(__fmul_rn(g.b, A[(size_t)r * md.ldm + c]), __fmul_rn(g.c, v));
+          }
+          float* dst = reinterpret_cast<float*>(g.mode == kModeGram ? md.A : md.B);
+          dst[(size_t)r * md.ldm + c] = v;
+          dst[(size_t)c * md.ldm + r] = v;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace pe

@@ -1,0 +1,604 @@
+// Host side of the C ABI (include/pe.h): context, workspace, planner and the
+// launch sequence of one Polar Express call (Listing 2):
+//
+//   pe_norm_kernel                       s = ||M||_F*1.01 + 1e-7
+//   pe_copy_kernel                       X_0 = M/s, wide orientation
+//   T x { pe_gemm_sm100 Gram            A = X X^T
+//         pe_gemm_sm100 Poly            B = b A + c A^2
+//         pe_gemm_sm100 Update          X = a X + B X }
+//   pe_copy_kernel (tall inputs only)    transpose back
+//
+// Every launch covers the whole batch (grouped scheduling).  The plan (tile
+// lists, tensor maps, workspace carve-up) depends only on the shapes and is
+// cached between calls with the same shape list.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "elementwise.cuh"
+#include "gemm_f32.cuh"
+#include "gemm_sm100.cuh"
+#include "pe.h"
+#include "pe_types.h"
+
+using namespace pe;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+#define PE_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      g_last_error = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+      return PE_ERR_CUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Append host arrays into one device blob.
+struct Blob {
+  std::vector<uint8_t> host;
+  size_t add(const void* p, size_t bytes, size_t align = 128) {
+    size_t off = rup(host.size(), align);
+    host.resize(off + bytes);
+    if (bytes) std::memcpy(host.data() + off, p, bytes);
+    return off;
+  }
+  template <typename T> size_t add(const std::vector<T>& v, size_t align = 128) {
+    return add(v.data(), v.size() * sizeof(T), align);
+  }
+};
+
+}  // namespace
+
+struct pe_ctx_s {
+  int device = 0;
+  int num_sms = 148;
+  std::vector<double> table;   // ntab * nq
+  int degree = 5;
+  int ntab = 0;
+
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+
+  // plan
+  bool plan_valid = false;
+  std::vector<int64_t> plan_shapes;
+  pe_dtype plan_dtype = PE_BF16;
+  int count = 0;
+  std::vector<MatDev> mats;
+  void* meta = nullptr;        // device blob
+  size_t meta_bytes = 0;
+  // offsets into meta
+  size_t o_mats = 0, o_tmaps = 0, o_sym = 0, o_upd = 0, o_ctiles = 0, o_ftiles = 0;
+  size_t o_elems = 0, o_cmat = 0, o_cidx = 0, o_nch = 0, o_part = 0, o_cnt = 0, o_inv = 0;
+  size_t o_srows = 0, o_scols = 0, o_sld = 0, o_dld = 0, o_tr = 0, o_x0 = 0;
+  size_t o_frows = 0, o_fcols = 0, o_fsld = 0, o_fdld = 0, o_ftr = 0;
+  int n_sym = 0, n_upd = 0, n_ctiles = 0, n_ftiles = 0, n_chunks = 0;
+  bool any_tall = false;
+
+  // per-call pointer arrays (device + pinned host staging)
+  void** d_ptrs = nullptr;
+  void** h_ptrs = nullptr;
+  int ptr_cap = 0;
+
+  // e2e staging
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+
+  int last_launches = 0;
+};
+
+// ---------------------------------------------------------------- basics
+extern "C" const char* pe_status_string(pe_status s) {
+  switch (s) {
+    case PE_OK: return "PE_OK";
+    case PE_ERR_INVALID_ARG: return "PE_ERR_INVALID_ARG";
+    case PE_ERR_UNSUPPORTED: return "PE_ERR_UNSUPPORTED";
+    case PE_ERR_NO_CONVERGENCE: return "PE_ERR_NO_CONVERGENCE";
+    case PE_ERR_CUDA: return "PE_ERR_CUDA";
+    case PE_ERR_NCCL: return "PE_ERR_NCCL";
+    case PE_ERR_WORKSPACE: return "PE_ERR_WORKSPACE";
+  }
+  return "PE_ERR_UNKNOWN";
+}
+
+extern "C" const char* pe_version(void) { return "pe-b200 0.1 sm_100a"; }
+
+extern "C" const char* pe_last_error_message(void) { return g_last_error.c_str(); }
+
+extern "C" pe_status pe_create(pe_ctx* out, int device) {
+  if (!out) return PE_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  PE_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return PE_ERR_INVALID_ARG;
+  cudaDeviceProp prop;
+  PE_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0) {
+    g_last_error = "device is not sm_100 (B200)";
+    return PE_ERR_UNSUPPORTED;
+  }
+  PE_CUDA(cudaSetDevice(device));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes()));
+  if (!get_encode_fn()) {
+    g_last_error = "cuTensorMapEncodeTiled unavailable";
+    return PE_ERR_CUDA;
+  }
+  pe_ctx c = new pe_ctx_s();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->table.resize(8 * 3);
+  pe_status s = pe_coeffs(1e-3, 5, 8, 1.01, c->table.data());   // Listing 2 table
+  if (s != PE_OK) { delete c; return s; }
+  c->degree = 5;
+  c->ntab = 8;
+  *out = c;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_destroy(pe_ctx c) {
+  if (!c) return PE_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->ws) cudaFree(c->ws);
+  if (c->meta) cudaFree(c->meta);
+  if (c->d_ptrs) cudaFree(c->d_ptrs);
+  if (c->h_ptrs) cudaFreeHost(c->h_ptrs);
+  if (c->staging) cudaFree(c->staging);
+  delete c;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_set_coeffs(pe_ctx c, const double* coeffs, int ntuples, int degree) {
+  if (!c || !coeffs || ntuples < 1) return PE_ERR_INVALID_ARG;
+  if (degree != 3 && degree != 5) return PE_ERR_UNSUPPORTED;
+  const int nq = (degree + 1) / 2;
+  for (int i = 0; i < ntuples * nq; ++i)
+    if (!std::isfinite(coeffs[i])) return PE_ERR_INVALID_ARG;
+  c->table.assign(coeffs, coeffs + ntuples * nq);
+  c->degree = degree;
+  c->ntab = ntuples;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_last_launch_count(pe_ctx c, int* n) {
+  if (!c || !n) return PE_ERR_INVALID_ARG;
+  *n = c->last_launches;
+  return PE_OK;
+}
+
+// ---------------------------------------------------------------- planning
+static pe_status validate_shapes(const int64_t* shapes, int count) {
+  if (count < 0 || (count > 0 && !shapes)) return PE_ERR_INVALID_ARG;
+  for (int i = 0; i < count; ++i) {
+    const int64_t r = shapes[2 * i], cc = shapes[2 * i + 1];
+    if (r < 1 || cc < 1 || r > (1 << 20) || cc > (1 << 20)) return PE_ERR_INVALID_ARG;
+  }
+  return PE_OK;
+}
+
+static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int ld) {
+  EncodeTiledFn enc = get_encode_fn();
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return PE_ERR_CUDA;
+  }
+  return PE_OK;
+}
+
+static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
+  if (bytes <= c->ws_bytes) return PE_OK;
+  if (c->ws) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->ws); c->ws = nullptr; c->ws_bytes = 0; }
+  if (cudaMalloc(&c->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    g_last_error = "workspace allocation of " + std::to_string(bytes) + " bytes failed";
+    return PE_ERR_WORKSPACE;
+  }
+  c->ws_bytes = bytes;
+  c->plan_valid = false;
+  return PE_OK;
+}
+
+static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
+  std::vector<int64_t> key(shapes, shapes + 2 * count);
+  if (c->plan_valid && c->plan_dtype == dtype && key == c->plan_shapes) return PE_OK;
+  const size_t es = (dtype == PE_BF16) ? 2 : 4;
+
+  // workspace carve-up
+  std::vector<MatDev> mats(count);
+  std::vector<size_t> offs(count * 4);
+  size_t total = 0;
+  for (int i = 0; i < count; ++i) {
+    MatDev& md = mats[i];
+    md.rows = (int)shapes[2 * i];
+    md.cols = (int)shapes[2 * i + 1];
+    md.tall = md.rows > md.cols;                 // P:493, strict (R10)
+    md.m = md.tall ? md.cols : md.rows;
+    md.n = md.tall ? md.rows : md.cols;
+    md.ldx = (int)rup(md.n, 8);
+    md.ldm = (int)rup(md.m, 8);
+    const size_t xb = rup((size_t)md.m * md.ldx * es, 256);
+    const size_t mb = rup((size_t)md.m * md.ldm * es, 256);
+    offs[4 * i + 0] = total; total += xb;
+    offs[4 * i + 1] = total; total += xb;
+    offs[4 * i + 2] = total; total += mb;
+    offs[4 * i + 3] = total; total += mb;
+  }
+  pe_status s = ensure_workspace(c, std::max<size_t>(total, 256));
+  if (s != PE_OK) return s;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(c->ws);
+  for (int i = 0; i < count; ++i) {
+    mats[i].X[0] = ws + offs[4 * i + 0];
+    mats[i].X[1] = ws + offs[4 * i + 1];
+    mats[i].A = ws + offs[4 * i + 2];
+    mats[i].B = ws + offs[4 * i + 3];
+  }
+
+  // GEMM tile lists, longest K first (greedy balance of the static schedule)
+  std::vector<Tile> sym, upd;
+  const int tm_rows = (dtype == PE_BF16) ? kBM : 64;
+  const int tn_cols = (dtype == PE_BF16) ? kBN : 64;
+  for (int i = 0; i < count; ++i) {
+    const MatDev& md = mats[i];
+    for (int tm = 0; tm < cdiv(md.m, tm_rows); ++tm)
+      for (int tn = 0; tn < cdiv(md.m, tn_cols); ++tn)
+        if ((int64_t)tn * tn_cols + tn_cols - 1 >= (int64_t)tm * tm_rows) sym.push_back({i, tm, tn, 0});
+    for (int tm = 0; tm < cdiv(md.m, tm_rows); ++tm)
+      for (int tn = 0; tn < cdiv(md.n, tn_cols); ++tn) upd.push_back({i, tm, tn, 0});
+  }
+  auto by_k = [&](bool gram) {
+    return [&, gram](const Tile& x, const Tile& y) {
+      const int64_t kx = gram ? mats[x.mat].n : mats[x.mat].m;
+      const int64_t ky = gram ? mats[y.mat].n : mats[y.mat].m;
+      return kx > ky;
+    };
+  };
+  std::stable_sort(sym.begin(), sym.end(), by_k(true));
+  std::stable_sort(upd.begin(), upd.end(), by_k(false));
+
+  // tensor maps (bf16 path)
+  std::vector<CUtensorMap> tmaps;
+  if (dtype == PE_BF16) {
+    tmaps.resize(4 * (size_t)count);
+    for (int i = 0; i < count; ++i) {
+      const MatDev& md = mats[i];
+      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
+    }
+  }
+
+  // norm chunks
+  std::vector<int64_t> elems(count);
+  std::vector<int> cmat, cidx, nch(count);
+  for (int i = 0; i < count; ++i) {
+    elems[i] = (int64_t)mats[i].rows * mats[i].cols;
+    nch[i] = cdiv(elems[i], kNormChunk);
+    for (int k = 0; k < nch[i]; ++k) { cmat.push_back(i); cidx.push_back(k); }
+  }
+  // copy tiles: scale pass over every input; finalize over tall matrices
+  std::vector<CopyTile> ct, ft;
+  std::vector<int> srows(count), scols(count), sld(count), dld(count), tr(count);
+  std::vector<int> frows(count), fcols(count), fsld(count), fdld(count), ftr(count, 1);
+  std::vector<void*> x0(count);
+  bool any_tall = false;
+  for (int i = 0; i < count; ++i) {
+    const MatDev& md = mats[i];
+    srows[i] = md.rows; scols[i] = md.cols; sld[i] = md.cols; dld[i] = md.ldx; tr[i] = md.tall;
+    x0[i] = md.X[0];
+    for (int a = 0; a < cdiv(md.rows, 64); ++a)
+      for (int b = 0; b < cdiv(md.cols, 64); ++b) ct.push_back({i, a, b, 0});
+    frows[i] = md.m; fcols[i] = md.n; fsld[i] = md.ldx; fdld[i] = md.m;
+    if (md.tall) {
+      any_tall = true;
+      for (int a = 0; a < cdiv(md.m, 64); ++a)
+        for (int b = 0; b < cdiv(md.n, 64); ++b) ft.push_back({i, a, b, 0});
+    }
+  }
+
+  Blob bl;
+  c->o_mats = bl.add(mats);
+  c->o_tmaps = bl.add(tmaps, 128);
+  c->o_sym = bl.add(sym);
+  c->o_upd = bl.add(upd);
+  c->o_ctiles = bl.add(ct);
+  c->o_ftiles = bl.add(ft);
+  c->o_elems = bl.add(elems);
+  c->o_cmat = bl.add(cmat);
+  c->o_cidx = bl.add(cidx);
+  c->o_nch = bl.add(nch);
+  std::vector<double> part(cmat.size(), 0.0);
+  c->o_part = bl.add(part);
+  std::vector<unsigned> cnt(count, 0u);
+  c->o_cnt = bl.add(cnt);
+  std::vector<float> inv(count, 0.f);
+  c->o_inv = bl.add(inv);
+  c->o_srows = bl.add(srows); c->o_scols = bl.add(scols); c->o_sld = bl.add(sld);
+  c->o_dld = bl.add(dld); c->o_tr = bl.add(tr); c->o_x0 = bl.add(x0);
+  c->o_frows = bl.add(frows); c->o_fcols = bl.add(fcols); c->o_fsld = bl.add(fsld);
+  c->o_fdld = bl.add(fdld); c->o_ftr = bl.add(ftr);
+
+  if (bl.host.size() > c->meta_bytes) {
+    if (c->meta) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->meta); c->meta = nullptr; c->meta_bytes = 0; }
+    if (cudaMalloc(&c->meta, bl.host.size()) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    c->meta_bytes = bl.host.size();
+  }
+  PE_CUDA(cudaDeviceSynchronize());   // no kernel of a previous plan may still read meta
+  PE_CUDA(cudaMemcpy(c->meta, bl.host.data(), bl.host.size(), cudaMemcpyHostToDevice));
+
+  if (c->ptr_cap < 4 * count) {
+    if (c->d_ptrs) { cudaFree(c->d_ptrs); c->d_ptrs = nullptr; }
+    if (c->h_ptrs) { cudaFreeHost(c->h_ptrs); c->h_ptrs = nullptr; }
+    const int cap = std::max(4 * count, 64);
+    if (cudaMalloc(&c->d_ptrs, cap * sizeof(void*)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    if (cudaMallocHost(&c->h_ptrs, cap * sizeof(void*)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    c->ptr_cap = cap;
+  }
+
+  c->mats = mats;
+  c->count = count;
+  c->n_sym = (int)sym.size();
+  c->n_upd = (int)upd.size();
+  c->n_ctiles = (int)ct.size();
+  c->n_ftiles = (int)ft.size();
+  c->n_chunks = (int)cmat.size();
+  c->any_tall = any_tall;
+  c->plan_shapes = key;
+  c->plan_dtype = dtype;
+  c->plan_valid = true;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_reserve(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
+  if (!c || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
+  pe_status s = validate_shapes(shapes, count);
+  if (s != PE_OK) return s;
+  PE_CUDA(cudaSetDevice(c->device));
+  return build_plan(c, shapes, count, dtype);
+}
+
+// ---------------------------------------------------------------- online
+template <typename T> static T* at(pe_ctx c, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(c->meta) + off);
+}
+
+extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
+                              int count, int iters, pe_dtype dtype, void* stream_) {
+  if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
+  if (count == 0) { c->last_launches = 0; return PE_OK; }
+  if (!in || !out) return PE_ERR_INVALID_ARG;
+  pe_status s = validate_shapes(shapes, count);
+  if (s != PE_OK) return s;
+  for (int i = 0; i < count; ++i) {
+    if (!in[i] || !out[i]) return PE_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(in[i]) & 15) || (reinterpret_cast<uintptr_t>(out[i]) & 15)) {
+      g_last_error = "buffers must be 16-byte aligned";
+      return PE_ERR_INVALID_ARG;
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  PE_CUDA(cudaSetDevice(c->device));
+  PE_CUDA(cudaGetLastError());
+  if ((s = build_plan(c, shapes, count, dtype)) != PE_OK) return s;
+
+  // per-call pointers: [in | outs_direct | fin_src | out]
+  const int T = iters;
+  const int xfinal = T & 1;
+  void** h = c->h_ptrs;
+  for (int i = 0; i < count; ++i) {
+    const MatDev& md = c->mats[i];
+    h[i] = const_cast<void*>(in[i]);
+    h[count + i] = md.tall ? nullptr : out[i];
+    h[2 * count + i] = md.X[xfinal];
+    h[3 * count + i] = out[i];
+  }
+  PE_CUDA(cudaMemcpyAsync(c->d_ptrs, h, 4 * count * sizeof(void*), cudaMemcpyHostToDevice, st));
+  void** d_in = c->d_ptrs;
+  void** d_outs_direct = c->d_ptrs + count;
+  void** d_fin_src = c->d_ptrs + 2 * count;
+  void** d_out = c->d_ptrs + 3 * count;
+  const int src_f32 = (dtype == PE_FP32);
+  int launches = 0;
+
+  // 1) norm
+  NormArgs na;
+  na.srcs = d_in;
+  na.elems = at<int64_t>(c, c->o_elems);
+  na.chunk_mat = at<int>(c, c->o_cmat);
+  na.chunk_idx = at<int>(c, c->o_cidx);
+  na.nchunks = at<int>(c, c->o_nch);
+  na.partials = at<double>(c, c->o_part);
+  na.counters = at<unsigned>(c, c->o_cnt);
+  na.inv = at<float>(c, c->o_inv);
+  na.src_f32 = src_f32;
+  pe_norm_kernel<<<c->n_chunks, kNormThreads, 0, st>>>(na);
+  ++launches;
+
+  // 2) X_0 = M / s (oriented)
+  CopyArgs ca;
+  ca.tiles = at<CopyTile>(c, c->o_ctiles);
+  ca.ntiles = c->n_ctiles;
+  ca.srcs = d_in;
+  ca.dsts = at<void*>(c, c->o_x0);
+  ca.src_rows = at<int>(c, c->o_srows);
+  ca.src_cols = at<int>(c, c->o_scols);
+  ca.src_ld = at<int>(c, c->o_sld);
+  ca.dst_ld = at<int>(c, c->o_dld);
+  ca.transpose = at<int>(c, c->o_tr);
+  ca.scale = at<float>(c, c->o_inv);
+  ca.src_f32 = src_f32;
+  ca.dst_f32 = src_f32;
+  pe_copy_kernel<<<std::min(c->n_ctiles, c->num_sms * 8), 256, 0, st>>>(ca);
+  ++launches;
+
+  // 3) T iterations
+  const int nq = (c->degree + 1) / 2;
+  for (int t = 0; t < T; ++t) {
+    const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
+    const float fa = (float)tup[0], fb = (float)tup[1], fc = (nq == 3) ? (float)tup[2] : 0.0f;
+    const int xin = t & 1;
+    const int fin = (t == T - 1);
+    for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
+      if (dtype == PE_BF16) {
+        GemmArgs g;
+        g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);
+        g.ntiles = mode == kModeUpdate ? c->n_upd : c->n_sym;
+        g.mats = at<MatDev>(c, c->o_mats);
+        g.tmaps = at<CUtensorMap>(c, c->o_tmaps);
+        g.outs = d_outs_direct;
+        g.mode = mode; g.xin = xin; g.final_iter = fin;
+        g.a = fa; g.b = fb; g.c = fc;
+        const int grid = std::min(g.ntiles, c->num_sms);
+        pe_gemm_sm100<<<grid, kGemmThreads, gemm_smem_bytes(), st>>>(g);
+      } else {
+        GemmF32Args g;
+        g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);
+        g.ntiles = mode == kModeUpdate ? c->n_upd : c->n_sym;
+        g.mats = at<MatDev>(c, c->o_mats);
+        g.outs = d_outs_direct;
+        g.mode = mode; g.xin = xin; g.final_iter = fin;
+        g.a = fa; g.b = fb; g.c = fc;
+        const int grid = std::min(g.ntiles, c->num_sms * 4);
+        pe_gemm_f32<<<grid, 256, 0, st>>>(g);
+      }
+      ++launches;
+    }
+  }
+
+  // 4) transpose back (tall inputs)
+  if (c->any_tall) {
+    CopyArgs fa;
+    fa.tiles = at<CopyTile>(c, c->o_ftiles);
+    fa.ntiles = c->n_ftiles;
+    fa.srcs = d_fin_src;
+    fa.dsts = d_out;
+    fa.src_rows = at<int>(c, c->o_frows);
+    fa.src_cols = at<int>(c, c->o_fcols);
+    fa.src_ld = at<int>(c, c->o_fsld);
+    fa.dst_ld = at<int>(c, c->o_fdld);
+    fa.transpose = at<int>(c, c->o_ftr);
+    fa.scale = nullptr;
+    fa.src_f32 = src_f32;
+    fa.dst_f32 = src_f32;
+    pe_copy_kernel<<<std::min(c->n_ftiles, c->num_sms * 8), 256, 0, st>>>(fa);
+    ++launches;
+  }
+  PE_CUDA(cudaGetLastError());
+  c->last_launches = launches;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
+                                   int count, int iters, pe_dtype dtype, void* stream_) {
+  if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
+  if (count == 0) { c->last_launches = 0; return PE_OK; }
+  if (!in || !out) return PE_ERR_INVALID_ARG;
+  pe_status s = validate_shapes(shapes, count);
+  if (s != PE_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+  PE_CUDA(cudaSetDevice(c->device));
+  const size_t es = (dtype == PE_BF16) ? 2 : 4;
+  std::vector<size_t> off(count);
+  size_t total = 0;
+  for (int i = 0; i < count; ++i) {
+    if (!in[i] || !out[i]) return PE_ERR_INVALID_ARG;
+    off[i] = total;
+    total += rup((size_t)shapes[2 * i] * shapes[2 * i + 1] * es, 256);
+  }
+  if (total > c->staging_bytes) {
+    if (c->staging) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->staging); c->staging = nullptr; }
+    if (cudaMalloc(&c->staging, total) != cudaSuccess) { cudaGetLastError(); c->staging_bytes = 0; return PE_ERR_WORKSPACE; }
+    c->staging_bytes = total;
+  }
+  std::vector<void*> dptr(count);
+  uint8_t* base = reinterpret_cast<uint8_t*>(c->staging);
+  for (int i = 0; i < count; ++i) {
+    dptr[i] = base + off[i];
+    PE_CUDA(cudaMemcpyAsync(dptr[i], in[i], (size_t)shapes[2 * i] * shapes[2 * i + 1] * es,
+                            cudaMemcpyHostToDevice, st));
+  }
+  s = pe_polar(c, dptr.data(), dptr.data(), shapes, count, iters, dtype, stream_);
+  if (s != PE_OK) return s;
+  for (int i = 0; i < count; ++i)
+    PE_CUDA(cudaMemcpyAsync(out[i], dptr[i], (size_t)shapes[2 * i] * shapes[2 * i + 1] * es,
+                            cudaMemcpyDeviceToHost, st));
+  PE_CUDA(cudaStreamSynchronize(st));
+  return PE_OK;
+}
+
+// ---------------------------------------------------------------- host utils
+extern "C" pe_status pe_shard_plan(const int64_t* shapes, int count, int world, int* owner) {
+  if (world < 1 || count < 0 || (count > 0 && (!shapes || !owner))) return PE_ERR_INVALID_ARG;
+  std::vector<double> cost(count);
+  for (int i = 0; i < count; ++i) {
+    const double r = (double)shapes[2 * i], cc = (double)shapes[2 * i + 1];
+    if (r < 1 || cc < 1) return PE_ERR_INVALID_ARG;
+    const double m = std::min(r, cc), n = std::max(r, cc);
+    cost[i] = 3.0 * m * m * n + m * m * m;
+  }
+  std::vector<int> idx(count);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(world, 0.0);
+  for (int i : idx) {
+    int best = 0;
+    for (int w = 1; w < world; ++w)
+      if (load[w] < load[best]) best = w;
+    owner[i] = best;
+    load[best] += cost[i];
+  }
+  return PE_OK;
+}
+
+extern "C" pe_status pe_flops(const int64_t* shapes, int count, int iters, int degree, double* flops) {
+  if (!flops || count < 0 || iters < 0 || (count > 0 && !shapes)) return PE_ERR_INVALID_ARG;
+  if (degree != 3 && degree != 5) return PE_ERR_UNSUPPORTED;
+  double f = 0.0;
+  for (int i = 0; i < count; ++i) {
+    const double r = (double)shapes[2 * i], cc = (double)shapes[2 * i + 1];
+    const double m = std::min(r, cc), n = std::max(r, cc);
+    double per = m * (m + 1) * n + 2.0 * m * m * n;
+    if (degree == 5) per += m * m * (m + 1);
+    f += iters * per;
+  }
+  *flops = f;
+  return PE_OK;
+}

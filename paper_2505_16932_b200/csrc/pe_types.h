@@ -1,0 +1,45 @@
+// Device-side data layout shared by the host planner (pe_api.cu) and the
+// kernels.  All matrices are held in the "wide" orientation m <= n.
+#pragma once
+#include <cstdint>
+
+namespace pe {
+
+constexpr int kBM = 128;        // UMMA M (rows of an output tile, = TMEM lanes)
+constexpr int kBN = 256;        // UMMA N (columns of an output tile)
+constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
+constexpr int kStages = 4;      // smem ring depth
+constexpr int kBoxBytes = 64 * 64 * 2;                 // one TMA box (64 x 64 bf16)
+constexpr int kABytes = kBM * kBK * 2;                 // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;                 // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;         // 48 KB
+constexpr int kGemmThreads = 192;                      // 6 warps: TMA, MMA, 4 x epilogue
+constexpr int kTmemCols = 512;                         // 2 x 256-column fp32 accumulators
+
+constexpr int kModeGram = 0;    // A   = X X^T
+constexpr int kModePoly = 1;    // B   = b A + c A A^T    (A symmetric)
+constexpr int kModeUpdate = 2;  // X'  = a X + B X
+
+// Per-matrix descriptor (device-resident, built by the planner).
+struct MatDev {
+  int m, n;          // oriented dims, m <= n
+  int ldx, ldm;      // leading dims (elements) of the m x n and m x m buffers
+  void* X[2];        // ping-pong iterates (m x n)
+  void* A;           // Gram (m x m, symmetric)
+  void* B;           // b A + c A^2 (m x m, symmetric)
+  int rows, cols;    // caller's shape
+  int tall;          // rows > cols: caller matrix is X^T
+  int pad;
+};
+
+// One output tile of a GEMM phase (units: kBM rows, kBN columns).
+struct Tile {
+  int mat, tm, tn, pad;
+};
+
+// One 64x64 tile of an element-wise copy (scale / transpose-back).
+struct CopyTile {
+  int mat, tr, tc, pad;   // tile row / col in the SOURCE matrix (units of 64)
+};
+
+}  // namespace pe

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.  Gates (from BASELINE.json
+north_star and SURVEY §8c):
+  G1  bf16, Gaussian / cond <= 10:  relF(gpu, oracle) <= 2e-2
+  G2  bf16, cond up to 1/ell:      relF restricted to sigma >= 0.1 sigma_max
+                                   <= 2e-2 and whole relF <= max(2e-2, 2 S(M))
+  G3  bf16, all inputs:            relF(gpu, polar) <= relF(oracle, polar) + 1e-2
+  F32 fp32 path:                   relF(gpu, oracle) <= 1e-5
+  BIT diagonal inputs: bit-exact against the R8 rounding-point emulation.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import pe_synth as syn
+from oracle import coeffs as oc
+from oracle import emulate, iteration as oi, metrics as om
+
+torch = pytest.importorskip("torch")
+pe = pytest.importorskip("paper_2505_16932_b200")
+
+pytestmark = pytest.mark.gpu
+
+TABLE, _ = oc.pe_coeffs(1e-3, 5, 8, 1.01)   # the oracle's own table (Listing 2)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = pe.Context(0)
+    yield c
+    c.close()
+
+
+def to_dev_bf16(M):
+    bits = syn.f32_to_bf16_bits(np.asarray(M, dtype=np.float32))
+    t = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16)
+    return t.cuda()
+
+
+def bf16_values(M):
+    return syn.to_bf16_values(M).astype(np.float64)
+
+
+def run(ctx, mats, T=5, dtype="bf16"):
+    if dtype == "bf16":
+        xs = [to_dev_bf16(M) for M in mats]
+    else:
+        xs = [torch.from_numpy(np.asarray(M, dtype=np.float32)).cuda() for M in mats]
+    ys = ctx.polar(xs, iters=T)
+    torch.cuda.synchronize()
+    return [y.float().cpu().numpy().astype(np.float64) for y in ys]
+
+
+def check_g1_g3(X, Mb, T=5, g1=2e-2):
+    ref = oi.polar_express(Mb, TABLE, T)
+    r = om.rel_frobenius(X, ref)
+    assert np.all(np.isfinite(X))
+    assert r <= g1, f"G1 relF={r:.4g}"
+    P = oi.exact_polar(Mb)
+    assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
+    return r
+
+
+@pytest.mark.parametrize("shape", [(768, 768), (256, 1024), (1024, 256), (768, 3072), (3072, 768),
+                                   (384, 640), (200, 520), (520, 200), (130, 1000), (37, 100), (8, 8),
+                                   (1, 64), (64, 1), (129, 257)])
+def test_gaussian_parity(ctx, shape):
+    M = syn.gaussian(*shape, seed=shape[0] * 7 + shape[1], std=0.02)
+    Mb = bf16_values(M)
+    X = run(ctx, [Mb])[0]
+    assert X.shape == shape
+    if min(shape) == 1:
+        # rank one: polar = M/|M|; bf16 error only
+        assert om.rel_frobenius(X, oi.polar_express(Mb, TABLE, 5)) <= 2e-2
+        return
+    # G1 is stated for m >= 64: below that the R8
+    # rounding points alone give 1.4-2.3e-2 (CPU emulation, 20 seeds at 37x100)
+    check_g1_g3(X, Mb, g1=2e-2 if min(shape) >= 64 else 3e-2)
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 6, 7, 8, 10])
+def test_iteration_counts(ctx, T):
+    """T past the table repeats the last tuple."""
+    M = syn.gaussian(256, 768, seed=T, std=1.0)
+    Mb = bf16_values(M)
+    X = run(ctx, [Mb], T=T)[0]
+    ref = oi.polar_express(Mb, TABLE, T)
+    # early iterates sit on steep parts of the composite (chaotic bf16
+    # sensitivity); the G1 gate applies from T >= 3 (SURVEY App. A 3.)
+    assert om.rel_frobenius(X, ref) <= (2e-2 if T >= 3 else 3e-2)
+
+
+def test_batch_mixed_shapes_and_batch_independence(ctx):
+    """One grouped call over a GPT-2-Small layer (6 matrices, both
+    orientations) equals per-matrix oracle results; each matrix's result is
+    bitwise independent of the batch it was computed in."""
+    shapes = syn.layer_set_shapes("gpt2-small", layers=1)
+    mats = [bf16_values(syn.gaussian(r, c, seed=i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    outs = run(ctx, mats)
+    for X, Mb in zip(outs, mats):
+        check_g1_g3(X, Mb)
+    alone = run(ctx, [mats[4]])[0]
+    assert np.array_equal(alone, outs[4])
+    again = run(ctx, mats)
+    for a, b in zip(outs, again):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kappa", [10.0, 100.0, 1000.0])
+@pytest.mark.parametrize("shape", [(256, 1024), (512, 512)])
+def test_prescribed_spectrum(ctx, kappa, shape):
+    k = min(shape)
+    M = syn.prescribed_spectrum(*shape, syn.logspaced(k, kappa), seed=int(kappa))
+    Mb = bf16_values(M)
+    X = run(ctx, [Mb])[0]
+    ref = oi.polar_express(Mb, TABLE, 5)
+    P = oi.exact_polar(Mb)
+    r = om.rel_frobenius(X, ref)
+    if kappa <= 10:
+        assert r <= 2e-2
+    else:
+        S = om.rel_frobenius(oi.polar_express(M, TABLE, 5), ref)
+        assert r <= max(2e-2, 2 * S), (r, S)
+        assert om.truncated_rel_frobenius(X, Mb, 0.1, reference=ref) <= 2e-2
+    assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
+    assert np.all(np.isfinite(X))
+
+
+@pytest.mark.parametrize("shape", [(64, 96), (96, 64), (200, 200), (300, 1100)])
+def test_diagonal_bit_exact(ctx, shape):
+    """Diagonal inputs: every product has one non-zero term, so the GPU must
+    equal the R8 rounding-point emulation bit for bit."""
+    k = min(shape)
+    sig = syn.to_bf16_values(np.linspace(1.0, 0.02, k)).astype(np.float64)
+    M = syn.diagonal(*shape, sig)
+    for T in (1, 3, 5, 8):
+        X = run(ctx, [M], T=T)[0]
+        emu = emulate.diagonal_bf16(sig, TABLE, T).astype(np.float64)
+        assert np.array_equal(np.diag(X)[:k], emu), T
+        off = X.copy()
+        off[np.arange(k), np.arange(k)] = 0
+        assert np.all(off == 0)
+
+
+@pytest.mark.parametrize("shape", [(128, 128), (1024, 4096), (4096, 1024), (2048, 2048)])
+def test_hadamard_closed_form(ctx, shape):
+    """Equal singular values: X_T = p*(sigma_hat) M / sqrt(n),
+    sigma_hat = sqrt(n) / (1.01 sqrt(mn) + 1e-7) -- no oracle run needed."""
+    M = syn.hadamard_rows(*shape)
+    m, n = min(shape), max(shape)
+    sh = math.sqrt(n) / (1.01 * math.sqrt(m * n) + 1e-7)
+    X = run(ctx, [M])[0]
+    s = float(oi.composite(sh, TABLE, 5))
+    assert om.rel_frobenius(X, s * M / math.sqrt(n)) <= 2e-2
+
+
+def test_symmetries_zero_and_inplace(ctx):
+    """Odd symmetry p(-M) = -p(M) bitwise (odd polynomials); transpose
+    trick pe(M^T) = pe(M)^T; zero input -> zeros (R9);
+    in-place call equals out-of-place."""
+    M = bf16_values(syn.gaussian(192, 448, seed=11, std=0.02))
+    X, Xn, Xt = run(ctx, [M, -M, M.T.copy()])
+    assert np.array_equal(Xn, -X)
+    assert np.array_equal(Xt, X.T)
+    Z = run(ctx, [np.zeros((64, 128))])[0]
+    assert np.all(Z == 0)
+    x = to_dev_bf16(M)
+    ctx.polar([x], [x], iters=5)
+    torch.cuda.synchronize()
+    assert np.array_equal(x.float().cpu().numpy().astype(np.float64), X)
+
+
+def test_host_entry_point_matches_device(ctx):
+    shapes = [(256, 512), (512, 256)]
+    mats = [bf16_values(syn.gaussian(r, c, seed=3, std=0.02)) for r, c in shapes]
+    dev = run(ctx, mats)
+    ins = [to_dev_bf16(M).cpu().pin_memory() for M in mats]
+    outs = [torch.empty_like(x).pin_memory() for x in ins]
+    ctx.polar_host(ins, outs, iters=5)
+    for a, b in zip(outs, dev):
+        assert np.array_equal(a.float().numpy().astype(np.float64), b)
+
+
+def test_fp32_config1(ctx):
+    """BASELINE.json configs[0]: one 128x128 fp32 Gaussian, T=5: relF <= 1e-5."""
+    for seed in (0, 1, 2):
+        M = syn.gaussian(128, 128, seed=seed).astype(np.float32).astype(np.float64)
+        X = run(ctx, [M], dtype="f32")[0]
+        assert om.rel_frobenius(X, oi.polar_express(M, TABLE, 5)) <= 1e-5
+
+
+@pytest.mark.parametrize("shape", [(256, 1024), (1024, 256), (300, 700), (512, 512)])
+def test_fp32_parity(ctx, shape):
+    M = syn.gaussian(*shape, seed=5).astype(np.float32).astype(np.float64)
+    X = run(ctx, [M], dtype="f32")[0]
+    assert om.rel_frobenius(X, oi.polar_express(M, TABLE, 5)) <= 1e-5
+
+
+def test_other_tables(ctx):
+    """Same kernels with user tables: Newton-Schulz-5, Jordan
+    and a degree-3 Polar Express table."""
+    M = bf16_values(syn.gaussian(256, 512, seed=9, std=0.02))
+    for tab in ([oc.NEWTON_SCHULZ_5], [oc.JORDAN], oc.pe_coeffs(1e-3, 3, 8, 1.01)[0]):
+        ctx.set_coeffs(tab)
+        X = run(ctx, [M], T=8)[0]
+        ref = oi.polar_express(M, tab, 8)
+        assert om.rel_frobenius(X, ref) <= 3e-2
+    ctx.set_coeffs(TABLE)
+
+
+@pytest.mark.slow
+def test_full_gpt2_small_set_sampled(ctx):
+    """BASELINE configs[1] at full size in the bench launch configuration (one
+    grouped call over all 72 matrices); sampled matrices against the oracle."""
+    shapes = syn.layer_set_shapes("gpt2-small")
+    mats = [bf16_values(syn.gaussian(r, c, seed=1000 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    outs = run(ctx, mats)
+    for i in (0, 4, 5, 37, 71):
+        check_g1_g3(outs[i], mats[i])
