@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the Polar Express hot path on B200 (BASELINE.json metric:
+"polar factors/s and TFLOP/s (fraction of bf16 tensor peak) at 1/2/4/8 B200").
+
+One step = one pe_polar call over a whole Muon layer set (all §8(a) rows:
+Frobenius norm, scale/orient, T x {Gram, b A + c A^2, a X + B X}, transpose
+back), inputs resident in HBM.  Default workload: BASELINE.json configs[1]
+(GPT-2 Small layer set, 72 matrices, bf16, T=5, degree 5).  With N ranks each
+rank computes its pe_shard_plan share and the results are all-gathered
+(strong scaling of one layer set).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                       [--impl ours|reference] [--extra llama3-8b,...]
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "polar factors/s and TFLOP/s (fraction of bf16 tensor peak) at 1/2/4/8 B200"
+UNIT = "matrices/s"
+STD = 0.02          # momentum-like N(0, 0.02^2) entries (scale-invariant method)
+ELL, DEGREE = 1e-3, 5
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                bits = int(parts[3], 16) if parts[3].startswith("0x") else int(parts[3])
+                for b, name in REASON_BITS.items():
+                    if bits & b and name != "gpu_idle":
+                        reasons.add(name)
+            except ValueError:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def layer_set(name):
+    import pe_synth as syn
+    return syn.layer_set_shapes(name)
+
+
+def make_inputs(shapes, idx, device, seed=0):
+    import torch
+    g = torch.Generator(device=device)
+    xs = []
+    for i in idx:
+        g.manual_seed(seed * 100003 + i)
+        r, c = shapes[i]
+        xs.append((torch.randn((r, c), generator=g, device=device, dtype=torch.float32) * STD).to(torch.bfloat16))
+    return xs
+
+
+def kind_work(shapes, T):
+    """Algorithmic work per launch of each kernel kind."""
+    fl = {"gram": 0.0, "poly": 0.0, "update": 0.0}
+    by = {"norm": 0.0, "scale": 0.0, "transpose_back": 0.0}
+    for r, c in shapes:
+        m, n = min(r, c), max(r, c)
+        fl["gram"] += m * (m + 1) * n
+        fl["poly"] += m * m * (m + 1)
+        fl["update"] += 2.0 * m * m * n
+        by["norm"] += 2.0 * m * n
+        by["scale"] += 4.0 * m * n
+        if r > c:
+            by["transpose_back"] += 4.0 * m * n
+    return fl, by
+
+
+def roofline(prof, shapes, T, step_ms, peaks, src):
+    fl, by = kind_work(shapes, T)
+    kind = max(prof, key=lambda k: prof[k][0])
+    tot, cnt = prof[kind]
+    per_launch_ms = tot / max(cnt, 1)
+    sustained = step_ms > 50.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(kind)
+    except Exception:
+        pass
+    if kind in fl:
+        achieved = fl[kind] / (per_launch_ms * 1e-3) / 1e12
+        peak = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
+        out = {"bound": "tensor", "unit": "TFLOP/s"}
+    else:
+        achieved = by[kind] / (per_launch_ms * 1e-3) / 1e9
+        peak = peaks["hbm_gbs"]
+        out = {"bound": "hbm", "unit": "GB/s"}
+    out.update({"kernel": f"pe_gemm_sm100[{kind}]" if kind in fl else kind, "achieved": round(achieved, 2),
+                "peak": peak, "peak_source": f"{src} {'sustained' if (sustained and kind in fl) else 'burst'}",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "launch_ms": round(per_launch_ms, 4),
+                "share_of_step": round(tot / max(sum(v[0] for v in prof.values()), 1e-9), 4)})
+    return out
+
+
+def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
+    """The fp64 oracle (as it stands) on host cores over a bounded sample."""
+    import numpy as np
+    import pe_synth as syn
+    from oracle import coeffs as oc, iteration as oi
+    table, _ = oc.pe_coeffs(ELL, DEGREE, 8, 1.01)
+    # sample: the first layer's matrices (or the first matrix for big sets)
+    nl = {"gpt2-small": 12, "gpt2-large": 36}.get(_workload_name[0], 32)
+    per_layer = max(1, len(shapes) // nl)
+    sample = list(range(per_layer))
+    if sum(min(shapes[i]) ** 2 * max(shapes[i]) for i in sample) > 4e11:
+        sample = [min(range(len(shapes)), key=lambda i: min(shapes[i]) ** 2 * max(shapes[i]))]
+    mats = [syn.gaussian(*shapes[i], seed=seed + i, std=STD) for i in sample]
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        cores = max((d.get("num_threads", 0) for d in info), default=os.cpu_count())
+        blas = ",".join(sorted({d.get("internal_api", "?") for d in info}))
+    except Exception:
+        cores, blas = os.cpu_count(), "?"
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        for M in mats:
+            oi.polar_express(M, table, T)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or el * (passes + 1) / passes > max_s:
+            break
+    dense = lambda s: T * (4 * min(s) ** 2 * max(s) + 2 * min(s) ** 3)
+    f_sample = sum(dense(shapes[i]) for i in sample)
+    f_set = sum(dense(s) for s in shapes)
+    t_sample = el / passes
+    t_set = t_sample * f_set / f_sample
+    return {"value": round(len(shapes) / t_set, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{len(sample)} of {len(shapes)} matrices (layer 0), {passes} passes in {el:.1f}s, "
+                      f"numpy fp64 ({blas}); set time extrapolated by dense-flop ratio {f_set / f_sample:.1f}",
+            "s_per_set_extrapolated": round(t_set, 3), "gflops_fp64": round(f_sample / t_sample / 1e9, 2)}
+
+
+_workload_name = ["gpt2-small"]
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    shapes = layer_set(args.workload)
+    # each step = one bounded-sample pass; warmup passes untimed
+    cb = oracle_time(shapes, args.iters, budget_s=max(2.0, 1.0 * (args.steps + args.warmup)),
+                     max_s=120.0)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * cb["s_per_set_extrapolated"], 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "matrices": len(shapes), "T": args.iters, "degree": DEGREE,
+                       "ell": ELL},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dist_on):
+    """Device-timed steps of one layer set; returns per-step ms list, profile, extras."""
+    import torch
+    import paper_2505_16932_b200 as pe
+    from paper_2505_16932_b200 import dist as pdist
+    idx, owner = pdist.owned(shapes, rank, world) if world > 1 else (list(range(len(shapes))), [0] * len(shapes))
+    xs = make_inputs(shapes, idx, device)
+    ys = [torch.empty_like(x) for x in xs]
+    ctx.reserve([shapes[i] for i in idx])
+    stream = torch.cuda.current_stream(device)
+
+    def step():
+        ctx.polar(xs, ys, iters=T, stream=stream)
+        if dist_on and world > 1:
+            local = {i: y.view(-1).view(torch.uint8) for i, y in zip(idx, ys)}
+            pdist.gather_outputs(local, shapes, owner, world, 2,
+                                 lambda nb: torch.empty(nb, dtype=torch.uint8, device=device))
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(device)
+    launches = ctx.last_launch_count()
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(device)
+    ctx.profile_enable(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()                    # evict L2 (buffer > 126 MB) between timed steps
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize(device)
+    if dist_on:
+        torch.distributed.barrier()
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    return ms, prof, launches, idx, xs, ys
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gpt2-small")
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--extra", default="llama3-8b", help="comma list of extra layer sets (N=1 only), or ''")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    _workload_name[0] = args.workload
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_2505_16932_b200 as pe
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    ctx = pe.Context(local_rank)
+    peaks, src = measured_peaks()
+    T = args.iters
+    shapes = layer_set(args.workload)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ms, prof, launches, idx, xs, ys = time_workload(ctx, shapes, T, args.steps, args.warmup, world, rank,
+                                                    device, flush, dist_on)
+    clk = clocks.stop()
+    mean_ms = sum(ms) / len(ms)
+    if dist_on:
+        t = torch.tensor([mean_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        mean_ms = float(t.item())
+    flops = pe.pe_flops(shapes, T, DEGREE)
+    value = len(shapes) / (mean_ms * 1e-3)
+    tflops = flops / (mean_ms * 1e-3) / 1e12
+    peak_key = "bf16_tflops_sustained" if mean_ms > 50 else "bf16_tflops"
+
+    # e2e through the public API on pinned host buffers (H2D + D2H inside)
+    hin = [x.cpu().pin_memory() for x in xs]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    ctx.polar_host(hin, hout, iters=T)
+    e2e_ms = []
+    for _ in range(max(3, min(args.steps, 10))):
+        t0 = time.perf_counter()
+        ctx.polar_host(hin, hout, iters=T)      # synchronises its stream
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_mean = sum(e2e_ms) / len(e2e_ms)
+    if dist_on:
+        t = torch.tensor([e2e_mean], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    io_bytes = sum(x.numel() * 2 for x in xs)
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(mean_ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: seeded N(0, 0.02^2) bf16 momentum matrices generated on device",
+        "config": {"workload": args.workload, "matrices": len(shapes), "T": T, "degree": DEGREE, "ell": ELL,
+                   "coeffs": "pe_coeffs(1e-3,5,8,1.01) (Listing 2 table)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "parallelism": f"dp{world} (LPT shard + all-gather)" if world > 1 else "single GPU"},
+        "tflops": round(tflops, 2), "tflops_unit": "TFLOP/s (algorithmic, symmetric-aware)",
+        "frac_of_bf16_peak": round(tflops / peaks[peak_key], 4),
+        "peak_used": f"{peaks[peak_key]} TFLOP/s ({src} {'sustained' if peak_key.endswith('sustained') else 'burst'})",
+        "e2e": {"value": round(len(shapes) / (e2e_mean * 1e-3), 3), "unit": UNIT,
+                "ms_per_step": round(e2e_mean, 3),
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+        "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src),
+        "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+    }
+
+    # extra layer sets (north-star Llama-3-8B) at N=1
+    extras = {}
+    if world == 1 and args.extra:
+        del xs, ys, hin, hout
+        for name in [s for s in args.extra.split(",") if s and s != args.workload]:
+            sh = layer_set(name)
+            ctx2 = pe.Context(local_rank)
+            c2 = ClockSampler(local_rank)
+            c2.start()
+            ms2, prof2, l2, idx2, xs2, ys2 = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False)
+            ck2 = c2.stop()
+            m2 = sum(ms2) / len(ms2)
+            f2 = pe.pe_flops(sh, T, DEGREE)
+            extras[name] = {"matrices": len(sh), "value": round(len(sh) / (m2 * 1e-3), 3), "unit": UNIT,
+                            "ms_per_step": round(m2, 3), "steps": 3, "warmup": 3,
+                            "tflops": round(f2 / (m2 * 1e-3) / 1e12, 2),
+                            "frac_of_bf16_peak_sustained": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
+                            "frac_of_bf16_peak_burst": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+                            "roofline": roofline(prof2, sh, T, m2, peaks, src),
+                            "per_kernel_ms_per_step": {k: round(v[0] / 3, 3) for k, v in prof2.items()},
+                            "clocks": ck2}
+            del xs2, ys2
+            ctx2.close()
+            torch.cuda.empty_cache()
+        line["extra_workloads"] = extras
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_time(shapes, T)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,20 @@ pe_status pe_polar_host(pe_ctx ctx, const void* const* in, void* const* out, con
 pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
 
 /*
+ * Per-kernel timing for the benchmark's roofline report.  When enabled, every
+ * launch of pe_polar is bracketed by CUDA events on the call's stream (no
+ * extra synchronisation).  pe_profile_read synchronises those events, adds
+ * their durations into ms[kind] and launch counts into counts[kind] for the
+ * first `nkinds` kinds, and clears the pending list.  Kinds:
+ *   0 norm (pe_norm_kernel)     1 scale/orient (pe_copy_kernel)
+ *   2 Gram  3 poly  4 update (pe_gemm_sm100 / pe_gemm_f32)
+ *   5 transpose-back (pe_copy_kernel)
+ */
+#define PE_PROFILE_KINDS 6
+pe_status pe_profile_enable(pe_ctx ctx, int on);
+pe_status pe_profile_read(pe_ctx ctx, double* ms, int* counts, int nkinds);
+
+/*
  * Deterministic matrix-to-rank partition for data-parallel Muon:
  * longest-processing-time greedy on the per-matrix cost 3 m^2 n + m^3
  * (m = min side), ties broken by matrix index, so every rank computes the

@@ -31,8 +31,9 @@ _STATUS = {0: "PE_OK", 1: "PE_ERR_INVALID_ARG", 2: "PE_ERR_UNSUPPORTED", 3: "PE_
 EXPORTED_SYMBOLS = [
     "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
-    "pe_last_launch_count", "pe_shard_plan", "pe_flops",
+    "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
 ]
+PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpe.so")
@@ -73,6 +74,8 @@ def lib():
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
+        "pe_profile_enable": (I, [P, I]),
+        "pe_profile_read": (I, [P, DP, ctypes.POINTER(I), I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -170,6 +173,17 @@ class Context:
         n = ctypes.c_int()
         _check(lib().pe_last_launch_count(self._h, ctypes.byref(n)), "pe_last_launch_count")
         return n.value
+
+    def profile_enable(self, on=True):
+        _check(lib().pe_profile_enable(self._h, int(bool(on))), "pe_profile_enable")
+
+    def profile_read(self):
+        """{kind: (total_ms, launches)} accumulated since the last read."""
+        k = len(PROFILE_KINDS)
+        ms = (ctypes.c_double * k)()
+        cnt = (ctypes.c_int * k)()
+        _check(lib().pe_profile_read(self._h, ms, cnt, k), "pe_profile_read")
+        return {PROFILE_KINDS[i]: (ms[i], cnt[i]) for i in range(k)}
 
     def polar(self, inputs, outputs=None, iters=5, stream=None):
         """pe_polar on device tensors (2-D, contiguous, same dtype: bf16 or fp32).

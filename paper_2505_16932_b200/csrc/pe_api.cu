@@ -115,7 +115,59 @@ struct pe_ctx_s {
   size_t staging_bytes = 0;
 
   int last_launches = 0;
+
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Pending { int kind; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
 };
+
+namespace {
+cudaEvent_t take_event(pe_ctx c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+// Bracket one launch with events when profiling (kind = PE profile kind).
+struct ProfScope {
+  pe_ctx c; int kind; cudaStream_t st; cudaEvent_t a = nullptr;
+  ProfScope(pe_ctx c_, int k, cudaStream_t s) : c(c_), kind(k), st(s) {
+    if (c->profiling && (a = take_event(c))) cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = take_event(c);
+    if (!b) return;
+    cudaEventRecord(b, st);
+    c->pending.push_back({kind, a, b});
+  }
+};
+}  // namespace
+
+extern "C" pe_status pe_profile_enable(pe_ctx c, int on) {
+  if (!c) return PE_ERR_INVALID_ARG;
+  c->profiling = on != 0;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_profile_read(pe_ctx c, double* ms, int* counts, int nkinds) {
+  if (!c || nkinds < 0 || (nkinds > 0 && (!ms || !counts))) return PE_ERR_INVALID_ARG;
+  PE_CUDA(cudaSetDevice(c->device));
+  for (const auto& p : c->pending) {
+    PE_CUDA(cudaEventSynchronize(p.b));
+    float t = 0.f;
+    PE_CUDA(cudaEventElapsedTime(&t, p.a, p.b));
+    if (p.kind < nkinds) { ms[p.kind] += t; counts[p.kind] += 1; }
+  }
+  c->pending.clear();
+  c->ev_used = 0;
+  return PE_OK;
+}
 
 // ---------------------------------------------------------------- basics
 extern "C" const char* pe_status_string(pe_status s) {
@@ -175,6 +227,7 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   if (c->d_ptrs) cudaFree(c->d_ptrs);
   if (c->h_ptrs) cudaFreeHost(c->h_ptrs);
   if (c->staging) cudaFree(c->staging);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
   return PE_OK;
 }
@@ -449,7 +502,8 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   na.counters = at<unsigned>(c, c->o_cnt);
   na.inv = at<float>(c, c->o_inv);
   na.src_f32 = src_f32;
-  pe_norm_kernel<<<c->n_chunks, kNormThreads, 0, st>>>(na);
+  { ProfScope ps(c, 0, st);
+    pe_norm_kernel<<<c->n_chunks, kNormThreads, 0, st>>>(na); }
   ++launches;
 
   // 2) X_0 = M / s (oriented)
@@ -466,7 +520,8 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   ca.scale = at<float>(c, c->o_inv);
   ca.src_f32 = src_f32;
   ca.dst_f32 = src_f32;
-  pe_copy_kernel<<<std::min(c->n_ctiles, c->num_sms * 8), 256, 0, st>>>(ca);
+  { ProfScope ps(c, 1, st);
+    pe_copy_kernel<<<std::min(c->n_ctiles, c->num_sms * 8), 256, 0, st>>>(ca); }
   ++launches;
 
   // 3) T iterations
@@ -487,6 +542,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
         const int grid = std::min(g.ntiles, c->num_sms);
+        ProfScope ps(c, 2 + mode, st);
         pe_gemm_sm100<<<grid, kGemmThreads, gemm_smem_bytes(), st>>>(g);
       } else {
         GemmF32Args g;
@@ -497,6 +553,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
         const int grid = std::min(g.ntiles, c->num_sms * 4);
+        ProfScope ps(c, 2 + mode, st);
         pe_gemm_f32<<<grid, 256, 0, st>>>(g);
       }
       ++launches;
@@ -518,6 +575,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     fa.scale = nullptr;
     fa.src_f32 = src_f32;
     fa.dst_f32 = src_f32;
+    ProfScope ps(c, 5, st);
     pe_copy_kernel<<<std::min(c->n_ftiles, c->num_sms * 8), 256, 0, st>>>(fa);
     ++launches;
   }

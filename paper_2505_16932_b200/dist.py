@@ -1,0 +1,59 @@
+"""Data-parallel Muon sharding of a layer set.
+
+Every rank holds every momentum matrix; rank r orthogonalises the matrices
+``pe_shard_plan`` assigns to it (deterministic LPT, identical on all ranks, no
+communication), then an all-gather gives every rank every result (each rank
+needs all of polar(M) for its weight update W <- W - lr * polar(M)).
+
+torch.distributed is plumbing here (process group, NCCL/gloo transport); the
+compute runs in libpe.so.  Outputs are exchanged as raw bytes packed per rank
+in matrix-index order, so the same code runs on NCCL (GPU) and gloo (CPU
+tests).
+"""
+from __future__ import annotations
+
+from . import pe_shard_plan
+
+
+def owned(shapes, rank, world):
+    """Indices of the matrices rank `rank` computes (ascending)."""
+    owner = pe_shard_plan(shapes, world)
+    return [i for i, o in enumerate(owner) if o == rank], owner
+
+
+def _nbytes(shape, elem_size):
+    return int(shape[0]) * int(shape[1]) * elem_size
+
+
+def gather_outputs(local, shapes, owner, world, elem_size, make_buffer, group=None):
+    """All-gather per-rank results.
+
+    local       dict {matrix index -> flat uint8 tensor of that matrix's bytes}
+                for the indices this rank owns (all on one device).
+    owner       pe_shard_plan output (list, len = len(shapes)).
+    make_buffer callable(nbytes) -> zero uint8 tensor on the transport device.
+    Returns {matrix index -> flat uint8 tensor} for every matrix.
+    """
+    import torch
+    import torch.distributed as dist
+
+    per_rank = [[i for i, o in enumerate(owner) if o == r] for r in range(world)]
+    sizes = [sum(_nbytes(shapes[i], elem_size) for i in idx) for idx in per_rank]
+    cap = max(max(sizes), 1)
+    rank = dist.get_rank(group)
+    send = make_buffer(cap)
+    off = 0
+    for i in per_rank[rank]:
+        nb = _nbytes(shapes[i], elem_size)
+        send[off:off + nb].copy_(local[i].view(torch.uint8).reshape(-1))
+        off += nb
+    recv = [make_buffer(cap) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    out = {}
+    for r in range(world):
+        off = 0
+        for i in per_rank[r]:
+            nb = _nbytes(shapes[i], elem_size)
+            out[i] = recv[r][off:off + nb]
+            off += nb
+    return out
