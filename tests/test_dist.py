@@ -1,0 +1,66 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): every rank computes the
+same LPT shard plan (pe_shard_plan), owns a disjoint subset, and the
+all-gather leaves every rank with every matrix's bytes."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import pe_synth as syn
+        from paper_2505_16932_b200 import dist as pdist
+        shapes = syn.layer_set_shapes("gpt2-small", layers=2) + [(5, 7), (9, 3)]
+        idx, owner = pdist.owned(shapes, rank, world)
+        # stand-in for pe_polar results: a value pattern unique per matrix
+        local = {}
+        for i in idx:
+            r, c = shapes[i]
+            t = (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16)
+            local[i] = t.view(torch.int16).view(torch.uint8)
+        out = pdist.gather_outputs(local, shapes, owner, world, 2,
+                                   lambda nb: torch.zeros(nb, dtype=torch.uint8))
+        ok = len(out) == len(shapes)
+        for i, (r, c) in enumerate(shapes):
+            exp = (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16)
+            got = out[i].view(torch.int16).view(torch.bfloat16)
+            ok = ok and torch.equal(got, exp)
+        plans = [None] * world
+        dist.all_gather_object(plans, owner)
+        q.put((rank, ok, all(p == owner for p in plans), sorted(idx)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_and_allgather_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    owned = []
+    for rank, ok, same_plan, idx in res:
+        assert ok and same_plan
+        owned += idx
+    assert sorted(owned) == list(range(len(owned)))
