@@ -1,24 +1,32 @@
-// Grouped persistent tcgen05 GEMM for the three products of one Polar
-// Express iteration (Listing 2), bf16 in / fp32 accumulate:
+// Grouped persistent tcgen05 GEMM (CTA-pair, cta_group::2) for the three
+// products of one Polar Express iteration (Listing 2), bf16 in /
+// fp32 accumulate:
 //
 //   kModeGram   A  = X X^T           both operands K-major rows of X; only
-//                                    tiles touching the upper triangle are
-//                                    computed, each element c >= r is stored
-//                                    at (r,c) and mirrored to (c,r).
+//                                    256x256 tiles with I <= J are computed;
+//                                    off-diagonal tiles are also stored
+//                                    transposed at (J, I).
 //   kModePoly   B  = b A + c (A A^T) A symmetric so A A = A A^T (SYRK on A);
 //                                    the epilogue reads the same bf16 A
 //                                    (reading R8); mirrored like the Gram.
 //   kModeUpdate X' = a X + B X       A-operand B (K-major), B-operand X
 //                                    (MN-major: X row-major is N-contiguous).
 //
-// One launch covers every tile of every matrix of the batch (the "grouped
-// persistent scheduler"): CTA b walks tiles b, b+grid, ... of a host-built
-// list sorted longest-K first.  Warp roles (192 threads):
-//   warp 0      TMA producer: 64x64 bf16 boxes, 128B swizzle, 4-stage ring
-//   warp 1      tcgen05.mma issuer (one thread), TMEM owner
-//   warps 2..5  epilogue: tcgen05.ld -> fp32 epilogue -> bf16 global stores
-// TMEM holds two 128x256 fp32 accumulators so the epilogue of tile i
-// overlaps the main loop of tile i+1.
+// A cluster of two CTAs on one TPC computes one 256x256 output tile with
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16): CTA r holds rows
+// [128r, 128r+128) of the left operand and rows/columns [128r, 128r+128) of
+// the right operand in its shared memory, and accumulator rows
+// [128r, 128r+128) x 256 columns in its TMEM.  Per CTA:
+//   warp 0      TMA producer (64x64 bf16 boxes, 128B swizzle, 6-stage ring;
+//               bytes of both CTAs are counted on the leader's barrier)
+//   warp 1      leader: single-thread MMA issuer; both: TMEM alloc (512 cols
+//               = two 256-column fp32 accumulators -> epilogue of tile i
+//               overlaps the main loop of tile i+1)
+//   warps 2..9  epilogue: lane quadrant (warp % 4) x column half
+//               ((warp-2) / 4): tcgen05.ld -> fp32 epilogue -> bf16 stores
+// Grouped scheduling: one launch covers every tile of every matrix of the
+// batch; cluster c walks tiles c, c + #clusters, ... of a host-built list
+// (longest K first; update tiles column-major for L2 reuse of B).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -31,7 +39,9 @@ struct GemmArgs {
   const Tile* tiles;
   int ntiles;
   const MatDev* mats;
-  const CUtensorMap* tmaps;    // 4 per matrix: X[0], X[1], A, B
+  const CUtensorMap* tmaps;    // main loop, 4 per matrix: X[0], X[1], A, B (64x64 boxes, 128B swizzle)
+  const CUtensorMap* emaps;    // epilogue, 4 per matrix: X[0], X[1], A, B (16-col x 32-row boxes)
+  const CUtensorMap* omaps;    // per call: caller output (16x32 boxes), valid where outs[mat] != nullptr
   void* const* outs;           // per matrix final destination (wide, bf16) or nullptr
   int mode;
   int xin;                     // which X buffer holds the current iterate
@@ -58,9 +68,19 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* f) {
   return u;
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
+// Mirrored store of a symmetric-output chunk: element (r, c0+j) -> (c0+j, r).
+// Lanes hold consecutive r, so each store instruction writes 64 contiguous bytes.
+__device__ __forceinline__ void mirror_chunk16(__nv_bfloat16* dst, int m, int ld, int r, int c0, const float* w) {
+  if (r >= m) return;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int c = c0 + j;
+    if (c < m) dst[(size_t)c * ld + r] = __float2bfloat16_rn(w[j]);
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the 128B-swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
@@ -68,11 +88,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs 
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbars = tempty + 2;                              // kEpiWarps x kEpiSlots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbars + kEpiWarps * kEpiSlots);
+  uint8_t* epi_smem = smem + kStages * kStageBytes + kBarrierBytes;   // kEpiWarps x kEpiSlots x 1 KB
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int mode = args.mode;
+  const uint32_t rank = cluster_rank();
+  const bool leader = (rank == 0);
+  const int cid = blockIdx.x >> 1;
+  const int ncl = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -81,22 +107,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs 
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 2 * kEpiWarps);
     }
+    for (int s = 0; s < kEpiWarps * kEpiSlots; ++s) mbar_init(&xbars[s], 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 1) tmem_alloc_pair(tmem_slot, kTmemCols);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
+      const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x) {
+      for (int t = cid; t < args.ntiles; t += ncl) {
         const Tile tl = args.tiles[t];
         const MatDev& md = args.mats[tl.mat];
         const CUtensorMap* maps = args.tmaps + 4 * tl.mat;
@@ -115,175 +143,200 @@ __global__ void __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs 
           K = md.m;
         }
         const int nk = (K + kBK - 1) / kBK;
-        const int row_a = tl.tm * kBM;
-        const int col_b = tl.tn * kBN;
+        const int row_a = tl.tm * kBM + (int)rank * (kBM / 2);
+        const int col_b = tl.tn * kBN + (int)rank * (kBN / 2);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t bar = full_leader0 + stage * sizeof(uint64_t);
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * kBBytes;
-          tma_load_2d(a_dst, mapA, &full[stage], kb * kBK, row_a);
-          tma_load_2d(a_dst + kBoxBytes, mapA, &full[stage], kb * kBK, row_a + 64);
+          tma_load_2d_pair(a_dst, mapA, bar, kb * kBK, row_a);
+          tma_load_2d_pair(a_dst + kBoxBytes, mapA, bar, kb * kBK, row_a + 64);
           if (mode != kModeUpdate) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_2d(b_dst + q * kBoxBytes, mapB, &full[stage], kb * kBK, col_b + 64 * q);
+            tma_load_2d_pair(b_dst, mapB, bar, kb * kBK, col_b);
+            tma_load_2d_pair(b_dst + kBoxBytes, mapB, bar, kb * kBK, col_b + 64);
           } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_2d(b_dst + q * kBoxBytes, mapB, &full[stage], col_b + 64 * q, kb * kBK);
+            tma_load_2d_pair(b_dst, mapB, bar, col_b, kb * kBK);
+            tma_load_2d_pair(b_dst + kBoxBytes, mapB, bar, col_b + 64, kb * kBK);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_bf16(kBM, kBN, 0, mode == kModeUpdate ? 1 : 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x) {
-      const Tile tl = args.tiles[t];
-      const MatDev& md = args.mats[tl.mat];
-      const int K = (mode == kModeGram) ? md.n : md.m;
-      const int nk = (K + kBK - 1) / kBK;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * kBN;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader) {
+      const uint32_t idesc = idesc_bf16(kBM, kBN, 0, mode == kModeUpdate ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < args.ntiles; t += ncl) {
+        const Tile tl = args.tiles[t];
+        const MatDev& md = args.mats[tl.mat];
+        const int K = (mode == kModeGram) ? md.n : md.m;
+        const int nk = (K + kBK - 1) / kBK;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a_addr = smem_u32(sA + stage * kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_addr = smem_u32(sA + stage * kABytes);
+            const uint32_t b_addr = smem_u32(sB + stage * kBBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adesc = smem_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bdesc = (mode != kModeUpdate)
-                                       ? smem_desc_sw128(b_addr + k * 32, 16, 1024)
-                                       : smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = smem_desc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bdesc = (mode != kModeUpdate)
+                                         ? smem_desc_sw128(b_addr + k * 32, 16, 1024)
+                                         : smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024);
+              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+            }
+            umma_commit_pair(&empty[stage], 0x3);
           }
-          umma_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
-      __syncwarp();
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp & 3;            // TMEM lane quadrant accessible by this warp
-    const int row_in_tile = ew * 32 + lane;
+    // Warp ew owns TMEM lane quadrant q (its 32 output rows) and column half
+    // `half` (128 columns) of the CTA's 128 x 256 accumulator, processed as
+    // 16-column chunks through a 3-slot smem ring: the operand chunk (X for
+    // update, A for poly) arrives by TMA, the bf16 result is written back in
+    // place and leaves by TMA store; mirrored (transposed) stores of the
+    // symmetric phases go straight to global (64 contiguous bytes per store).
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    uint8_t* slots = epi_smem + ew * kEpiSlots * kEpiSlotBytes;
+    uint64_t* xbar = xbars + ew * kEpiSlots;
+    const bool need_load = (mode != kModeGram);
+    const int emap_in = (mode == kModeUpdate) ? args.xin : 2;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const int row_off = (int)rank * (kBM / 2) + q * 32;
+
+    // iterator over this warp's valid chunks (for operand prefetch)
+    auto valid = [&](int tt, int kk) -> bool {
+      const Tile tl2 = args.tiles[tt];
+      const MatDev& m2 = args.mats[tl2.mat];
+      const int nc = (mode == kModeUpdate) ? m2.n : m2.m;
+      return tl2.tn * kBN + half * (kBN / 2) + kk * kEpiCols < nc;
+    };
+    auto advance = [&](int& tt, int& kk) {
+      while (tt < args.ntiles) {
+        if (kk < kEpiChunks && valid(tt, kk)) return;
+        tt += ncl;
+        kk = 0;
+      }
+    };
+    auto issue_load = [&](int tt, int kk, int slot) {
+      const Tile tl2 = args.tiles[tt];
+      mbar_arrive_expect_tx(&xbar[slot], kEpiSlotBytes);
+      tma_load_2d(slots + slot * kEpiSlotBytes, args.emaps + 4 * tl2.mat + emap_in, &xbar[slot],
+                  tl2.tn * kBN + half * (kBN / 2) + kk * kEpiCols, tl2.tm * kBM + row_off);
+    };
+    int pt = cid, pk = 0;          // next chunk to prefetch
+    advance(pt, pk);
+    if (need_load && lane == 0 && pt < args.ntiles) issue_load(pt, pk, 0);
+    ++pk;
+    advance(pt, pk);
+
+    int g = 0;                     // chunks processed by this warp
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < args.ntiles; t += gridDim.x) {
+    for (int t = cid; t < args.ntiles; t += ncl) {
       const Tile tl = args.tiles[t];
       const MatDev md = args.mats[tl.mat];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int r = tl.tm * kBM + row_in_tile;
-      const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(ew * 32) << 16);
-      if (mode != kModeUpdate) {
-        // symmetric output (m x m)
-        const int m = md.m, ld = md.ldm;
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
-        const __nv_bfloat16* Ain = reinterpret_cast<const __nv_bfloat16*>(md.A);
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          const int c0 = tl.tn * kBN + ch * 32;
-          if (c0 >= m) break;                       // warp-uniform
-          float v[32];
-          tmem_ld32(t_row + ch * 32, v);
-          if (r < m && c0 + 31 >= r) {
-            if (mode == kModePoly) {
-              float av[32];
-              if (c0 + 32 <= m) {
+      const int r0 = tl.tm * kBM + row_off;
+      const int r = r0 + lane;
+      const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
+      const int ncols = (mode == kModeUpdate) ? md.n : md.m;
+      const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
+      const CUtensorMap* dmap;
+      if (mode == kModeGram) dmap = args.emaps + 4 * tl.mat + 2;
+      else if (mode == kModePoly) dmap = args.emaps + 4 * tl.mat + 3;
+      else if (args.final_iter && args.outs != nullptr && args.outs[tl.mat] != nullptr) dmap = args.omaps + tl.mat;
+      else dmap = args.emaps + 4 * tl.mat + (args.xin ^ 1);
+      __nv_bfloat16* mdst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
+      float v[32];
+#pragma unroll 1
+      for (int k2 = 0; k2 < kEpiChunks; k2 += 2) {
+        if (tl.tn * kBN + half * (kBN / 2) + k2 * kEpiCols >= ncols) break;   // warp-uniform
+        tmem_ld32(t_row + k2 * kEpiCols, v);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) load8_bf16(Ain + (size_t)r * ld + c0 + 8 * q, av + 8 * q);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int k = k2 + h2;
+          const int c0 = tl.tn * kBN + half * (kBN / 2) + k * kEpiCols;
+          if (c0 < ncols) {
+            const int slot = g % kEpiSlots;
+            if (need_load) {
+              if (lane == 0) {
+                bulk_wait_read<1>();                  // slot of chunk g+1 (last used by g-2) is free
+                if (pt < args.ntiles) issue_load(pt, pk, (g + 1) % kEpiSlots);
+              }
+              ++pk;
+              advance(pt, pk);
+              mbar_wait(&xbar[slot], (uint32_t)((g / kEpiSlots) & 1));
+            } else {
+              if (lane == 0) bulk_wait_read<kEpiSlots - 1>();   // slot g%3 (last used by g-3) is free
+              __syncwarp();
+            }
+            float w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[j] = v[h2 * 16 + j];
+            uint4* sp = reinterpret_cast<uint4*>(slots + slot * kEpiSlotBytes + lane * (kEpiCols * 2));
+            if (need_load) {
+              float o[16];
+              load8_bf16(reinterpret_cast<const __nv_bfloat16*>(sp), o);
+              load8_bf16(reinterpret_cast<const __nv_bfloat16*>(sp + 1), o + 8);
+              if (mode == kModePoly) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) w[j] = __fadd_rn(__fmul_rn(args.b, o[j]), __fmul_rn(args.c, w[j]));
               } else {
-                for (int j = 0; j < 32; ++j)
-                  av[j] = (c0 + j < m) ? __bfloat162float(Ain[(size_t)r * ld + c0 + j]) : 0.f;
-              }
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(__fmul_rn(args.b, av[j]), __fmul_rn(args.c, v[j]));
-            }
-            if (c0 >= r && c0 + 32 <= m) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(dst + (size_t)r * ld + c0 + 8 * q) = pack8_bf16(v + 8 * q);
-            } else {
-              for (int j = 0; j < 32; ++j) {
-                const int c = c0 + j;
-                if (c >= r && c < m) dst[(size_t)r * ld + c] = __float2bfloat16_rn(v[j]);
+                for (int j = 0; j < 16; ++j) w[j] = __fadd_rn(__fmul_rn(args.a, o[j]), w[j]);
               }
             }
-          }
-          // mirrored store (c, r) for c > r; lanes = consecutive r -> contiguous
-          if (r < m) {
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-              const int c = c0 + j;
-              if (c > r && c < m) dst[(size_t)c * ld + r] = __float2bfloat16_rn(v[j]);
+            sp[0] = pack8_bf16(w);
+            sp[1] = pack8_bf16(w + 8);
+            if (mirror) mirror_chunk16(mdst, md.m, md.ldm, r, c0, w);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(dmap, slots + slot * kEpiSlotBytes, c0, r0);
+              bulk_commit();
             }
-          }
-        }
-      } else {
-        const int m = md.m, n = md.n;
-        const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.X[args.xin]);
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(md.X[args.xin ^ 1]);
-        int ldd = md.ldx;
-        if (args.final_iter && args.outs != nullptr && args.outs[tl.mat] != nullptr) {
-          dst = reinterpret_cast<__nv_bfloat16*>(args.outs[tl.mat]);
-          ldd = md.n;
-        }
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-          const int c0 = tl.tn * kBN + ch * 32;
-          if (c0 >= n) break;
-          float v[32];
-          tmem_ld32(t_row + ch * 32, v);
-          if (r < m) {
-            float xv[32];
-            const bool full_chunk = (c0 + 32 <= n);
-            if (full_chunk) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) load8_bf16(X + (size_t)r * md.ldx + c0 + 8 * q, xv + 8 * q);
-            } else {
-              for (int j = 0; j < 32; ++j)
-                xv[j] = (c0 + j < n) ? __bfloat162float(X[(size_t)r * md.ldx + c0 + j]) : 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(__fmul_rn(args.a, xv[j]), v[j]);
-            if (full_chunk && (ldd % 8) == 0) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(dst + (size_t)r * ldd + c0 + 8 * q) = pack8_bf16(v + 8 * q);
-            } else {
-              for (int j = 0; j < 32; ++j)
-                if (c0 + j < n) dst[(size_t)r * ldd + c0 + j] = __float2bfloat16_rn(v[j]);
-            }
+            ++g;
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+  if (warp == 1) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
 constexpr size_t gemm_smem_bytes() {
-  return 1024 + (size_t)kStages * kStageBytes + (2 * kStages + 4) * sizeof(uint64_t) + 16;
+  return 1024 + (size_t)kStages * kStageBytes + kBarrierBytes + (size_t)kEpiWarps * kEpiSlots * kEpiSlotBytes;
 }
 
 }  // namespace pe

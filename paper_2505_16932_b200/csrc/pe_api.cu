@@ -98,17 +98,18 @@ struct pe_ctx_s {
   void* meta = nullptr;        // device blob
   size_t meta_bytes = 0;
   // offsets into meta
-  size_t o_mats = 0, o_tmaps = 0, o_sym = 0, o_upd = 0, o_ctiles = 0, o_ftiles = 0;
+  size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0, o_ctiles = 0, o_ftiles = 0;
   size_t o_elems = 0, o_cmat = 0, o_cidx = 0, o_nch = 0, o_part = 0, o_cnt = 0, o_inv = 0;
   size_t o_srows = 0, o_scols = 0, o_sld = 0, o_dld = 0, o_tr = 0, o_x0 = 0;
   size_t o_frows = 0, o_fcols = 0, o_fsld = 0, o_fdld = 0, o_ftr = 0;
   int n_sym = 0, n_upd = 0, n_ctiles = 0, n_ftiles = 0, n_chunks = 0;
   bool any_tall = false;
 
-  // per-call pointer arrays (device + pinned host staging)
+  // per-call pointer arrays + caller-output tensor maps (device + pinned host staging)
   void** d_ptrs = nullptr;
   void** h_ptrs = nullptr;
   int ptr_cap = 0;
+  std::vector<uint8_t> direct;   // per matrix: final update stores straight into out[i]
 
   // e2e staging
   void* staging = nullptr;
@@ -260,15 +261,19 @@ static pe_status validate_shapes(const int64_t* shapes, int count) {
   return PE_OK;
 }
 
-static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int ld) {
+// bf16 2-D tensor map over a rows x cols row-major buffer with leading dim ld.
+// Main-loop operands: 64x64 boxes, 128B swizzle; epilogue chunks: 16-column x
+// 32-row boxes, no swizzle.
+static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int ld, bool epilogue = false) {
   EncodeTiledFn enc = get_encode_fn();
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {64, 64};
+  if (epilogue) { box[0] = kEpiCols; box[1] = 32; }
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, epilogue ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return PE_ERR_CUDA;
@@ -288,6 +293,9 @@ static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
   c->plan_valid = false;
   return PE_OK;
 }
+
+// per-call upload: 4*cap pointers, then cap caller-output tensor maps
+static size_t call_bytes(int cap) { return rup((size_t)4 * cap * sizeof(void*), 128) + (size_t)cap * sizeof(CUtensorMap); }
 
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
@@ -324,17 +332,19 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     mats[i].B = ws + offs[4 * i + 3];
   }
 
-  // GEMM tile lists, longest K first (greedy balance of the static schedule)
+  // GEMM tile lists.  bf16: 256x256 pair tiles, symmetric phases only I <= J;
+  // fp32: 64x64 tiles, symmetric phases only tn >= tm.  Update tiles are
+  // generated row-block fastest so concurrently running tiles share a column
+  // panel of X (L2 reuse); lists are then stably sorted longest K first.
   std::vector<Tile> sym, upd;
-  const int tm_rows = (dtype == PE_BF16) ? kBM : 64;
-  const int tn_cols = (dtype == PE_BF16) ? kBN : 64;
+  const int tile = (dtype == PE_BF16) ? kBN : 64;
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
-    for (int tm = 0; tm < cdiv(md.m, tm_rows); ++tm)
-      for (int tn = 0; tn < cdiv(md.m, tn_cols); ++tn)
-        if ((int64_t)tn * tn_cols + tn_cols - 1 >= (int64_t)tm * tm_rows) sym.push_back({i, tm, tn, 0});
-    for (int tm = 0; tm < cdiv(md.m, tm_rows); ++tm)
-      for (int tn = 0; tn < cdiv(md.n, tn_cols); ++tn) upd.push_back({i, tm, tn, 0});
+    const int nm = cdiv(md.m, tile), nn = cdiv(md.n, tile);
+    for (int tm = 0; tm < nm; ++tm)
+      for (int tn = tm; tn < nm; ++tn) sym.push_back({i, tm, tn, 0});
+    for (int tn = 0; tn < nn; ++tn)
+      for (int tm = 0; tm < nm; ++tm) upd.push_back({i, tm, tn, 0});
   }
   auto by_k = [&](bool gram) {
     return [&, gram](const Tile& x, const Tile& y) {
@@ -347,15 +357,19 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   std::stable_sort(upd.begin(), upd.end(), by_k(false));
 
   // tensor maps (bf16 path)
-  std::vector<CUtensorMap> tmaps;
+  std::vector<CUtensorMap> tmaps, emaps;
   if (dtype == PE_BF16) {
     tmaps.resize(4 * (size_t)count);
+    emaps.resize(4 * (size_t)count);
     for (int i = 0; i < count; ++i) {
       const MatDev& md = mats[i];
-      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
+      for (int e = 0; e < 2; ++e) {
+        std::vector<CUtensorMap>& v = e ? emaps : tmaps;
+        if ((s = make_tmap(&v[4 * i + 0], md.X[0], md.m, md.n, md.ldx, e)) != PE_OK) return s;
+        if ((s = make_tmap(&v[4 * i + 1], md.X[1], md.m, md.n, md.ldx, e)) != PE_OK) return s;
+        if ((s = make_tmap(&v[4 * i + 2], md.A, md.m, md.m, md.ldm, e)) != PE_OK) return s;
+        if ((s = make_tmap(&v[4 * i + 3], md.B, md.m, md.m, md.ldm, e)) != PE_OK) return s;
+      }
     }
   }
 
@@ -370,7 +384,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   // copy tiles: scale pass over every input; finalize over tall matrices
   std::vector<CopyTile> ct, ft;
   std::vector<int> srows(count), scols(count), sld(count), dld(count), tr(count);
-  std::vector<int> frows(count), fcols(count), fsld(count), fdld(count), ftr(count, 1);
+  std::vector<int> frows(count), fcols(count), fsld(count), fdld(count), ftr(count, 0);
   std::vector<void*> x0(count);
   bool any_tall = false;
   for (int i = 0; i < count; ++i) {
@@ -379,8 +393,9 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     x0[i] = md.X[0];
     for (int a = 0; a < cdiv(md.rows, 64); ++a)
       for (int b = 0; b < cdiv(md.cols, 64); ++b) ct.push_back({i, a, b, 0});
-    frows[i] = md.m; fcols[i] = md.n; fsld[i] = md.ldx; fdld[i] = md.m;
-    if (md.tall) {
+    frows[i] = md.m; fcols[i] = md.n; fsld[i] = md.ldx; fdld[i] = md.tall ? md.m : md.n;
+    ftr[i] = md.tall;
+    if (md.tall || (dtype == PE_BF16 && md.cols % 8 != 0)) {
       any_tall = true;
       for (int a = 0; a < cdiv(md.m, 64); ++a)
         for (int b = 0; b < cdiv(md.n, 64); ++b) ft.push_back({i, a, b, 0});
@@ -390,6 +405,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   Blob bl;
   c->o_mats = bl.add(mats);
   c->o_tmaps = bl.add(tmaps, 128);
+  c->o_emaps = bl.add(emaps, 128);
   c->o_sym = bl.add(sym);
   c->o_upd = bl.add(upd);
   c->o_ctiles = bl.add(ct);
@@ -417,14 +433,18 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   PE_CUDA(cudaDeviceSynchronize());   // no kernel of a previous plan may still read meta
   PE_CUDA(cudaMemcpy(c->meta, bl.host.data(), bl.host.size(), cudaMemcpyHostToDevice));
 
-  if (c->ptr_cap < 4 * count) {
+  if (c->ptr_cap < count) {
     if (c->d_ptrs) { cudaFree(c->d_ptrs); c->d_ptrs = nullptr; }
     if (c->h_ptrs) { cudaFreeHost(c->h_ptrs); c->h_ptrs = nullptr; }
-    const int cap = std::max(4 * count, 64);
-    if (cudaMalloc(&c->d_ptrs, cap * sizeof(void*)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
-    if (cudaMallocHost(&c->h_ptrs, cap * sizeof(void*)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    const int cap = std::max(count, 16);
+    const size_t bytes = call_bytes(cap);
+    if (cudaMalloc(&c->d_ptrs, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    if (cudaMallocHost(&c->h_ptrs, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
     c->ptr_cap = cap;
   }
+  c->direct.assign(count, 0);
+  for (int i = 0; i < count; ++i)
+    c->direct[i] = !mats[i].tall && (dtype == PE_FP32 || mats[i].cols % 8 == 0);
 
   c->mats = mats;
   c->count = count;
@@ -472,18 +492,27 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   PE_CUDA(cudaGetLastError());
   if ((s = build_plan(c, shapes, count, dtype)) != PE_OK) return s;
 
-  // per-call pointers: [in | outs_direct | fin_src | out]
+  // per-call pointers: [in | outs_direct | fin_src | out] + caller-output tensor maps
   const int T = iters;
   const int xfinal = T & 1;
   void** h = c->h_ptrs;
+  const size_t omap_off = rup((size_t)4 * c->ptr_cap * sizeof(void*), 128);
+  CUtensorMap* h_omaps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = c->mats[i];
     h[i] = const_cast<void*>(in[i]);
-    h[count + i] = md.tall ? nullptr : out[i];
+    h[count + i] = c->direct[i] ? out[i] : nullptr;
     h[2 * count + i] = md.X[xfinal];
     h[3 * count + i] = out[i];
+    if (c->direct[i] && dtype == PE_BF16)
+      if ((s = make_tmap(&h_omaps[i], out[i], md.rows, md.cols, md.cols, true)) != PE_OK) return s;
   }
   PE_CUDA(cudaMemcpyAsync(c->d_ptrs, h, 4 * count * sizeof(void*), cudaMemcpyHostToDevice, st));
+  if (dtype == PE_BF16)
+    PE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(c->d_ptrs) + omap_off, h_omaps, count * sizeof(CUtensorMap),
+                            cudaMemcpyHostToDevice, st));
+  const CUtensorMap* d_omaps =
+      reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(c->d_ptrs) + omap_off);
   void** d_in = c->d_ptrs;
   void** d_outs_direct = c->d_ptrs + count;
   void** d_fin_src = c->d_ptrs + 2 * count;
@@ -538,10 +567,12 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.ntiles = mode == kModeUpdate ? c->n_upd : c->n_sym;
         g.mats = at<MatDev>(c, c->o_mats);
         g.tmaps = at<CUtensorMap>(c, c->o_tmaps);
+        g.emaps = at<CUtensorMap>(c, c->o_emaps);
+        g.omaps = d_omaps;
         g.outs = d_outs_direct;
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
-        const int grid = std::min(g.ntiles, c->num_sms);
+        const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
         ProfScope ps(c, 2 + mode, st);
         pe_gemm_sm100<<<grid, kGemmThreads, gemm_smem_bytes(), st>>>(g);
       } else {

@@ -5,16 +5,23 @@
 
 namespace pe {
 
-constexpr int kBM = 128;        // UMMA M (rows of an output tile, = TMEM lanes)
-constexpr int kBN = 256;        // UMMA N (columns of an output tile)
+// bf16 tensor-core path: one 256x256 output tile per CTA pair (cta_group::2)
+constexpr int kBM = 256;        // UMMA M of the pair (128 rows per CTA = TMEM lanes)
+constexpr int kBN = 256;        // UMMA N (each CTA stages 128 of the right operand)
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
-constexpr int kStages = 4;      // smem ring depth
+constexpr int kStages = 6;      // smem ring depth
 constexpr int kBoxBytes = 64 * 64 * 2;                 // one TMA box (64 x 64 bf16)
-constexpr int kABytes = kBM * kBK * 2;                 // 16 KB
-constexpr int kBBytes = kBN * kBK * 2;                 // 32 KB
-constexpr int kStageBytes = kABytes + kBBytes;         // 48 KB
-constexpr int kGemmThreads = 192;                      // 6 warps: TMA, MMA, 4 x epilogue
+constexpr int kABytes = (kBM / 2) * kBK * 2;           // 16 KB per CTA
+constexpr int kBBytes = (kBN / 2) * kBK * 2;           // 16 KB per CTA
+constexpr int kStageBytes = kABytes + kBBytes;         // 32 KB per CTA
+constexpr int kEpiWarps = 8;                           // 4 lane quadrants x 2 column halves
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;      // TMA warp, MMA warp, epilogue warps
 constexpr int kTmemCols = 512;                         // 2 x 256-column fp32 accumulators
+constexpr int kEpiCols = 16;                           // epilogue chunk: 32 rows x 16 columns
+constexpr int kEpiChunks = (kBN / 2) / kEpiCols;       // chunks per warp per tile
+constexpr int kEpiSlots = 3;                           // smem ring per epilogue warp
+constexpr int kEpiSlotBytes = 32 * kEpiCols * 2;       // 1 KB
+constexpr int kBarrierBytes = 1024;                    // mbarriers + TMEM slot (rounded up)
 
 constexpr int kModeGram = 0;    // A   = X X^T
 constexpr int kModePoly = 1;    // B   = b A + c A A^T    (A symmetric)
