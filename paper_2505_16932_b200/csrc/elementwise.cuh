@@ -1,11 +1,14 @@
 // HBM-bound passes of the hot path:
-//   pe_norm_kernel  -- per-matrix sum of squares (fp64, deterministic
-//                      two-level reduction) -> s = ||M||_F * 1.01 + 1e-7
-//                      (Listing 2; reading R1/R2), inv = fp32(1/s).
-//   pe_copy_kernel  -- X_0 = bf16(fp32(x) * inv) in the wide orientation
-//                      (transpose trick P:493), and the final transpose-back
-//                      of tall results.  64x64 tiles through smem so
-//                      both the read and the write are row-contiguous.
+//   pe_norm_kernel       per-matrix sum of squares (fp64, deterministic
+//                        two-level reduction) -> s = ||M||_F * 1.01 + 1e-7
+//                        (Listing 2; readings R1/R2), inv = fp32(1/s).
+//   pe_rows_kernel       row-contiguous copy with optional scale: X_0 = M/s for
+//                        wide inputs, and the final copy for outputs whose
+//                        rows are not 16-byte multiples.  16-byte vectors.
+//   pe_transpose_kernel  64x64 tiles through smem: X_0 = (M/s)^T for tall
+//                        inputs (transpose trick) and the transpose
+//                        back of tall results.  16-byte vectors on
+//                        both the read and the write side.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -13,7 +16,7 @@
 
 namespace pe {
 
-constexpr int kNormChunk = 32768;   // elements per norm block
+constexpr int kNormChunk = 65536;   // elements per norm block
 constexpr int kNormThreads = 256;
 
 struct NormArgs {
@@ -28,6 +31,17 @@ struct NormArgs {
   int src_f32;                 // 1: fp32 input, 0: bf16
 };
 
+__device__ __forceinline__ double sumsq8_bf16(uint4 u) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(h[q]);
+    acc += (double)(f.x * f.x) + (double)(f.y * f.y);   // bf16^2 is exact in fp32
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a) {
   const int blk = blockIdx.x;
   const int mat = a.chunk_mat[blk];
@@ -38,32 +52,37 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
   double acc = 0.0;
   if (a.src_f32) {
     const float* p = reinterpret_cast<const float*>(a.srcs[mat]);
-    for (int64_t i = begin + (int64_t)threadIdx.x * 4; i < end; i += (int64_t)kNormThreads * 4) {
-      if (i + 4 <= end && ((reinterpret_cast<uintptr_t>(p + i) & 15) == 0)) {
-        float4 v = *reinterpret_cast<const float4*>(p + i);
+    const bool al = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    int64_t i = begin + (int64_t)threadIdx.x * 4;
+    if (al) {
+      for (; i + 4 <= end; i += (int64_t)kNormThreads * 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p + i));
         acc += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
-      } else {
-        for (int64_t j = i; j < min(i + 4, end); ++j) acc += (double)p[j] * p[j];
       }
     }
+    for (; i < end; i += (int64_t)kNormThreads * 4)
+      for (int64_t j = i; j < min(i + 4, end); ++j) acc += (double)p[j] * p[j];
   } else {
     const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(a.srcs[mat]);
-    for (int64_t i = begin + (int64_t)threadIdx.x * 8; i < end; i += (int64_t)kNormThreads * 8) {
-      if (i + 8 <= end && ((reinterpret_cast<uintptr_t>(p + i) & 15) == 0)) {
-        uint4 u = *reinterpret_cast<const uint4*>(p + i);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float2 f = __bfloat1622float2(h[q]);
-          acc += (double)(f.x * f.x) + (double)(f.y * f.y);   // bf16^2 is exact in fp32
-        }
-      } else {
-        for (int64_t j = i; j < min(i + 8, end); ++j) {
-          float f = __bfloat162float(p[j]);
-          acc += (double)(f * f);
-        }
+    const bool al = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    int64_t i = begin + (int64_t)threadIdx.x * 8;
+    constexpr int64_t kStride = (int64_t)kNormThreads * 8;
+    if (al) {
+      // four independent 16-byte loads in flight per thread
+      for (; i + 3 * kStride + 8 <= end; i += 4 * kStride) {
+        uint4 u0 = __ldg(reinterpret_cast<const uint4*>(p + i));
+        uint4 u1 = __ldg(reinterpret_cast<const uint4*>(p + i + kStride));
+        uint4 u2 = __ldg(reinterpret_cast<const uint4*>(p + i + 2 * kStride));
+        uint4 u3 = __ldg(reinterpret_cast<const uint4*>(p + i + 3 * kStride));
+        acc += sumsq8_bf16(u0) + sumsq8_bf16(u1) + sumsq8_bf16(u2) + sumsq8_bf16(u3);
       }
+      for (; i + 8 <= end; i += kStride) acc += sumsq8_bf16(__ldg(reinterpret_cast<const uint4*>(p + i)));
     }
+    for (; i < end; i += kStride)
+      for (int64_t j = i; j < min(i + 8, end); ++j) {
+        const float f = __bfloat162float(p[j]);
+        acc += (double)(f * f);
+      }
   }
   // block reduction in a fixed order (deterministic)
   __shared__ double red[kNormThreads / 32];
@@ -93,71 +112,148 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
   }
 }
 
-struct CopyArgs {
-  const CopyTile* tiles;
-  int ntiles;
-  const void* const* srcs;     // per matrix source
-  void* const* dsts;           // per matrix destination
-  const int* src_rows;         // per matrix
-  const int* src_cols;
-  const int* src_ld;
-  const int* dst_ld;
-  const int* transpose;        // per matrix: dst = src^T
-  const float* scale;          // per matrix multiplier or nullptr
-  int src_f32, dst_f32;
+// Per-matrix parameters of a copy pass (row copy or tile transpose).
+struct CopyMat {
+  int rows, cols;        // source shape
+  int sld, dld;          // leading dims (elements)
+  int pad0, pad1;
 };
 
-template <typename T> __device__ __forceinline__ float to_f(T v);
-template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
-template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+// Work item of the copy passes: a band of rows (row kernel) or a 64x64 tile
+// (transpose kernel) of one matrix.
+struct CopyItem {
+  int mat, a, b, pad;    // rows: a = first row, b = row count; transpose: a = tile row, b = tile col
+};
+
+struct CopyArgs {
+  const CopyItem* items;
+  int nitems;
+  const CopyMat* mats;
+  const void* const* srcs;     // per matrix source
+  void* const* dsts;           // per matrix destination
+  const float* scale;          // per matrix multiplier or nullptr
+};
+
+template <typename T> struct VecT;
+template <> struct VecT<__nv_bfloat16> { static constexpr int N = 8; };
+template <> struct VecT<float> { static constexpr int N = 4; };
+
+__device__ __forceinline__ void unpack(const uint4& u, float* f, __nv_bfloat16*) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void unpack(const uint4& u, float* f, float*) {
+  f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+  f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+}
+__device__ __forceinline__ uint4 pack(const float* f, __nv_bfloat16*) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+__device__ __forceinline__ uint4 pack(const float* f, float*) {
+  return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+}
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
 template <typename T> __device__ __forceinline__ T from_f(float v);
 template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
-template <typename TS, typename TD>
-__device__ __forceinline__ void copy_tile(const CopyArgs& a, const CopyTile ct, float (*tile)[65]) {
-  const int mat = ct.mat;
-  const TS* src = reinterpret_cast<const TS*>(a.srcs[mat]);
-  TD* dst = reinterpret_cast<TD*>(a.dsts[mat]);
-  const int R = a.src_rows[mat], C = a.src_cols[mat];
-  const int sld = a.src_ld[mat], dld = a.dst_ld[mat];
-  const bool tr = a.transpose[mat] != 0;
-  const float sc = a.scale ? a.scale[mat] : 1.0f;
-  const int r0 = ct.tr * 64, c0 = ct.tc * 64;
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;   // 64 x 4
-  for (int i = ty; i < 64; i += 4) {
-    const int r = r0 + i, c = c0 + tx;
-    float v = 0.f;
-    if (r < R && c < C) v = to_f<TS>(src[(size_t)r * sld + c]);
-    tile[i][tx] = a.scale ? __fmul_rn(v, sc) : v;
-  }
-  __syncthreads();
-  if (!tr) {
-    for (int i = ty; i < 64; i += 4) {
-      const int r = r0 + i, c = c0 + tx;
-      if (r < R && c < C) dst[(size_t)r * dld + c] = from_f<TD>(tile[i][tx]);
+// dst[r][c] = scale * src[r][c] for the rows of each item.
+template <typename T>
+__global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
+  constexpr int V = VecT<T>::N;
+  for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    const CopyItem ci = a.items[it];
+    const CopyMat cm = a.mats[ci.mat];
+    const T* src = reinterpret_cast<const T*>(a.srcs[ci.mat]);
+    T* dst = reinterpret_cast<T*>(a.dsts[ci.mat]);
+    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const bool vec = (cm.cols % V == 0) && (cm.sld % V == 0) && (cm.dld % V == 0) &&
+                     ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    if (vec) {
+      const int vpr = cm.cols / V;                    // vectors per row
+      const int64_t nv = (int64_t)vpr * ci.b;
+      for (int64_t e = threadIdx.x; e < nv; e += blockDim.x) {
+        const int rr = ci.a + (int)(e / vpr);
+        const int cc = (int)(e % vpr) * V;
+        const uint4 u = *reinterpret_cast<const uint4*>(src + (size_t)rr * cm.sld + cc);
+        float f[V];
+        unpack(u, f, (T*)nullptr);
+        if (a.scale) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) f[j] = __fmul_rn(f[j], sc);
+        }
+        *reinterpret_cast<uint4*>(dst + (size_t)rr * cm.dld + cc) = pack(f, (T*)nullptr);
+      }
+    } else {
+      const int64_t ne = (int64_t)cm.cols * ci.b;
+      for (int64_t e = threadIdx.x; e < ne; e += blockDim.x) {
+        const int rr = ci.a + (int)(e / cm.cols);
+        const int cc = (int)(e % cm.cols);
+        float f = to_f(src[(size_t)rr * cm.sld + cc]);
+        if (a.scale) f = __fmul_rn(f, sc);
+        dst[(size_t)rr * cm.dld + cc] = from_f<T>(f);
+      }
     }
-  } else {
-    // dst is C x R: dst[c][r] = src[r][c]
-    for (int i = ty; i < 64; i += 4) {
-      const int c = c0 + i, r = r0 + tx;
-      if (r < R && c < C) dst[(size_t)c * dld + r] = from_f<TD>(tile[tx][i]);
-    }
   }
-  __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) pe_copy_kernel(const CopyArgs a) {
+// dst (cols x rows) = (scale * src)^T, 64x64 tiles, 256 threads.
+template <typename T>
+__global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
+  constexpr int V = VecT<T>::N;                 // elements per 16-byte vector
+  constexpr int VPR = 64 / V;                   // vectors per 64-element tile row
   __shared__ float tile[64][65];
-  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    const CopyTile ct = a.tiles[t];
-    if (a.src_f32) {
-      if (a.dst_f32) copy_tile<float, float>(a, ct, tile);
-      else copy_tile<float, __nv_bfloat16>(a, ct, tile);
-    } else {
-      if (a.dst_f32) copy_tile<__nv_bfloat16, float>(a, ct, tile);
-      else copy_tile<__nv_bfloat16, __nv_bfloat16>(a, ct, tile);
+  for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    const CopyItem ci = a.items[it];
+    const CopyMat cm = a.mats[ci.mat];
+    const T* src = reinterpret_cast<const T*>(a.srcs[ci.mat]);
+    T* dst = reinterpret_cast<T*>(a.dsts[ci.mat]);
+    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const int r0 = ci.a * 64, c0 = ci.b * 64;
+    const bool vin = (cm.sld % V == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    const bool vout = (cm.dld % V == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    // load 64 x 64 (rows r0.., cols c0..)
+    for (int e = threadIdx.x; e < 64 * VPR; e += 256) {
+      const int i = e / VPR, jv = (e % VPR) * V;
+      const int r = r0 + i, c = c0 + jv;
+      float f[V];
+      if (vin && r < cm.rows && c + V <= cm.cols) {
+        unpack(*reinterpret_cast<const uint4*>(src + (size_t)r * cm.sld + c), f, (T*)nullptr);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) f[j] = (r < cm.rows && c + j < cm.cols) ? to_f(src[(size_t)r * cm.sld + c + j]) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) tile[i][jv + j] = a.scale ? __fmul_rn(f[j], sc) : f[j];
     }
+    __syncthreads();
+    // store transposed: dst row = c0 + i (source column), dst cols = r0.. (source rows)
+    for (int e = threadIdx.x; e < 64 * VPR; e += 256) {
+      const int i = e / VPR, jv = (e % VPR) * V;
+      const int dr = c0 + i, dc = r0 + jv;
+      if (dr >= cm.cols) continue;
+      float f[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) f[j] = tile[jv + j][i];
+      if (vout && dc + V <= cm.rows) {
+        *reinterpret_cast<uint4*>(dst + (size_t)dr * cm.dld + dc) = pack(f, (T*)nullptr);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          if (dc + j < cm.rows) dst[(size_t)dr * cm.dld + dc + j] = from_f<T>(f[j]);
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -98,12 +98,13 @@ struct pe_ctx_s {
   void* meta = nullptr;        // device blob
   size_t meta_bytes = 0;
   // offsets into meta
-  size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0, o_ctiles = 0, o_ftiles = 0;
+  size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0;
   size_t o_elems = 0, o_cmat = 0, o_cidx = 0, o_nch = 0, o_part = 0, o_cnt = 0, o_inv = 0;
-  size_t o_srows = 0, o_scols = 0, o_sld = 0, o_dld = 0, o_tr = 0, o_x0 = 0;
-  size_t o_frows = 0, o_fcols = 0, o_fsld = 0, o_fdld = 0, o_ftr = 0;
-  int n_sym = 0, n_upd = 0, n_ctiles = 0, n_ftiles = 0, n_chunks = 0;
-  bool any_tall = false;
+  // copy passes: scale/orient (rows: wide inputs, tr: tall inputs) and
+  // finalize (tr: tall outputs, rows: wide outputs whose rows are not 16-byte multiples)
+  size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_it[4] = {0, 0, 0, 0};
+  int n_it[4] = {0, 0, 0, 0};
+  int n_sym = 0, n_upd = 0, n_chunks = 0;
 
   // per-call pointer arrays + caller-output tensor maps (device + pinned host staging)
   void** d_ptrs = nullptr;
@@ -381,24 +382,26 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     nch[i] = cdiv(elems[i], kNormChunk);
     for (int k = 0; k < nch[i]; ++k) { cmat.push_back(i); cidx.push_back(k); }
   }
-  // copy tiles: scale pass over every input; finalize over tall matrices
-  std::vector<CopyTile> ct, ft;
-  std::vector<int> srows(count), scols(count), sld(count), dld(count), tr(count);
-  std::vector<int> frows(count), fcols(count), fsld(count), fdld(count), ftr(count, 0);
+  // copy passes (see elementwise.cuh): item lists 0 scale-rows, 1 scale-transpose,
+  // 2 finalize-transpose, 3 finalize-rows
+  std::vector<CopyItem> it[4];
+  std::vector<CopyMat> smats(count), fmats(count);
   std::vector<void*> x0(count);
-  bool any_tall = false;
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
-    srows[i] = md.rows; scols[i] = md.cols; sld[i] = md.cols; dld[i] = md.ldx; tr[i] = md.tall;
     x0[i] = md.X[0];
-    for (int a = 0; a < cdiv(md.rows, 64); ++a)
-      for (int b = 0; b < cdiv(md.cols, 64); ++b) ct.push_back({i, a, b, 0});
-    frows[i] = md.m; fcols[i] = md.n; fsld[i] = md.ldx; fdld[i] = md.tall ? md.m : md.n;
-    ftr[i] = md.tall;
-    if (md.tall || (dtype == PE_BF16 && md.cols % 8 != 0)) {
-      any_tall = true;
+    smats[i] = {md.rows, md.cols, md.cols, md.ldx, 0, 0};
+    fmats[i] = {md.m, md.n, md.ldx, md.tall ? md.m : md.n, 0, 0};
+    if (md.tall) {
+      for (int a = 0; a < cdiv(md.rows, 64); ++a)
+        for (int b = 0; b < cdiv(md.cols, 64); ++b) it[1].push_back({i, a, b, 0});
       for (int a = 0; a < cdiv(md.m, 64); ++a)
-        for (int b = 0; b < cdiv(md.n, 64); ++b) ft.push_back({i, a, b, 0});
+        for (int b = 0; b < cdiv(md.n, 64); ++b) it[2].push_back({i, a, b, 0});
+    } else {
+      const int band = std::max(1, 16384 / md.cols);
+      for (int r = 0; r < md.rows; r += band) it[0].push_back({i, r, std::min(band, md.rows - r), 0});
+      if (dtype == PE_BF16 && md.cols % 8 != 0)
+        for (int r = 0; r < md.m; r += band) it[3].push_back({i, r, std::min(band, md.m - r), 0});
     }
   }
 
@@ -408,8 +411,10 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   c->o_emaps = bl.add(emaps, 128);
   c->o_sym = bl.add(sym);
   c->o_upd = bl.add(upd);
-  c->o_ctiles = bl.add(ct);
-  c->o_ftiles = bl.add(ft);
+  for (int k = 0; k < 4; ++k) c->o_it[k] = bl.add(it[k]);
+  c->o_smats = bl.add(smats);
+  c->o_fmats = bl.add(fmats);
+  c->o_x0 = bl.add(x0);
   c->o_elems = bl.add(elems);
   c->o_cmat = bl.add(cmat);
   c->o_cidx = bl.add(cidx);
@@ -420,10 +425,6 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   c->o_cnt = bl.add(cnt);
   std::vector<float> inv(count, 0.f);
   c->o_inv = bl.add(inv);
-  c->o_srows = bl.add(srows); c->o_scols = bl.add(scols); c->o_sld = bl.add(sld);
-  c->o_dld = bl.add(dld); c->o_tr = bl.add(tr); c->o_x0 = bl.add(x0);
-  c->o_frows = bl.add(frows); c->o_fcols = bl.add(fcols); c->o_fsld = bl.add(fsld);
-  c->o_fdld = bl.add(fdld); c->o_ftr = bl.add(ftr);
 
   if (bl.host.size() > c->meta_bytes) {
     if (c->meta) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->meta); c->meta = nullptr; c->meta_bytes = 0; }
@@ -450,10 +451,8 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   c->count = count;
   c->n_sym = (int)sym.size();
   c->n_upd = (int)upd.size();
-  c->n_ctiles = (int)ct.size();
-  c->n_ftiles = (int)ft.size();
+  for (int k = 0; k < 4; ++k) c->n_it[k] = (int)it[k].size();
   c->n_chunks = (int)cmat.size();
-  c->any_tall = any_tall;
   c->plan_shapes = key;
   c->plan_dtype = dtype;
   c->plan_valid = true;
@@ -536,22 +535,29 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   ++launches;
 
   // 2) X_0 = M / s (oriented)
-  CopyArgs ca;
-  ca.tiles = at<CopyTile>(c, c->o_ctiles);
-  ca.ntiles = c->n_ctiles;
-  ca.srcs = d_in;
-  ca.dsts = at<void*>(c, c->o_x0);
-  ca.src_rows = at<int>(c, c->o_srows);
-  ca.src_cols = at<int>(c, c->o_scols);
-  ca.src_ld = at<int>(c, c->o_sld);
-  ca.dst_ld = at<int>(c, c->o_dld);
-  ca.transpose = at<int>(c, c->o_tr);
-  ca.scale = at<float>(c, c->o_inv);
-  ca.src_f32 = src_f32;
-  ca.dst_f32 = src_f32;
-  { ProfScope ps(c, 1, st);
-    pe_copy_kernel<<<std::min(c->n_ctiles, c->num_sms * 8), 256, 0, st>>>(ca); }
-  ++launches;
+  auto copy_pass = [&](int k, bool scale, bool fin) {
+    if (c->n_it[k] == 0) return;
+    CopyArgs ca;
+    ca.items = at<CopyItem>(c, c->o_it[k]);
+    ca.nitems = c->n_it[k];
+    ca.mats = at<CopyMat>(c, fin ? c->o_fmats : c->o_smats);
+    ca.srcs = fin ? d_fin_src : d_in;
+    ca.dsts = fin ? d_out : at<void*>(c, c->o_x0);
+    ca.scale = scale ? at<float>(c, c->o_inv) : nullptr;
+    const int grid = std::min(c->n_it[k], c->num_sms * 8);
+    ProfScope ps(c, fin ? 5 : 1, st);
+    const bool tr = (k == 1 || k == 2);
+    if (dtype == PE_BF16) {
+      if (tr) pe_transpose_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(ca);
+      else pe_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(ca);
+    } else {
+      if (tr) pe_transpose_kernel<float><<<grid, 256, 0, st>>>(ca);
+      else pe_rows_kernel<float><<<grid, 256, 0, st>>>(ca);
+    }
+    ++launches;
+  };
+  copy_pass(0, true, false);
+  copy_pass(1, true, false);
 
   // 3) T iterations
   const int nq = (c->degree + 1) / 2;
@@ -591,25 +597,9 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     }
   }
 
-  // 4) transpose back (tall inputs)
-  if (c->any_tall) {
-    CopyArgs fa;
-    fa.tiles = at<CopyTile>(c, c->o_ftiles);
-    fa.ntiles = c->n_ftiles;
-    fa.srcs = d_fin_src;
-    fa.dsts = d_out;
-    fa.src_rows = at<int>(c, c->o_frows);
-    fa.src_cols = at<int>(c, c->o_fcols);
-    fa.src_ld = at<int>(c, c->o_fsld);
-    fa.dst_ld = at<int>(c, c->o_fdld);
-    fa.transpose = at<int>(c, c->o_ftr);
-    fa.scale = nullptr;
-    fa.src_f32 = src_f32;
-    fa.dst_f32 = src_f32;
-    ProfScope ps(c, 5, st);
-    pe_copy_kernel<<<std::min(c->n_ftiles, c->num_sms * 8), 256, 0, st>>>(fa);
-    ++launches;
-  }
+  // 4) transpose back (tall inputs) / copy out (rows not 16-byte multiples)
+  copy_pass(2, false, true);
+  copy_pass(3, false, true);
   PE_CUDA(cudaGetLastError());
   c->last_launches = launches;
   return PE_OK;

@@ -44,9 +44,5 @@ struct Tile {
   int mat, tm, tn, pad;
 };
 
-// One 64x64 tile of an element-wise copy (scale / transpose-back).
-struct CopyTile {
-  int mat, tr, tc, pad;   // tile row / col in the SOURCE matrix (units of 64)
-};
 
 }  // namespace pe
