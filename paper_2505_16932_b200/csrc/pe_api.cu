@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -105,6 +106,7 @@ struct pe_ctx_s {
   size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_it[4] = {0, 0, 0, 0};
   int n_it[4] = {0, 0, 0, 0};
   int n_sym = 0, n_upd = 0, n_chunks = 0;
+  bool long_k[3] = {true, true, true};   // per GEMM mode: deep-ring variant (else tile-prefetch epilogue)
 
   // per-call pointer arrays + caller-output tensor maps (device + pinned host staging)
   void** d_ptrs = nullptr;
@@ -117,6 +119,8 @@ struct pe_ctx_s {
   size_t staging_bytes = 0;
 
   int last_launches = 0;
+  int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1 are set)
+  long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
 
   // profiling
   bool profiling = false;
@@ -150,6 +154,15 @@ struct ProfScope {
   }
 };
 }  // namespace
+
+// debug-only: copy the per-CTA wait counters of the last GEMM launch of each
+// mode (3 x 2048 int64) to host memory `out` (not part of the public header).
+extern "C" pe_status pe_debug_stats(pe_ctx c, long long* out) {
+  if (!c || !out || !c->stats) return PE_ERR_INVALID_ARG;
+  PE_CUDA(cudaDeviceSynchronize());
+  PE_CUDA(cudaMemcpy(out, c->stats, 3 * 2048 * sizeof(long long), cudaMemcpyDeviceToHost));
+  return PE_OK;
+}
 
 extern "C" pe_status pe_profile_enable(pe_ctx c, int on) {
   if (!c) return PE_ERR_INVALID_ARG;
@@ -202,8 +215,10 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
     return PE_ERR_UNSUPPORTED;
   }
   PE_CUDA(cudaSetDevice(device));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<6, 3>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<4, kEpiChunks>()));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -211,6 +226,7 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
   pe_ctx c = new pe_ctx_s();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  if (const char* d = getenv("PE_DEBUG_GEMM")) c->dbg = atoi(d);
   c->table.resize(8 * 3);
   pe_status s = pe_coeffs(1e-3, 5, 8, 1.01, c->table.data());   // Listing 2 table
   if (s != PE_OK) { delete c; return s; }
@@ -449,6 +465,17 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
 
   c->mats = mats;
   c->count = count;
+  // kernel variant per mode (measured on B200, profiles/r1_variants.md): the
+  // Gram has no epilogue operand, so it takes the deep 6-stage ring; poly and
+  // update take the tile-prefetch epilogue (4 stages + 8 operand slots/warp).
+  {
+    const char* ov = getenv("PE_GEMM_VARIANT");
+    for (int mode = 0; mode < 3; ++mode) {
+      c->long_k[mode] = (mode == kModeGram);
+      if (ov && !strcmp(ov, "long")) c->long_k[mode] = true;
+      if (ov && !strcmp(ov, "short")) c->long_k[mode] = false;
+    }
+  }
   c->n_sym = (int)sym.size();
   c->n_upd = (int)upd.size();
   for (int k = 0; k < 4; ++k) c->n_it[k] = (int)it[k].size();
@@ -578,9 +605,18 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.outs = d_outs_direct;
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
+        g.dbg = c->dbg;
+        g.stats = nullptr;
+        if (c->dbg & 4) {
+          if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
+          g.stats = c->stats + (size_t)mode * 2048;
+        }
         const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
         ProfScope ps(c, 2 + mode, st);
-        pe_gemm_sm100<<<grid, kGemmThreads, gemm_smem_bytes(), st>>>(g);
+        if (c->long_k[mode])
+          pe_gemm_sm100<6, 3><<<grid, kGemmThreads, gemm_smem_bytes<6, 3>(), st>>>(g);
+        else
+          pe_gemm_sm100<4, kEpiChunks><<<grid, kGemmThreads, gemm_smem_bytes<4, kEpiChunks>(), st>>>(g);
       } else {
         GemmF32Args g;
         g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);

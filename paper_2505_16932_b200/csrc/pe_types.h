@@ -8,8 +8,9 @@ namespace pe {
 // bf16 tensor-core path: one 256x256 output tile per CTA pair (cta_group::2)
 constexpr int kBM = 256;        // UMMA M of the pair (128 rows per CTA = TMEM lanes)
 constexpr int kBN = 256;        // UMMA N (each CTA stages 128 of the right operand)
+constexpr int kPrefetch = 0;    // L2 prefetch distance of the producer (k-blocks); 0 = off
+                                // (measured slower: the extra bulk-prefetch requests compete with the ring's loads)
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
-constexpr int kStages = 6;      // smem ring depth
 constexpr int kBoxBytes = 64 * 64 * 2;                 // one TMA box (64 x 64 bf16)
 constexpr int kABytes = (kBM / 2) * kBK * 2;           // 16 KB per CTA
 constexpr int kBBytes = (kBN / 2) * kBK * 2;           // 16 KB per CTA
@@ -19,7 +20,6 @@ constexpr int kGemmThreads = 64 + 32 * kEpiWarps;      // TMA warp, MMA warp, ep
 constexpr int kTmemCols = 512;                         // 2 x 256-column fp32 accumulators
 constexpr int kEpiCols = 16;                           // epilogue chunk: 32 rows x 16 columns
 constexpr int kEpiChunks = (kBN / 2) / kEpiCols;       // chunks per warp per tile
-constexpr int kEpiSlots = 3;                           // smem ring per epilogue warp
 constexpr int kEpiSlotBytes = 32 * kEpiCols * 2;       // 1 KB
 constexpr int kBarrierBytes = 1024;                    // mbarriers + TMEM slot (rounded up)
 

@@ -36,11 +36,15 @@ def test_library_is_sm100a_only():
     import subprocess
     out = subprocess.run(["cuobjdump", "-lelf", pe.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN2pe13pe_gemm_sm100ENS_8GemmArgsE", pe.LIB_PATH],
-                          capture_output=True, text=True).stdout
-    assert "UTCHMMA" in sass or "UTCQMMA" in sass or "UTCMMA" in sass
-    assert "UTMALDG" in sass
-    assert "LDTM" in sass
+    sass = subprocess.run(["cuobjdump", "-sass", pe.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    gemm = [f for f in funcs if f.startswith("_ZN2pe13pe_gemm_sm100")]
+    assert len(gemm) >= 2        # the deep-ring and the tile-prefetch variants
+    for f in gemm:
+        assert "UTCHMMA" in f or "UTCQMMA" in f or "UTCMMA" in f   # tcgen05.mma
+        assert "UTMALDG" in f                                       # TMA load
+        assert "UTMASTG" in f                                       # TMA store
+        assert "LDTM" in f                                          # tcgen05.ld
 
 
 def load_printed():
