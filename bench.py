@@ -130,7 +130,7 @@ def kind_work(shapes, T):
     return fl, by
 
 
-def roofline(prof, shapes, T, step_ms, peaks, src):
+def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
     fl, by = kind_work(shapes, T)
     kind = max(prof, key=lambda k: prof[k][0])
     tot, cnt = prof[kind]
@@ -139,7 +139,7 @@ def roofline(prof, shapes, T, step_ms, peaks, src):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(kind)
+            traffic = json.load(f).get(workload or "", {}).get(kind)
     except Exception:
         pass
     if kind in fl:
@@ -343,7 +343,7 @@ def main():
                 "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
-        "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src),
+        "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
     }
 
@@ -365,7 +365,7 @@ def main():
                             "tflops": round(f2 / (m2 * 1e-3) / 1e12, 2),
                             "frac_of_bf16_peak_sustained": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
                             "frac_of_bf16_peak_burst": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
-                            "roofline": roofline(prof2, sh, T, m2, peaks, src),
+                            "roofline": roofline(prof2, sh, T, m2, peaks, src, name),
                             "per_kernel_ms_per_step": {k: round(v[0] / 3, 3) for k, v in prof2.items()},
                             "clocks": ck2}
             del xs2, ys2
