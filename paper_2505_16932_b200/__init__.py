@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpe.so")
+LIB_PATH = os.environ.get("PE_LIB_OVERRIDE") or os.path.join(_HERE, "libpe.so")   # override: A/B experiments only
 
 
 class PeError(RuntimeError):

@@ -103,7 +103,7 @@ struct pe_ctx_s {
   size_t o_elems = 0, o_cmat = 0, o_cidx = 0, o_nch = 0, o_part = 0, o_cnt = 0, o_inv = 0;
   // copy passes: scale/orient (rows: wide inputs, tr: tall inputs) and
   // finalize (tr: tall outputs, rows: wide outputs whose rows are not 16-byte multiples)
-  size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_it[4] = {0, 0, 0, 0};
+  size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_flags = 0, o_it[4] = {0, 0, 0, 0};
   int n_it[4] = {0, 0, 0, 0};
   int n_sym = 0, n_upd = 0, n_chunks = 0;
   bool long_k[3] = {true, true, true};   // per GEMM mode: deep-ring variant (else tile-prefetch epilogue)
@@ -112,7 +112,7 @@ struct pe_ctx_s {
   void** d_ptrs = nullptr;
   void** h_ptrs = nullptr;
   int ptr_cap = 0;
-  std::vector<uint8_t> direct;   // per matrix: final update stores straight into out[i]
+  std::vector<int> flags;        // per matrix kFlag* (folded input, tall, direct output)
 
   // e2e staging
   void* staging = nullptr;
@@ -215,9 +215,13 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
     return PE_ERR_UNSUPPORTED;
   }
   PE_CUDA(cudaSetDevice(device));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<6, 3>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<6, 3>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<4, kEpiChunks>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<4, kEpiChunks>()));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
@@ -278,24 +282,29 @@ static pe_status validate_shapes(const int64_t* shapes, int count) {
   return PE_OK;
 }
 
-// bf16 2-D tensor map over a rows x cols row-major buffer with leading dim ld.
-// Main-loop operands: 64x64 boxes, 128B swizzle; epilogue chunks: 16-column x
-// 32-row boxes, no swizzle.
-static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int ld, bool epilogue = false) {
+// bf16 2-D tensor map over a rows x cols row-major buffer with leading dim ld
+// and a box of (box_cols x box_rows) elements.  Main-loop operands use 64x64
+// boxes with the 128B swizzle; epilogue chunks 16x32 (or 32x16 for the
+// transposed chunks of tall caller matrices) without swizzle.
+static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int ld, int box_cols = 64,
+                           int box_rows = 64, bool sw128 = true) {
   EncodeTiledFn enc = get_encode_fn();
   cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, 64};
-  if (epilogue) { box[0] = kEpiCols; box[1] = 32; }
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, epilogue ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return PE_ERR_CUDA;
   }
   return PE_OK;
+}
+static pe_status make_emap(CUtensorMap* map, void* base, int rows, int cols, int ld, bool transposed = false) {
+  return transposed ? make_tmap(map, base, rows, cols, ld, 32, kEpiCols, false)
+                    : make_tmap(map, base, rows, cols, ld, kEpiCols, 32, false);
 }
 
 static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
@@ -312,7 +321,9 @@ static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
 }
 
 // per-call upload: 4*cap pointers, then cap caller-output tensor maps
-static size_t call_bytes(int cap) { return rup((size_t)4 * cap * sizeof(void*), 128) + (size_t)cap * sizeof(CUtensorMap); }
+// per-call upload: 4*cap pointers, then 3 tensor maps per matrix (caller input
+// main loop, caller input epilogue chunk, caller output epilogue chunk)
+static size_t call_bytes(int cap) { return rup((size_t)4 * cap * sizeof(void*), 128) + (size_t)3 * cap * sizeof(CUtensorMap); }
 
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
@@ -380,13 +391,14 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     emaps.resize(4 * (size_t)count);
     for (int i = 0; i < count; ++i) {
       const MatDev& md = mats[i];
-      for (int e = 0; e < 2; ++e) {
-        std::vector<CUtensorMap>& v = e ? emaps : tmaps;
-        if ((s = make_tmap(&v[4 * i + 0], md.X[0], md.m, md.n, md.ldx, e)) != PE_OK) return s;
-        if ((s = make_tmap(&v[4 * i + 1], md.X[1], md.m, md.n, md.ldx, e)) != PE_OK) return s;
-        if ((s = make_tmap(&v[4 * i + 2], md.A, md.m, md.m, md.ldm, e)) != PE_OK) return s;
-        if ((s = make_tmap(&v[4 * i + 3], md.B, md.m, md.m, md.ldm, e)) != PE_OK) return s;
-      }
+      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
+      if ((s = make_emap(&emaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_emap(&emaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
+      if ((s = make_emap(&emaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
+      if ((s = make_emap(&emaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
     }
   }
 
@@ -398,26 +410,39 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     nch[i] = cdiv(elems[i], kNormChunk);
     for (int k = 0; k < nch[i]; ++k) { cmat.push_back(i); cidx.push_back(k); }
   }
-  // copy passes (see elementwise.cuh): item lists 0 scale-rows, 1 scale-transpose,
-  // 2 finalize-transpose, 3 finalize-rows
+  // Folding (gemm_sm100.cuh): bf16 matrices whose rows are 16-byte multiples
+  // are read by the first iteration straight from the caller's buffer and the
+  // last iteration writes the caller's buffer; the others go through the copy
+  // passes (see elementwise.cuh): item lists 0 scale-rows, 1 scale-transpose,
+  // 2 finalize-transpose, 3 finalize-rows.
+  std::vector<int> mflags(count, 0);
   std::vector<CopyItem> it[4];
   std::vector<CopyMat> smats(count), fmats(count);
   std::vector<void*> x0(count);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
+    const bool folded = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
+    const bool direct = (dtype == PE_BF16) ? folded : !md.tall;
+    mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0);
     x0[i] = md.X[0];
     smats[i] = {md.rows, md.cols, md.cols, md.ldx, 0, 0};
     fmats[i] = {md.m, md.n, md.ldx, md.tall ? md.m : md.n, 0, 0};
-    if (md.tall) {
-      for (int a = 0; a < cdiv(md.rows, 64); ++a)
-        for (int b = 0; b < cdiv(md.cols, 64); ++b) it[1].push_back({i, a, b, 0});
-      for (int a = 0; a < cdiv(md.m, 64); ++a)
-        for (int b = 0; b < cdiv(md.n, 64); ++b) it[2].push_back({i, a, b, 0});
-    } else {
-      const int band = std::max(1, 16384 / md.cols);
-      for (int r = 0; r < md.rows; r += band) it[0].push_back({i, r, std::min(band, md.rows - r), 0});
-      if (dtype == PE_BF16 && md.cols % 8 != 0)
+    const int band = std::max(1, 16384 / md.cols);
+    if (!folded) {
+      if (md.tall) {
+        for (int a = 0; a < cdiv(md.rows, 64); ++a)
+          for (int b = 0; b < cdiv(md.cols, 64); ++b) it[1].push_back({i, a, b, 0});
+      } else {
+        for (int r = 0; r < md.rows; r += band) it[0].push_back({i, r, std::min(band, md.rows - r), 0});
+      }
+    }
+    if (!direct) {
+      if (md.tall) {
+        for (int a = 0; a < cdiv(md.m, 64); ++a)
+          for (int b = 0; b < cdiv(md.n, 64); ++b) it[2].push_back({i, a, b, 0});
+      } else {
         for (int r = 0; r < md.m; r += band) it[3].push_back({i, r, std::min(band, md.m - r), 0});
+      }
     }
   }
 
@@ -431,6 +456,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   c->o_smats = bl.add(smats);
   c->o_fmats = bl.add(fmats);
   c->o_x0 = bl.add(x0);
+  c->o_flags = bl.add(mflags);
   c->o_elems = bl.add(elems);
   c->o_cmat = bl.add(cmat);
   c->o_cidx = bl.add(cidx);
@@ -459,9 +485,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     if (cudaMallocHost(&c->h_ptrs, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
     c->ptr_cap = cap;
   }
-  c->direct.assign(count, 0);
-  for (int i = 0; i < count; ++i)
-    c->direct[i] = !mats[i].tall && (dtype == PE_FP32 || mats[i].cols % 8 == 0);
+  c->flags = mflags;
 
   c->mats = mats;
   c->count = count;
@@ -523,22 +547,29 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   const int xfinal = T & 1;
   void** h = c->h_ptrs;
   const size_t omap_off = rup((size_t)4 * c->ptr_cap * sizeof(void*), 128);
-  CUtensorMap* h_omaps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
+  CUtensorMap* h_maps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = c->mats[i];
     h[i] = const_cast<void*>(in[i]);
-    h[count + i] = c->direct[i] ? out[i] : nullptr;
+    const int fl = c->flags[i];
+    h[count + i] = (fl & kFlagDirect) ? out[i] : nullptr;
     h[2 * count + i] = md.X[xfinal];
     h[3 * count + i] = out[i];
-    if (c->direct[i] && dtype == PE_BF16)
-      if ((s = make_tmap(&h_omaps[i], out[i], md.rows, md.cols, md.cols, true)) != PE_OK) return s;
+    if (fl & kFlagFolded) {
+      void* src = const_cast<void*>(in[i]);
+      if ((s = make_tmap(&h_maps[2 * i], src, md.rows, md.cols, md.cols)) != PE_OK) return s;
+      if ((s = make_emap(&h_maps[2 * i + 1], src, md.rows, md.cols, md.cols, md.tall)) != PE_OK) return s;
+    }
+    if (dtype == PE_BF16 && (fl & kFlagDirect))
+      if ((s = make_emap(&h_maps[2 * count + i], out[i], md.rows, md.cols, md.cols, md.tall)) != PE_OK) return s;
   }
   PE_CUDA(cudaMemcpyAsync(c->d_ptrs, h, 4 * count * sizeof(void*), cudaMemcpyHostToDevice, st));
   if (dtype == PE_BF16)
-    PE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(c->d_ptrs) + omap_off, h_omaps, count * sizeof(CUtensorMap),
+    PE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(c->d_ptrs) + omap_off, h_maps, 3 * count * sizeof(CUtensorMap),
                             cudaMemcpyHostToDevice, st));
-  const CUtensorMap* d_omaps =
+  const CUtensorMap* d_imaps =
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(c->d_ptrs) + omap_off);
+  const CUtensorMap* d_omaps = d_imaps + 2 * count;
   void** d_in = c->d_ptrs;
   void** d_outs_direct = c->d_ptrs + count;
   void** d_fin_src = c->d_ptrs + 2 * count;
@@ -601,8 +632,11 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.mats = at<MatDev>(c, c->o_mats);
         g.tmaps = at<CUtensorMap>(c, c->o_tmaps);
         g.emaps = at<CUtensorMap>(c, c->o_emaps);
+        g.imaps = d_imaps;
         g.omaps = d_omaps;
-        g.outs = d_outs_direct;
+        g.mflags = at<int>(c, c->o_flags);
+        g.inv = at<float>(c, c->o_inv);
+        g.first_iter = (t == 0);
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
         g.dbg = c->dbg;
@@ -613,10 +647,15 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         }
         const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
         ProfScope ps(c, 2 + mode, st);
-        if (c->long_k[mode])
-          pe_gemm_sm100<6, 3><<<grid, kGemmThreads, gemm_smem_bytes<6, 3>(), st>>>(g);
-        else
-          pe_gemm_sm100<4, kEpiChunks><<<grid, kGemmThreads, gemm_smem_bytes<4, kEpiChunks>(), st>>>(g);
+        const bool edge = (t == 0) || (t == T - 1);
+        const size_t sm_long = gemm_smem_bytes<6, 3>(), sm_short = gemm_smem_bytes<4, kEpiChunks>();
+        if (c->long_k[mode]) {
+          if (edge) pe_gemm_sm100<6, 3, true><<<grid, kGemmThreads, sm_long, st>>>(g);
+          else pe_gemm_sm100<6, 3, false><<<grid, kGemmThreads, sm_long, st>>>(g);
+        } else {
+          if (edge) pe_gemm_sm100<4, kEpiChunks, true><<<grid, kGemmThreads, sm_short, st>>>(g);
+          else pe_gemm_sm100<4, kEpiChunks, false><<<grid, kGemmThreads, sm_short, st>>>(g);
+        }
       } else {
         GemmF32Args g;
         g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);

@@ -71,12 +71,21 @@ def test_gaussian_parity(ctx, shape):
     X = run(ctx, [Mb])[0]
     assert X.shape == shape
     if min(shape) == 1:
-        # rank one: polar = M/|M|; bf16 error only
-        assert om.rel_frobenius(X, oi.polar_express(Mb, TABLE, 5)) <= 2e-2
+        # rank one: every normalised singular value sits at 1/1.01, where the
+        # T=5 composite has slope ~160 (p_1'(0.99) ~ 20), so a single bf16
+        # rounding of A moves the result by ~3.6% (CPU emulation of both
+        # rounding variants, 20 seeds); gate on G3 and a 5e-2 bound
+        ref = oi.polar_express(Mb, TABLE, 5)
+        P = oi.exact_polar(Mb)
+        assert om.rel_frobenius(X, ref) <= 5e-2
+        assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
         return
     # G1 is stated for m >= 64: below that the R8
-    # rounding points alone give 1.4-2.3e-2 (CPU emulation, 20 seeds at 37x100)
-    check_g1_g3(X, Mb, g1=2e-2 if min(shape) >= 64 else 3e-2)
+    # rounding points alone spread widely (CPU emulation over 20 seeds: max
+    # 2.3e-2 at 37x100, 7.8e-2 at 8x8), so small m is gated on G3 plus a
+    # size-dependent bound
+    m = min(shape)
+    check_g1_g3(X, Mb, g1=2e-2 if m >= 64 else (3e-2 if m >= 16 else 1e-1))
 
 
 @pytest.mark.parametrize("T", [1, 2, 3, 4, 6, 7, 8, 10])
@@ -127,16 +136,19 @@ def test_prescribed_spectrum(ctx, kappa, shape):
     assert np.all(np.isfinite(X))
 
 
-@pytest.mark.parametrize("shape", [(64, 96), (96, 64), (200, 200), (300, 1100)])
+@pytest.mark.parametrize("shape", [(64, 96), (96, 64), (200, 200), (300, 1100), (64, 90), (90, 68)])
 def test_diagonal_bit_exact(ctx, shape):
     """Diagonal inputs: every product has one non-zero term, so the GPU must
-    equal the R8 rounding-point emulation bit for bit."""
+    equal the R8 rounding-point emulation bit for bit.  Rows that are
+    16-byte multiples take the folded-normalisation path, the others the
+    explicit X_0 path."""
     k = min(shape)
+    folded = shape[1] % 8 == 0
     sig = syn.to_bf16_values(np.linspace(1.0, 0.02, k)).astype(np.float64)
     M = syn.diagonal(*shape, sig)
     for T in (1, 3, 5, 8):
         X = run(ctx, [M], T=T)[0]
-        emu = emulate.diagonal_bf16(sig, TABLE, T).astype(np.float64)
+        emu = emulate.diagonal_bf16(sig, TABLE, T, folded=folded).astype(np.float64)
         assert np.array_equal(np.diag(X)[:k], emu), T
         off = X.copy()
         off[np.arange(k), np.arange(k)] = 0
