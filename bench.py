@@ -154,6 +154,7 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
                 "peak": peak, "peak_source": f"{src} {'sustained' if (sustained and kind in fl) else 'burst'}",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "launch_ms": round(per_launch_ms, 4),
+                "timing": "CUDA events around each launch of this kernel, on its stream, in a second pass of the same K steps",
                 "share_of_step": round(tot / max(sum(v[0] for v in prof.values()), 1e-9), 4)})
     return out
 
@@ -242,22 +243,30 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         step()
     torch.cuda.synchronize(device)
     launches = ctx.last_launch_count()
-    if dist_on:
-        torch.distributed.barrier()
-    torch.cuda.synchronize(device)
-    ctx.profile_enable(True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for k in range(steps):
-        flush.zero_()                    # evict L2 (buffer > 126 MB) between timed steps
-        evs[k][0].record(stream)
-        step()
-        evs[k][1].record(stream)
-    torch.cuda.synchronize(device)
-    if dist_on:
-        torch.distributed.barrier()
-    prof = ctx.profile_read()
-    ctx.profile_enable(False)
-    ms = [a.elapsed_time(b) for a, b in evs]
+
+    def timed(profile):
+        if dist_on:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(device)
+        ctx.profile_enable(profile)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            flush.zero_()                    # evict L2 (buffer > 126 MB) between timed steps
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(device)
+        if dist_on:
+            torch.distributed.barrier()
+        prof = ctx.profile_read() if profile else None
+        ctx.profile_enable(False)
+        return [a.elapsed_time(b) for a, b in evs], prof
+
+    # headline: no per-launch events inside the step (they would break the
+    # programmatic-dependent-launch overlap between kernels); a second pass
+    # with per-launch events gives the per-kernel split and the roofline
+    ms, _ = timed(False)
+    _, prof = timed(True)
     return ms, prof, launches, idx, xs, ys
 
 

@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include "pe_types.h"
+#include "ptx.cuh"
 
 namespace pe {
 
@@ -43,6 +44,8 @@ __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
 }
 
 __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int blk = blockIdx.x;
   const int mat = a.chunk_mat[blk];
   const int ci = a.chunk_idx[blk];
@@ -170,6 +173,8 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float
 // dst[r][c] = scale * src[r][c] for the rows of each item.
 template <typename T>
 __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = VecT<T>::N;
   for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
     const CopyItem ci = a.items[it];
@@ -210,6 +215,8 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
 // dst (cols x rows) = (scale * src)^T, 64x64 tiles, 256 threads.
 template <typename T>
 __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = VecT<T>::N;                 // elements per 16-byte vector
   constexpr int VPR = 64 / V;                   // vectors per 64-element tile row
   __shared__ float tile[64][65];

@@ -6,6 +6,7 @@
 // Symmetric modes compute only tiles with tn >= tm and mirror-store.
 #pragma once
 #include "pe_types.h"
+#include "ptx.cuh"
 
 namespace pe {
 
@@ -19,6 +20,8 @@ struct GemmF32Args {
 };
 
 __global__ void __launch_bounds__(256) pe_gemm_f32(const GemmF32Args g) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;

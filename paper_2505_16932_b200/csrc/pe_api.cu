@@ -21,6 +21,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "elementwise.cuh"
@@ -61,6 +62,25 @@ EncodeTiledFn get_encode_fn() {
 }
 
 inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Every launch is programmatic (PDL): the kernel's prologue overlaps the tail
+// of the previous kernel in the stream; each kernel calls griddepcontrol.wait
+// before touching memory (see ptx.cuh pdl_wait).  PE_NO_PDL=1 disables it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool pdl = getenv("PE_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // Append host arrays into one device blob.
@@ -589,7 +609,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   na.inv = at<float>(c, c->o_inv);
   na.src_f32 = src_f32;
   { ProfScope ps(c, 0, st);
-    pe_norm_kernel<<<c->n_chunks, kNormThreads, 0, st>>>(na); }
+    launch(pe_norm_kernel, c->n_chunks, kNormThreads, 0, st, na); }
   ++launches;
 
   // 2) X_0 = M / s (oriented)
@@ -606,11 +626,11 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     ProfScope ps(c, fin ? 5 : 1, st);
     const bool tr = (k == 1 || k == 2);
     if (dtype == PE_BF16) {
-      if (tr) pe_transpose_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(ca);
-      else pe_rows_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(ca);
+      if (tr) launch(pe_transpose_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
+      else launch(pe_rows_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
     } else {
-      if (tr) pe_transpose_kernel<float><<<grid, 256, 0, st>>>(ca);
-      else pe_rows_kernel<float><<<grid, 256, 0, st>>>(ca);
+      if (tr) launch(pe_transpose_kernel<float>, grid, 256, 0, st, ca);
+      else launch(pe_rows_kernel<float>, grid, 256, 0, st, ca);
     }
     ++launches;
   };
@@ -650,11 +670,11 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         const bool edge = (t == 0) || (t == T - 1);
         const size_t sm_long = gemm_smem_bytes<6, 3>(), sm_short = gemm_smem_bytes<4, kEpiChunks>();
         if (c->long_k[mode]) {
-          if (edge) pe_gemm_sm100<6, 3, true><<<grid, kGemmThreads, sm_long, st>>>(g);
-          else pe_gemm_sm100<6, 3, false><<<grid, kGemmThreads, sm_long, st>>>(g);
+          if (edge) launch(pe_gemm_sm100<6, 3, true>, grid, kGemmThreads, sm_long, st, g);
+          else launch(pe_gemm_sm100<6, 3, false>, grid, kGemmThreads, sm_long, st, g);
         } else {
-          if (edge) pe_gemm_sm100<4, kEpiChunks, true><<<grid, kGemmThreads, sm_short, st>>>(g);
-          else pe_gemm_sm100<4, kEpiChunks, false><<<grid, kGemmThreads, sm_short, st>>>(g);
+          if (edge) launch(pe_gemm_sm100<4, kEpiChunks, true>, grid, kGemmThreads, sm_short, st, g);
+          else launch(pe_gemm_sm100<4, kEpiChunks, false>, grid, kGemmThreads, sm_short, st, g);
         }
       } else {
         GemmF32Args g;
@@ -666,7 +686,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         g.a = fa; g.b = fb; g.c = fc;
         const int grid = std::min(g.ntiles, c->num_sms * 4);
         ProfScope ps(c, 2 + mode, st);
-        pe_gemm_f32<<<grid, 256, 0, st>>>(g);
+        launch(pe_gemm_f32, grid, 256, 0, st, g);
       }
       ++launches;
     }
