@@ -190,6 +190,7 @@ class Context:
         ``outputs`` defaults to new tensors; pass ``inputs`` for in-place."""
         import torch
         if len(inputs) == 0:
+            _check(lib().pe_polar(self._h, None, None, None, 0, int(iters), PE_BF16, None), "pe_polar")
             return []
         dt = _dtype_code(inputs[0])
         if outputs is None:

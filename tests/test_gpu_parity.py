@@ -230,3 +230,89 @@ def test_full_gpt2_small_set_sampled(ctx):
     outs = run(ctx, mats)
     for i in (0, 4, 5, 37, 71):
         check_g1_g3(outs[i], mats[i])
+
+
+def test_empty_batch_and_single_rows(ctx):
+    """Degenerate batches: no matrices (no launch), 1 x n and n x 1 rows in a
+    mixed batch with a zero matrix (R9)."""
+    assert ctx.polar([], iters=5) == []
+    assert ctx.last_launch_count() == 0
+    mats = [bf16_values(syn.gaussian(1, 40, seed=1, std=0.02)), np.zeros((16, 24)),
+            bf16_values(syn.gaussian(40, 1, seed=2, std=0.02))]
+    X = run(ctx, mats)
+    for Xi, M in zip(X, mats):
+        assert np.all(np.isfinite(Xi))
+        if not M.any():
+            assert np.all(Xi == 0)
+        else:
+            P = oi.exact_polar(M)     # rank one: M / |M|
+            ref = oi.polar_express(M, TABLE, 5)
+            assert om.rel_frobenius(Xi, P) <= om.rel_frobenius(ref, P) + 1e-2
+
+
+@pytest.mark.slow
+def test_max_size_square_hadamard(ctx):
+    """BASELINE configs[4] upper end: one 16384 x 16384 matrix (sweep max) via
+    the equal-sigma closed form; bf16 tolerance."""
+    n = 16384
+    H = syn.sylvester_hadamard(n)
+    x = to_dev_bf16(H)
+    del H
+    y = ctx.polar([x], iters=5)[0]
+    torch.cuda.synchronize()
+    sh = math.sqrt(n) / (1.01 * n + 1e-7)
+    s = float(oi.composite(sh, TABLE, 5))
+    # compare a sample of rows against s * H / sqrt(n)
+    Hs = syn.sylvester_hadamard(n)[::997]
+    Y = y[::997].float().cpu().numpy().astype(np.float64)
+    assert om.rel_frobenius(Y, s * Hs / math.sqrt(n)) <= 2e-2
+
+
+@pytest.mark.slow
+def test_full_gpt2_large_set_sampled(ctx):
+    """BASELINE configs[2] at full size in the bench launch configuration (one
+    grouped call over all 216 matrices); sampled matrices against the oracle."""
+    shapes = syn.layer_set_shapes("gpt2-large")
+    picks = {0: None, 4: None, 5: None, 100: None, 215: None}
+    xs = []
+    for i, (r, c) in enumerate(shapes):
+        if i in picks:
+            picks[i] = bf16_values(syn.gaussian(r, c, seed=2000 + i, std=0.02))
+            xs.append(to_dev_bf16(picks[i]))
+        else:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(i)
+            xs.append((torch.randn((r, c), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    ys = ctx.polar(xs, iters=5)
+    torch.cuda.synchronize()
+    for i, Mb in picks.items():
+        check_g1_g3(ys[i].float().cpu().numpy().astype(np.float64), Mb)
+
+
+@pytest.mark.slow
+def test_full_llama_set_sampled(ctx):
+    """BASELINE configs[3] (single-GPU share = the whole set) in the bench
+    launch configuration: all 224 Llama-3-8B matrices in one call; layer 0's
+    q_proj (4096^2), k_proj (1024x4096) and gate_proj (14336x4096, tall)
+    against the oracle (G1; G3 where the SVD is affordable)."""
+    shapes = syn.layer_set_shapes("llama3-8b")
+    xs, checks = [], {}
+    for i, (r, c) in enumerate(shapes):
+        if i in (0, 2, 4):
+            M = bf16_values(syn.gaussian(r, c, seed=3000 + i, std=0.02))
+            checks[i] = M
+            xs.append(to_dev_bf16(M))
+        else:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(i)
+            xs.append((torch.randn((r, c), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    ys = ctx.polar(xs, iters=5)
+    torch.cuda.synchronize()
+    for i, M in checks.items():
+        Y = ys[i].float().cpu().numpy().astype(np.float64)
+        if max(M.shape) > 4096:
+            ref = oi.polar_express(M, TABLE, 5)
+            assert np.all(np.isfinite(Y))
+            assert om.rel_frobenius(Y, ref) <= 2e-2
+        else:
+            check_g1_g3(Y, M)
