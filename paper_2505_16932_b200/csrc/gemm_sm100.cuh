@@ -155,66 +155,99 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* f) {
 
 // Mirrored store of a symmetric-output chunk: element (r, c0+j) -> (c0+j, r).
 // Lanes hold consecutive r, so each store instruction writes 64 contiguous bytes.
-__device__ __forceinline__ void mirror_chunk16(__nv_bfloat16* dst, int m, int ld, int r, int c0, const float* w) {
+__device__ __forceinline__ void mirror_chunk32(__nv_bfloat16* dst, int m, int ld, int r, int c0, const float* w) {
   if (r >= m) return;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < 32; ++j) {
     const int c = c0 + j;
     if (c < m) dst[(size_t)c * ld + r] = __float2bfloat16_rn(w[j]);
   }
 }
 
-// Epilogue arithmetic of one 32-row x 16-column chunk (thread = row `lane`):
-// w (fp32 accumulator in) -> w (result), reading the operand chunk from `slot`
-// and writing the bf16 result back into `slot` (row-major [32][16], or
-// [16][32] when the caller's matrix is tall).  Rounding points: reading R8.
+// Epilogue arithmetic of one half (32 columns) of a 32-row x 64-column chunk
+// (thread = row `lane`): w (fp32 accumulator in) -> w (result).  The operand
+// is read from `slot` and the bf16 result written back to `slot`.  Slot
+// layouts: row-major [32][64] with the TMA 128B swizzle (16-byte unit j of
+// row r at r*128 + ((j ^ (r & 7)) * 16)), or -- for the transposed chunks of
+// a tall caller matrix -- [64][32] plain (element (c, r) at c*32 + r).
+// Rounding points: reading R8.
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+
 template <bool kEdge>
 __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& cfg, float inv, uint8_t* slot,
-                                             int lane, float* w) {
-  if (g.mode != kModeGram) {
-    float o[16];
-    if (!(kEdge && cfg.ein_tr)) {
-      const uint4* sp = reinterpret_cast<const uint4*>(slot + lane * 32);
-      bf16x8_to_f32(sp[0], o);
-      bf16x8_to_f32(sp[1], o + 8);
-    } else {
-      const __nv_bfloat16* sp = reinterpret_cast<const __nv_bfloat16*>(slot) + lane;
+                                             int lane, int half32, float* w, const uint32_t* pre) {
+  // pre != nullptr: the operand half was read into packed bf16 pairs before
+  // any result of this chunk was written (mixed layouts, see caller)
+  const bool tr_in = kEdge && cfg.ein_tr;
+  const bool tr_out = kEdge && cfg.eout_tr;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) o[j] = __bfloat162float(sp[j * 32]);
-    }
-    if (g.mode == kModePoly) {
+  for (int qq = 0; qq < 2; ++qq) {           // 16 columns at a time (register pressure)
+    float* wq = w + 16 * qq;
+    if (g.mode != kModeGram) {
+      float o[16];
+      if (kEdge && pre != nullptr) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = __fadd_rn(__fmul_rn(g.b, o[j]), __fmul_rn(g.c, w[j]));
-    } else {
+        for (int j = 0; j < 8; ++j) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pre[qq * 8 + j]));
+          o[2 * j] = f.x;
+          o[2 * j + 1] = f.y;
+        }
+      } else if (!tr_in) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = __fadd_rn(__fmul_rn(g.a, o[j]), w[j]);
-      if (kEdge && cfg.scaled) {
+        for (int v = 0; v < 2; ++v)
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(slot + sw128_off(lane, half32 * 4 + qq * 2 + v)), o + 8 * v);
+      } else {
+        const __nv_bfloat16* sp = reinterpret_cast<const __nv_bfloat16*>(slot) + lane;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) w[j] = __fmul_rn(w[j], inv);
+        for (int j = 0; j < 16; ++j) o[j] = __bfloat162float(sp[(half32 * 32 + qq * 16 + j) * 32]);
       }
+      if (g.mode == kModePoly) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(g.b, o[j]), __fmul_rn(g.c, wq[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(g.a, o[j]), wq[j]);
+        if (kEdge && cfg.scaled) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv);
+        }
+      }
+    } else if (kEdge && cfg.scaled) {
+      const float inv2 = __fmul_rn(inv, inv);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv2);
     }
-  } else if (kEdge && cfg.scaled) {
-    const float inv2 = __fmul_rn(inv, inv);
+    if (!tr_out) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) w[j] = __fmul_rn(w[j], inv2);
-  }
-  if (!(kEdge && cfg.eout_tr)) {
-    uint4* sp = reinterpret_cast<uint4*>(slot + lane * 32);
-    sp[0] = pack8_bf16(w);
-    sp[1] = pack8_bf16(w + 8);
-  } else {
-    __nv_bfloat16* sp = reinterpret_cast<__nv_bfloat16*>(slot) + lane;
+      for (int v = 0; v < 2; ++v)
+        *reinterpret_cast<uint4*>(slot + sw128_off(lane, half32 * 4 + qq * 2 + v)) = pack8_bf16(wq + 8 * v);
+    } else {
+      __nv_bfloat16* sp = reinterpret_cast<__nv_bfloat16*>(slot) + lane;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sp[j * 32] = __float2bfloat16_rn(w[j]);
+      for (int j = 0; j < 16; ++j) sp[(half32 * 32 + qq * 16 + j) * 32] = __float2bfloat16_rn(wq[j]);
+    }
   }
 }
 
-// kSt: smem pipeline stages; kSl: epilogue smem slots per warp.  kSl == 3:
-// operand chunks are prefetched one chunk ahead (deep ring; used for the
-// Gram, which has no epilogue operand); kSl == kEpiChunks: a whole tile's
-// operand chunks are prefetched while the MMA of that tile runs (poly,
-// update), since one chunk of lookahead cannot hide the TMA latency.
-template <int kSt, int kSl, bool kEdge>
+// Operand half (32 values of row `lane`) of a chunk, packed as bf16 pairs.
+template <bool kTr>
+__device__ __forceinline__ void read_operand_half(const uint8_t* slot, int lane, int half32, uint32_t* pre) {
+  if (!kTr) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint4 u = *reinterpret_cast<const uint4*>(slot + sw128_off(lane, half32 * 4 + v));
+      pre[4 * v] = u.x; pre[4 * v + 1] = u.y; pre[4 * v + 2] = u.z; pre[4 * v + 3] = u.w;
+    }
+  } else {
+    const uint16_t* sp = reinterpret_cast<const uint16_t*>(slot) + lane;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      pre[j] = (uint32_t)sp[(half32 * 32 + 2 * j) * 32] | ((uint32_t)sp[(half32 * 32 + 2 * j + 1) * 32] << 16);
+  }
+}
+
+// kSt: smem pipeline stages; kEdge: first/last-iteration specialisation.
+template <int kSt, bool kEdge>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -224,9 +257,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;
   uint64_t* tempty = tfull + 2;
-  uint64_t* xbars = tempty + 2;                              // kEpiWarps x kSl
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbars + kEpiWarps * kSl);
-  uint8_t* epi_smem = smem + kSt * kStageBytes + kBarrierBytes;   // kEpiWarps x kSl x 1 KB
+  uint64_t* xbars = tempty + 2;                              // kEpiWarps x kEpiChunks
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbars + kEpiWarps * kEpiChunks);
+  uint8_t* epi_smem = smem + kSt * kStageBytes + kBarrierBytes;   // kEpiWarps x kEpiChunks x 4 KB
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -247,7 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 2 * kEpiWarps);
     }
-    for (int s = 0; s < kEpiWarps * kSl; ++s) mbar_init(&xbars[s], 1);
+    for (int s = 0; s < kEpiWarps * kEpiChunks; ++s) mbar_init(&xbars[s], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, kTmemCols);
@@ -277,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           const uint32_t bar = full_leader0 + stage * sizeof(uint64_t);
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * kBBytes;
-          const int k0 = kb * kBK;
+          const int k0 = (args.dbg & 8) ? 0 : kb * kBK;   // dbg 8: every load hits the same (L2-resident) boxes
           if (!o.a_mn) {
             tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a);
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, k0, o.row_a + 64);
@@ -349,194 +382,125 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   } else {
     // ------------------------------------------------------------ epilogue
     // Warp ew owns TMEM lane quadrant q (its 32 output rows) and column half
-    // `half` (128 columns) of the CTA's 128 x 256 accumulator, processed as
-    // 16-column chunks through smem slots.
+    // `half` (128 columns) of the CTA's 128 x 256 accumulator: two 32 x 64
+    // chunks, each staged in a 4 KB smem slot (128B-swizzled, so the
+    // row-per-thread accesses are conflict-free).  The whole tile's operand
+    // chunks (A for poly, X for update) are loaded by TMA while the tile's MMA
+    // runs; results leave by TMA store; the mirrored half of a symmetric
+    // output is stored directly (64 contiguous bytes per warp store).
     const int ew = warp - 2;
     const int q = warp & 3;
     const int half = ew >> 2;
-    uint8_t* slots = epi_smem + ew * kSl * kEpiSlotBytes;
-    uint64_t* xbar = xbars + ew * kSl;
+    uint8_t* slots = epi_smem + ew * kEpiChunks * kEpiSlotBytes;
+    uint64_t* xbar = xbars + ew * kEpiChunks;
     const bool need_load = (mode != kModeGram) && !(args.dbg & 3);
     const bool do_work = !(args.dbg & 1);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const int row_off = (int)rank * (kBM / 2) + q * 32;
 
     auto col0 = [&](const Tile& tl2, int kk) { return tl2.tn * kBN + half * (kBN / 2) + kk * kEpiCols; };
-    auto valid = [&](int tt, int kk) -> bool {
-      const Tile tl2 = args.tiles[tt];
+    auto ncols_of = [&](const Tile& tl2) {
       const MatDev& m2 = args.mats[tl2.mat];
-      return col0(tl2, kk) < ((mode == kModeUpdate) ? m2.n : m2.m);
+      return (mode == kModeUpdate) ? m2.n : m2.m;
     };
-    auto issue_load_cfg = [&](const Tile& tl2, const TileCfg& c2, int kk, int slot) {
-      const int r0 = tl2.tm * kBM + row_off, c0 = col0(tl2, kk);
-      mbar_arrive_expect_tx(&xbar[slot], kEpiSlotBytes);
-      if (!(kEdge && c2.ein_tr)) tma_load_2d(slots + slot * kEpiSlotBytes, c2.ein, &xbar[slot], c0, r0);
-      else tma_load_2d(slots + slot * kEpiSlotBytes, c2.ein, &xbar[slot], r0, c0);
-    };
-    auto issue_load = [&](int tt, int kk, int slot) {
-      const Tile tl2 = args.tiles[tt];
-      issue_load_cfg(tl2, tile_cfg<kEdge>(args, tl2, rank), kk, slot);
-    };
-    auto store_chunk = [&](const TileCfg& cfg, int slot, int r0, int c0) {
-      if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + slot * kEpiSlotBytes, c0, r0);
-      else tma_store_2d(cfg.eout, slots + slot * kEpiSlotBytes, r0, c0);
+    auto issue_tile = [&](const Tile& tl2, const TileCfg& c2, int nc) {
+      const int r0 = tl2.tm * kBM + row_off;
+      for (int kk = 0; kk < kEpiChunks && col0(tl2, kk) < nc; ++kk) {
+        const int c0 = col0(tl2, kk);
+        mbar_arrive_expect_tx(&xbar[kk], kEpiSlotBytes);
+        if (!(kEdge && c2.ein_tr)) tma_load_2d(slots + kk * kEpiSlotBytes, c2.ein, &xbar[kk], c0, r0);
+        else tma_load_2d(slots + kk * kEpiSlotBytes, c2.ein, &xbar[kk], r0, c0);
+      }
     };
 
     int acc = 0;
     uint32_t acc_phase = 0;
-    if constexpr (kSl >= kEpiChunks) {
-      // ---- tile-prefetch epilogue: slot k <-> chunk k of the current tile
-      uint32_t phase_bits = 0;
-      auto issue_tile = [&](const Tile& tl2, const TileCfg& c2, int nc) {
-        for (int kk = 0; kk < kEpiChunks && col0(tl2, kk) < nc; ++kk) issue_load_cfg(tl2, c2, kk, kk);
-      };
-      auto ncols_of = [&](const Tile& tl2) {
-        const MatDev& m2 = args.mats[tl2.mat];
-        return (mode == kModeUpdate) ? m2.n : m2.m;
-      };
-      Tile ntl{};
-      TileCfg ncfg{};
-      int nnc = 0;
-      if (cid < args.ntiles) {
-        ntl = args.tiles[cid];
+    uint32_t phase_bits = 0;
+    Tile ntl{};
+    TileCfg ncfg{};
+    int nnc = 0;
+    if (cid < args.ntiles) {
+      ntl = args.tiles[cid];
+      ncfg = tile_cfg<kEdge>(args, ntl, rank);
+      nnc = ncols_of(ntl);
+      if (lane == 0 && need_load) issue_tile(ntl, ncfg, nnc);
+    }
+    for (int t = cid; t < args.ntiles; t += ncl) {
+      const Tile tl = ntl;
+      const MatDev md = args.mats[tl.mat];
+      const TileCfg cfg = ncfg;
+      const bool has_next = t + ncl < args.ntiles;
+      if (has_next) {                        // next tile's description, loaded early
+        ntl = args.tiles[t + ncl];
         ncfg = tile_cfg<kEdge>(args, ntl, rank);
         nnc = ncols_of(ntl);
-        if (lane == 0 && need_load) issue_tile(ntl, ncfg, nnc);
       }
-      for (int t = cid; t < args.ntiles; t += ncl) {
-        const Tile tl = ntl;
-        const MatDev md = args.mats[tl.mat];
-        const TileCfg cfg = ncfg;
-        const bool has_next = t + ncl < args.ntiles;
-        if (has_next) {                        // next tile's description, loaded early
-          ntl = args.tiles[t + ncl];
-          ncfg = tile_cfg<kEdge>(args, ntl, rank);
-          nnc = ncols_of(ntl);
-        }
-        const float inv = cfg.scaled ? args.inv[tl.mat] : 1.0f;
-        long long t2 = clock64();
-        mbar_wait(&tfull[acc], acc_phase);
-        st_wait_tfull += clock64() - t2;
-        tc_fence_after();
-        const int r0 = tl.tm * kBM + row_off;
-        const int r = r0 + lane;
-        const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
-        const int ncols = (mode == kModeUpdate) ? md.n : md.m;
-        const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
-        __nv_bfloat16* mdst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
-        int nvalid = 0;
-        float v[32];
+      const float inv = cfg.scaled ? args.inv[tl.mat] : 1.0f;
+      long long t2 = clock64();
+      mbar_wait(&tfull[acc], acc_phase);
+      st_wait_tfull += clock64() - t2;
+      tc_fence_after();
+      const int r0 = tl.tm * kBM + row_off;
+      const int r = r0 + lane;
+      const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
+      const int ncols = (mode == kModeUpdate) ? md.n : md.m;
+      const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
+      __nv_bfloat16* mdst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
+      int nvalid = 0;
 #pragma unroll 1
-        for (int k2 = 0; k2 < kEpiChunks; k2 += 2) {
-          if (col0(tl, k2) >= ncols) break;                 // warp-uniform
-          tmem_ld32(t_row + k2 * kEpiCols, v);
+      for (int k = 0; k < kEpiChunks; ++k) {
+        const int c0 = col0(tl, k);
+        if (c0 >= ncols || !do_work) break;                  // warp-uniform
+        if (need_load) {
+          mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
+          phase_bits ^= 1u << k;
+        }
+        uint8_t* slot = slots + k * kEpiSlotBytes;
+        if (kEdge && need_load && cfg.ein_tr != cfg.eout_tr) {
+          // operand and result layouts differ (tall caller matrix, first or
+          // last iteration): read the whole operand chunk before the in-place
+          // result writes can overwrite any of it
+          uint32_t pre[2][16];
+          if (cfg.ein_tr) { read_operand_half<true>(slot, lane, 0, pre[0]); read_operand_half<true>(slot, lane, 1, pre[1]); }
+          else { read_operand_half<false>(slot, lane, 0, pre[0]); read_operand_half<false>(slot, lane, 1, pre[1]); }
+          __syncwarp();
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int k = k2 + h2;
-            const int c0 = col0(tl, k);
-            if (c0 < ncols && do_work) {
-              if (need_load) {
-                mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
-                phase_bits ^= 1u << k;
-              }
-              float w[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) w[j] = v[h2 * 16 + j];
-              epilogue_math<kEdge>(args, cfg, inv, slots + k * kEpiSlotBytes, lane, w);
-              if (mirror) mirror_chunk16(mdst, md.m, md.ldm, r, c0, w);
-              ++nvalid;
+          for (int h = 0; h < 2; ++h) {
+            if (c0 + 32 * h < ncols) {
+              float w[32];
+              tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+              epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, pre[h]);
             }
           }
-        }
-        // one proxy fence and one bulk group for the whole tile
-        fence_async_smem();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-          for (int k = 0; k < nvalid; ++k) store_chunk(cfg, k, r0, col0(tl, k));
-          bulk_commit();
-          bulk_wait_read<0>();          // this tile's stores have left smem: slots are free
-          if (has_next && need_load) issue_tile(ntl, ncfg, nnc);
-        }
-        __syncwarp();
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-      }
-    } else {
-      // ---- chunk-prefetch epilogue: kSl-slot ring, one chunk of lookahead
-      auto advance = [&](int& tt, int& kk) {
-        while (tt < args.ntiles) {
-          if (kk < kEpiChunks && valid(tt, kk)) return;
-          tt += ncl;
-          kk = 0;
-        }
-      };
-      int pt = cid, pk = 0;          // next chunk to prefetch
-      advance(pt, pk);
-      if (need_load && lane == 0 && pt < args.ntiles) issue_load(pt, pk, 0);
-      ++pk;
-      advance(pt, pk);
-      int g = 0;                     // chunks processed by this warp
-      for (int t = cid; t < args.ntiles; t += ncl) {
-        const Tile tl = args.tiles[t];
-        const MatDev md = args.mats[tl.mat];
-        const TileCfg cfg = tile_cfg<kEdge>(args, tl, rank);
-        const float inv = cfg.scaled ? args.inv[tl.mat] : 1.0f;
-        long long t2 = clock64();
-        mbar_wait(&tfull[acc], acc_phase);
-        st_wait_tfull += clock64() - t2;
-        tc_fence_after();
-        const int r0 = tl.tm * kBM + row_off;
-        const int r = r0 + lane;
-        const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
-        const int ncols = (mode == kModeUpdate) ? md.n : md.m;
-        const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
-        __nv_bfloat16* mdst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
-        float v[32];
+        } else {
 #pragma unroll 1
-        for (int k2 = 0; k2 < kEpiChunks; k2 += 2) {
-          if (col0(tl, k2) >= ncols) break;                 // warp-uniform
-          tmem_ld32(t_row + k2 * kEpiCols, v);
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int k = k2 + h2;
-            const int c0 = col0(tl, k);
-            if (c0 < ncols && do_work) {
-              const int slot = g % kSl;
-              if (need_load) {
-                if (lane == 0) {
-                  bulk_wait_read<1>();                  // slot of chunk g+1 (last used by g-2) is free
-                  if (pt < args.ntiles) issue_load(pt, pk, (g + 1) % kSl);
-                }
-                ++pk;
-                advance(pt, pk);
-                mbar_wait(&xbar[slot], (uint32_t)((g / kSl) & 1));
-              } else {
-                if (lane == 0) bulk_wait_read<kSl - 1>();   // slot g%kSl (last used by g-kSl) is free
-                __syncwarp();
-              }
-              float w[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) w[j] = v[h2 * 16 + j];
-              epilogue_math<kEdge>(args, cfg, inv, slots + slot * kEpiSlotBytes, lane, w);
-              if (mirror) mirror_chunk16(mdst, md.m, md.ldm, r, c0, w);
-              fence_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                store_chunk(cfg, slot, r0, c0);
-                bulk_commit();
-              }
-              ++g;
-            }
+          for (int h = 0; h < 2; ++h) {
+            if (c0 + 32 * h >= ncols) break;
+            float w[32];
+            tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+            epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr);
+            if (mirror) mirror_chunk32(mdst, md.m, md.ldm, r, c0 + 32 * h, w);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        ++nvalid;
       }
+      // one proxy fence and one bulk group for the whole tile
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
+        for (int k = 0; k < nvalid; ++k) {
+          if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
+          else tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, r0, col0(tl, k));
+        }
+        bulk_commit();
+        bulk_wait_read<0>();          // this tile's stores have left smem: slots are free
+        if (has_next && need_load) issue_tile(ntl, ncfg, nnc);
+      }
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -552,8 +516,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   }
 }
 
-template <int kSt, int kSl> constexpr size_t gemm_smem_bytes() {
-  return 1024 + (size_t)kSt * kStageBytes + kBarrierBytes + (size_t)kEpiWarps * kSl * kEpiSlotBytes;
+template <int kSt> constexpr size_t gemm_smem_bytes() {
+  return 1024 + (size_t)kSt * kStageBytes + kBarrierBytes + (size_t)kEpiWarps * kEpiChunks * kEpiSlotBytes;
 }
 
 }  // namespace pe

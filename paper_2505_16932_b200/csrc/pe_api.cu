@@ -32,6 +32,17 @@
 
 using namespace pe;
 
+// smem ring depths of the two GEMM instantiations (gemm_smem_bytes must stay
+// below the 227 KB per-CTA limit: 5 x 32 KB ring + 64 KB epilogue slots)
+#ifndef PE_LONG_STAGES
+#define PE_LONG_STAGES 5
+#endif
+#ifndef PE_SHORT_STAGES
+#define PE_SHORT_STAGES 4
+#endif
+constexpr int kLongStages = PE_LONG_STAGES;
+constexpr int kShortStages = PE_SHORT_STAGES;
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -235,14 +246,14 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
     return PE_ERR_UNSUPPORTED;
   }
   PE_CUDA(cudaSetDevice(device));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<6, 3>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<6, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<6, 3>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<4, kEpiChunks>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<4, kEpiChunks, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<4, kEpiChunks>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kShortStages>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kShortStages>()));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -322,9 +333,11 @@ static pe_status make_tmap(CUtensorMap* map, void* base, int rows, int cols, int
   }
   return PE_OK;
 }
+// Epilogue chunk maps: 64 columns x 32 rows with the 128B swizzle, or the
+// transposed 32 x 64 chunk (tall caller matrices) without swizzle.
 static pe_status make_emap(CUtensorMap* map, void* base, int rows, int cols, int ld, bool transposed = false) {
   return transposed ? make_tmap(map, base, rows, cols, ld, 32, kEpiCols, false)
-                    : make_tmap(map, base, rows, cols, ld, kEpiCols, 32, false);
+                    : make_tmap(map, base, rows, cols, ld, kEpiCols, 32, true);
 }
 
 static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
@@ -510,15 +523,11 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   c->mats = mats;
   c->count = count;
   // kernel variant per mode (measured on B200, profiles/r1_variants.md): the
-  // Gram has no epilogue operand, so it takes the deep 6-stage ring; poly and
-  // update take the tile-prefetch epilogue (4 stages + 8 operand slots/warp).
+  // 5-stage instantiation for every phase; PE_GEMM_VARIANT=short selects the
+  // 4-stage one (A/B experiments).
   {
     const char* ov = getenv("PE_GEMM_VARIANT");
-    for (int mode = 0; mode < 3; ++mode) {
-      c->long_k[mode] = (mode == kModeGram);
-      if (ov && !strcmp(ov, "long")) c->long_k[mode] = true;
-      if (ov && !strcmp(ov, "short")) c->long_k[mode] = false;
-    }
+    for (int mode = 0; mode < 3; ++mode) c->long_k[mode] = !(ov && !strcmp(ov, "short"));
   }
   c->n_sym = (int)sym.size();
   c->n_upd = (int)upd.size();
@@ -668,13 +677,13 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
         ProfScope ps(c, 2 + mode, st);
         const bool edge = (t == 0) || (t == T - 1);
-        const size_t sm_long = gemm_smem_bytes<6, 3>(), sm_short = gemm_smem_bytes<4, kEpiChunks>();
+        const size_t sm_long = gemm_smem_bytes<kLongStages>(), sm_short = gemm_smem_bytes<kShortStages>();
         if (c->long_k[mode]) {
-          if (edge) launch(pe_gemm_sm100<6, 3, true>, grid, kGemmThreads, sm_long, st, g);
-          else launch(pe_gemm_sm100<6, 3, false>, grid, kGemmThreads, sm_long, st, g);
+          if (edge) launch(pe_gemm_sm100<kLongStages, true>, grid, kGemmThreads, sm_long, st, g);
+          else launch(pe_gemm_sm100<kLongStages, false>, grid, kGemmThreads, sm_long, st, g);
         } else {
-          if (edge) launch(pe_gemm_sm100<4, kEpiChunks, true>, grid, kGemmThreads, sm_short, st, g);
-          else launch(pe_gemm_sm100<4, kEpiChunks, false>, grid, kGemmThreads, sm_short, st, g);
+          if (edge) launch(pe_gemm_sm100<kShortStages, true>, grid, kGemmThreads, sm_short, st, g);
+          else launch(pe_gemm_sm100<kShortStages, false>, grid, kGemmThreads, sm_short, st, g);
         }
       } else {
         GemmF32Args g;

@@ -18,9 +18,9 @@ constexpr int kStageBytes = kABytes + kBBytes;         // 32 KB per CTA
 constexpr int kEpiWarps = 8;                           // 4 lane quadrants x 2 column halves
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;      // TMA warp, MMA warp, epilogue warps
 constexpr int kTmemCols = 512;                         // 2 x 256-column fp32 accumulators
-constexpr int kEpiCols = 16;                           // epilogue chunk: 32 rows x 16 columns
-constexpr int kEpiChunks = (kBN / 2) / kEpiCols;       // chunks per warp per tile
-constexpr int kEpiSlotBytes = 32 * kEpiCols * 2;       // 1 KB
+constexpr int kEpiCols = 64;                           // epilogue chunk: 32 rows x 64 columns (128B rows)
+constexpr int kEpiChunks = (kBN / 2) / kEpiCols;       // chunks (= smem slots) per warp per tile
+constexpr int kEpiSlotBytes = 32 * kEpiCols * 2;       // 4 KB
 constexpr int kBarrierBytes = 1024;                    // mbarriers + TMEM slot (rounded up)
 
 constexpr int kModeGram = 0;    // A   = X X^T
