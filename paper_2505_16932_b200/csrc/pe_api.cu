@@ -8,9 +8,13 @@
 //         pe_gemm_sm100 Update          X = a X + B X }
 //   pe_copy_kernel (tall inputs only)    transpose back
 //
-// Every launch covers the whole batch (grouped scheduling).  The plan (tile
-// lists, tensor maps, workspace carve-up) depends only on the shapes and is
-// cached between calls with the same shape list.
+// Every launch covers the whole batch (grouped scheduling).  A plan (tile
+// lists, tensor maps, workspace carve-up) depends only on the shape list; the
+// context caches the last few plans, all carving the same workspace (their
+// kernels are stream-ordered).  Per-call data (caller pointers and tensor
+// maps) goes through a small ring of pinned upload buffers, each guarded by
+// an event, so back-to-back asynchronous calls never overwrite an upload the
+// GPU has not consumed yet.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -110,24 +114,14 @@ struct Blob {
 
 }  // namespace
 
-struct pe_ctx_s {
-  int device = 0;
-  int num_sms = 148;
-  std::vector<double> table;   // ntab * nq
-  int degree = 5;
-  int ntab = 0;
-
-  // workspace
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
-
-  // plan
-  bool plan_valid = false;
-  std::vector<int64_t> plan_shapes;
-  pe_dtype plan_dtype = PE_BF16;
+// One cached plan: the device-side description of a shape list.
+struct Plan {
+  std::vector<int64_t> key;     // shapes
+  pe_dtype dtype = PE_BF16;
   int count = 0;
   std::vector<MatDev> mats;
-  void* meta = nullptr;        // device blob
+  std::vector<int> flags;       // per matrix kFlag* (folded input, tall, direct output)
+  void* meta = nullptr;         // device blob
   size_t meta_bytes = 0;
   // offsets into meta
   size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0;
@@ -137,20 +131,47 @@ struct pe_ctx_s {
   size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_flags = 0, o_it[4] = {0, 0, 0, 0};
   int n_it[4] = {0, 0, 0, 0};
   int n_sym = 0, n_upd = 0, n_chunks = 0;
-  bool long_k[3] = {true, true, true};   // per GEMM mode: deep-ring variant (else tile-prefetch epilogue)
+  bool long_k[3] = {true, true, true};   // per GEMM mode: 5-stage (else 4-stage) instantiation
+  size_t ws_needed = 0;
+  uint64_t last_use = 0;
+};
 
-  // per-call pointer arrays + caller-output tensor maps (device + pinned host staging)
-  void** d_ptrs = nullptr;
-  void** h_ptrs = nullptr;
-  int ptr_cap = 0;
-  std::vector<int> flags;        // per matrix kFlag* (folded input, tall, direct output)
+// One pinned upload buffer of the per-call ring.
+struct CallSlot {
+  void* h = nullptr;            // pinned host
+  void* d = nullptr;            // device
+  size_t bytes = 0;
+  cudaEvent_t done = nullptr;   // recorded after the upload on the call's stream
+  bool armed = false;
+};
 
-  // e2e staging
+constexpr int kMaxPlans = 8;
+constexpr int kCallSlots = 4;
+
+struct pe_ctx_s {
+  int device = 0;
+  int num_sms = 148;
+  std::vector<double> table;   // ntab * nq
+  int degree = 5;
+  int ntab = 0;
+
+  // workspace shared by every cached plan
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::vector<Plan*> plans;
+  uint64_t use_clock = 0;
+
+  CallSlot calls[kCallSlots];
+  int next_call = 0;
+
+  // pe_polar_host: staging + copy streams
   void* staging = nullptr;
   size_t staging_bytes = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> host_ev;
 
   int last_launches = 0;
-  int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1 are set)
+  int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1/3 are set)
   long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
 
   // profiling
@@ -160,6 +181,11 @@ struct pe_ctx_s {
   struct Pending { int kind; cudaEvent_t a, b; };
   std::vector<Pending> pending;
 };
+
+static void free_plan(Plan* p) {
+  if (p->meta) cudaFree(p->meta);
+  delete p;
+}
 
 namespace {
 cudaEvent_t take_event(pe_ctx c) {
@@ -276,11 +302,18 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   if (c->ws) cudaFree(c->ws);
-  if (c->meta) cudaFree(c->meta);
-  if (c->d_ptrs) cudaFree(c->d_ptrs);
-  if (c->h_ptrs) cudaFreeHost(c->h_ptrs);
+  for (Plan* p : c->plans) free_plan(p);
+  for (CallSlot& cs : c->calls) {
+    if (cs.d) cudaFree(cs.d);
+    if (cs.h) cudaFreeHost(cs.h);
+    if (cs.done) cudaEventDestroy(cs.done);
+  }
   if (c->staging) cudaFree(c->staging);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  for (auto e : c->host_ev) cudaEventDestroy(e);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->stats) cudaFree(c->stats);
   delete c;
   return PE_OK;
 }
@@ -340,28 +373,38 @@ static pe_status make_emap(CUtensorMap* map, void* base, int rows, int cols, int
                     : make_tmap(map, base, rows, cols, ld, kEpiCols, 32, true);
 }
 
+// Grow the shared workspace; every cached plan points into it, so growth
+// drops the cache (after the device has finished with it).
 static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
   if (bytes <= c->ws_bytes) return PE_OK;
-  if (c->ws) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->ws); c->ws = nullptr; c->ws_bytes = 0; }
+  PE_CUDA(cudaDeviceSynchronize());
+  for (Plan* p : c->plans) free_plan(p);
+  c->plans.clear();
+  if (c->ws) { cudaFree(c->ws); c->ws = nullptr; c->ws_bytes = 0; }
   if (cudaMalloc(&c->ws, bytes) != cudaSuccess) {
     cudaGetLastError();
     g_last_error = "workspace allocation of " + std::to_string(bytes) + " bytes failed";
     return PE_ERR_WORKSPACE;
   }
   c->ws_bytes = bytes;
-  c->plan_valid = false;
   return PE_OK;
 }
 
-// per-call upload: 4*cap pointers, then cap caller-output tensor maps
-// per-call upload: 4*cap pointers, then 3 tensor maps per matrix (caller input
-// main loop, caller input epilogue chunk, caller output epilogue chunk)
-static size_t call_bytes(int cap) { return rup((size_t)4 * cap * sizeof(void*), 128) + (size_t)3 * cap * sizeof(CUtensorMap); }
+// per-call upload: 4*count pointers, then 3 tensor maps per matrix (caller
+// input main loop, caller input epilogue chunk, caller output epilogue chunk)
+static size_t call_ptr_bytes(int count) { return rup((size_t)4 * count * sizeof(void*), 128); }
+static size_t call_bytes(int count) { return call_ptr_bytes(count) + (size_t)3 * count * sizeof(CUtensorMap); }
 
-static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
+static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
-  if (c->plan_valid && c->plan_dtype == dtype && key == c->plan_shapes) return PE_OK;
+  for (Plan* p : c->plans)
+    if (p->dtype == dtype && p->key == key) {
+      p->last_use = ++c->use_clock;
+      *out = p;
+      return PE_OK;
+    }
   const size_t es = (dtype == PE_BF16) ? 2 : 4;
+  Plan* P = nullptr;
 
   // workspace carve-up
   std::vector<MatDev> mats(count);
@@ -385,6 +428,10 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   }
   pe_status s = ensure_workspace(c, std::max<size_t>(total, 256));
   if (s != PE_OK) return s;
+  P = new Plan();
+  P->key = key;
+  P->dtype = dtype;
+  P->ws_needed = total;
   uint8_t* ws = reinterpret_cast<uint8_t*>(c->ws);
   for (int i = 0; i < count; ++i) {
     mats[i].X[0] = ws + offs[4 * i + 0];
@@ -424,14 +471,17 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     emaps.resize(4 * (size_t)count);
     for (int i = 0; i < count; ++i) {
       const MatDev& md = mats[i];
-      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
-      if ((s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
-      if ((s = make_emap(&emaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_emap(&emaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK) return s;
-      if ((s = make_emap(&emaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK) return s;
-      if ((s = make_emap(&emaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) return s;
+      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
+          (s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
+          (s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK ||
+          (s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK ||
+          (s = make_emap(&emaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
+          (s = make_emap(&emaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
+          (s = make_emap(&emaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK ||
+          (s = make_emap(&emaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) {
+        delete P;
+        return s;
+      }
     }
   }
 
@@ -480,62 +530,63 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   }
 
   Blob bl;
-  c->o_mats = bl.add(mats);
-  c->o_tmaps = bl.add(tmaps, 128);
-  c->o_emaps = bl.add(emaps, 128);
-  c->o_sym = bl.add(sym);
-  c->o_upd = bl.add(upd);
-  for (int k = 0; k < 4; ++k) c->o_it[k] = bl.add(it[k]);
-  c->o_smats = bl.add(smats);
-  c->o_fmats = bl.add(fmats);
-  c->o_x0 = bl.add(x0);
-  c->o_flags = bl.add(mflags);
-  c->o_elems = bl.add(elems);
-  c->o_cmat = bl.add(cmat);
-  c->o_cidx = bl.add(cidx);
-  c->o_nch = bl.add(nch);
+  P->o_mats = bl.add(mats);
+  P->o_tmaps = bl.add(tmaps, 128);
+  P->o_emaps = bl.add(emaps, 128);
+  P->o_sym = bl.add(sym);
+  P->o_upd = bl.add(upd);
+  for (int k = 0; k < 4; ++k) P->o_it[k] = bl.add(it[k]);
+  P->o_smats = bl.add(smats);
+  P->o_fmats = bl.add(fmats);
+  P->o_x0 = bl.add(x0);
+  P->o_flags = bl.add(mflags);
+  P->o_elems = bl.add(elems);
+  P->o_cmat = bl.add(cmat);
+  P->o_cidx = bl.add(cidx);
+  P->o_nch = bl.add(nch);
   std::vector<double> part(cmat.size(), 0.0);
-  c->o_part = bl.add(part);
+  P->o_part = bl.add(part);
   std::vector<unsigned> cnt(count, 0u);
-  c->o_cnt = bl.add(cnt);
+  P->o_cnt = bl.add(cnt);
   std::vector<float> inv(count, 0.f);
-  c->o_inv = bl.add(inv);
+  P->o_inv = bl.add(inv);
 
-  if (bl.host.size() > c->meta_bytes) {
-    if (c->meta) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->meta); c->meta = nullptr; c->meta_bytes = 0; }
-    if (cudaMalloc(&c->meta, bl.host.size()) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
-    c->meta_bytes = bl.host.size();
+  if (cudaMalloc(&P->meta, bl.host.size()) != cudaSuccess) {
+    cudaGetLastError();
+    delete P;
+    return PE_ERR_WORKSPACE;
   }
-  PE_CUDA(cudaDeviceSynchronize());   // no kernel of a previous plan may still read meta
-  PE_CUDA(cudaMemcpy(c->meta, bl.host.data(), bl.host.size(), cudaMemcpyHostToDevice));
-
-  if (c->ptr_cap < count) {
-    if (c->d_ptrs) { cudaFree(c->d_ptrs); c->d_ptrs = nullptr; }
-    if (c->h_ptrs) { cudaFreeHost(c->h_ptrs); c->h_ptrs = nullptr; }
-    const int cap = std::max(count, 16);
-    const size_t bytes = call_bytes(cap);
-    if (cudaMalloc(&c->d_ptrs, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
-    if (cudaMallocHost(&c->h_ptrs, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
-    c->ptr_cap = cap;
+  P->meta_bytes = bl.host.size();
+  if (cudaMemcpy(P->meta, bl.host.data(), bl.host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    g_last_error = "plan upload failed";
+    free_plan(P);
+    return PE_ERR_CUDA;
   }
-  c->flags = mflags;
-
-  c->mats = mats;
-  c->count = count;
+  P->flags = mflags;
+  P->mats = mats;
+  P->count = count;
   // kernel variant per mode (measured on B200, profiles/r1_variants.md): the
   // 5-stage instantiation for every phase; PE_GEMM_VARIANT=short selects the
   // 4-stage one (A/B experiments).
   {
     const char* ov = getenv("PE_GEMM_VARIANT");
-    for (int mode = 0; mode < 3; ++mode) c->long_k[mode] = !(ov && !strcmp(ov, "short"));
+    for (int mode = 0; mode < 3; ++mode) P->long_k[mode] = !(ov && !strcmp(ov, "short"));
   }
-  c->n_sym = (int)sym.size();
-  c->n_upd = (int)upd.size();
-  for (int k = 0; k < 4; ++k) c->n_it[k] = (int)it[k].size();
-  c->n_chunks = (int)cmat.size();
-  c->plan_shapes = key;
-  c->plan_dtype = dtype;
-  c->plan_valid = true;
+  P->n_sym = (int)sym.size();
+  P->n_upd = (int)upd.size();
+  for (int k = 0; k < 4; ++k) P->n_it[k] = (int)it[k].size();
+  P->n_chunks = (int)cmat.size();
+  // LRU eviction (the evicted plan's kernels may still be queued: sync first)
+  if ((int)c->plans.size() >= kMaxPlans) {
+    auto lru = std::min_element(c->plans.begin(), c->plans.end(),
+                                [](const Plan* a, const Plan* b) { return a->last_use < b->last_use; });
+    PE_CUDA(cudaDeviceSynchronize());
+    free_plan(*lru);
+    c->plans.erase(lru);
+  }
+  P->last_use = ++c->use_clock;
+  c->plans.push_back(P);
+  *out = P;
   return PE_OK;
 }
 
@@ -544,12 +595,36 @@ extern "C" pe_status pe_reserve(pe_ctx c, const int64_t* shapes, int count, pe_d
   pe_status s = validate_shapes(shapes, count);
   if (s != PE_OK) return s;
   PE_CUDA(cudaSetDevice(c->device));
-  return build_plan(c, shapes, count, dtype);
+  Plan* P = nullptr;
+  return build_plan(c, shapes, count, dtype, &P);
 }
 
 // ---------------------------------------------------------------- online
-template <typename T> static T* at(pe_ctx c, size_t off) {
-  return reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(c->meta) + off);
+template <typename T> static T* at(const Plan* p, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(p->meta) + off);
+}
+
+// Next upload buffer of the ring, large enough for `bytes`; waits only if the
+// GPU has not yet consumed this slot's previous upload.
+static pe_status take_call_slot(pe_ctx c, size_t bytes, CallSlot** out) {
+  CallSlot& cs = c->calls[c->next_call];
+  c->next_call = (c->next_call + 1) % kCallSlots;
+  if (cs.armed) PE_CUDA(cudaEventSynchronize(cs.done));
+  cs.armed = false;
+  if (!cs.done) PE_CUDA(cudaEventCreateWithFlags(&cs.done, cudaEventDisableTiming));
+  if (cs.bytes < bytes) {
+    if (cs.d) { cudaFree(cs.d); cs.d = nullptr; }
+    if (cs.h) { cudaFreeHost(cs.h); cs.h = nullptr; }
+    cs.bytes = 0;
+    const size_t nb = std::max<size_t>(bytes, 64 * 1024);
+    if (cudaMalloc(&cs.d, nb) != cudaSuccess || cudaMallocHost(&cs.h, nb) != cudaSuccess) {
+      cudaGetLastError();
+      return PE_ERR_WORKSPACE;
+    }
+    cs.bytes = nb;
+  }
+  *out = &cs;
+  return PE_OK;
 }
 
 extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
@@ -569,18 +644,21 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   PE_CUDA(cudaSetDevice(c->device));
   PE_CUDA(cudaGetLastError());
-  if ((s = build_plan(c, shapes, count, dtype)) != PE_OK) return s;
+  Plan* P = nullptr;
+  if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) return s;
 
-  // per-call pointers: [in | outs_direct | fin_src | out] + caller-output tensor maps
+  // per-call pointers: [in | outs_direct | fin_src | out] + caller tensor maps
   const int T = iters;
   const int xfinal = T & 1;
-  void** h = c->h_ptrs;
-  const size_t omap_off = rup((size_t)4 * c->ptr_cap * sizeof(void*), 128);
+  CallSlot* cs = nullptr;
+  if ((s = take_call_slot(c, call_bytes(count), &cs)) != PE_OK) return s;
+  void** h = reinterpret_cast<void**>(cs->h);
+  const size_t omap_off = call_ptr_bytes(count);
   CUtensorMap* h_maps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
   for (int i = 0; i < count; ++i) {
-    const MatDev& md = c->mats[i];
+    const MatDev& md = P->mats[i];
     h[i] = const_cast<void*>(in[i]);
-    const int fl = c->flags[i];
+    const int fl = P->flags[i];
     h[count + i] = (fl & kFlagDirect) ? out[i] : nullptr;
     h[2 * count + i] = md.X[xfinal];
     h[3 * count + i] = out[i];
@@ -592,46 +670,47 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     if (dtype == PE_BF16 && (fl & kFlagDirect))
       if ((s = make_emap(&h_maps[2 * count + i], out[i], md.rows, md.cols, md.cols, md.tall)) != PE_OK) return s;
   }
-  PE_CUDA(cudaMemcpyAsync(c->d_ptrs, h, 4 * count * sizeof(void*), cudaMemcpyHostToDevice, st));
-  if (dtype == PE_BF16)
-    PE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(c->d_ptrs) + omap_off, h_maps, 3 * count * sizeof(CUtensorMap),
-                            cudaMemcpyHostToDevice, st));
+  PE_CUDA(cudaMemcpyAsync(cs->d, h, dtype == PE_BF16 ? call_bytes(count) : 4 * count * sizeof(void*),
+                          cudaMemcpyHostToDevice, st));
+  PE_CUDA(cudaEventRecord(cs->done, st));
+  cs->armed = true;
+  void** d_ptrs = reinterpret_cast<void**>(cs->d);
   const CUtensorMap* d_imaps =
-      reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(c->d_ptrs) + omap_off);
+      reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
   const CUtensorMap* d_omaps = d_imaps + 2 * count;
-  void** d_in = c->d_ptrs;
-  void** d_outs_direct = c->d_ptrs + count;
-  void** d_fin_src = c->d_ptrs + 2 * count;
-  void** d_out = c->d_ptrs + 3 * count;
+  void** d_in = d_ptrs;
+  void** d_outs_direct = d_ptrs + count;
+  void** d_fin_src = d_ptrs + 2 * count;
+  void** d_out = d_ptrs + 3 * count;
   const int src_f32 = (dtype == PE_FP32);
   int launches = 0;
 
   // 1) norm
   NormArgs na;
   na.srcs = d_in;
-  na.elems = at<int64_t>(c, c->o_elems);
-  na.chunk_mat = at<int>(c, c->o_cmat);
-  na.chunk_idx = at<int>(c, c->o_cidx);
-  na.nchunks = at<int>(c, c->o_nch);
-  na.partials = at<double>(c, c->o_part);
-  na.counters = at<unsigned>(c, c->o_cnt);
-  na.inv = at<float>(c, c->o_inv);
+  na.elems = at<int64_t>(P, P->o_elems);
+  na.chunk_mat = at<int>(P, P->o_cmat);
+  na.chunk_idx = at<int>(P, P->o_cidx);
+  na.nchunks = at<int>(P, P->o_nch);
+  na.partials = at<double>(P, P->o_part);
+  na.counters = at<unsigned>(P, P->o_cnt);
+  na.inv = at<float>(P, P->o_inv);
   na.src_f32 = src_f32;
   { ProfScope ps(c, 0, st);
-    launch(pe_norm_kernel, c->n_chunks, kNormThreads, 0, st, na); }
+    launch(pe_norm_kernel, P->n_chunks, kNormThreads, 0, st, na); }
   ++launches;
 
   // 2) X_0 = M / s (oriented)
   auto copy_pass = [&](int k, bool scale, bool fin) {
-    if (c->n_it[k] == 0) return;
+    if (P->n_it[k] == 0) return;
     CopyArgs ca;
-    ca.items = at<CopyItem>(c, c->o_it[k]);
-    ca.nitems = c->n_it[k];
-    ca.mats = at<CopyMat>(c, fin ? c->o_fmats : c->o_smats);
+    ca.items = at<CopyItem>(P, P->o_it[k]);
+    ca.nitems = P->n_it[k];
+    ca.mats = at<CopyMat>(P, fin ? P->o_fmats : P->o_smats);
     ca.srcs = fin ? d_fin_src : d_in;
-    ca.dsts = fin ? d_out : at<void*>(c, c->o_x0);
-    ca.scale = scale ? at<float>(c, c->o_inv) : nullptr;
-    const int grid = std::min(c->n_it[k], c->num_sms * 8);
+    ca.dsts = fin ? d_out : at<void*>(P, P->o_x0);
+    ca.scale = scale ? at<float>(P, P->o_inv) : nullptr;
+    const int grid = std::min(P->n_it[k], c->num_sms * 8);
     ProfScope ps(c, fin ? 5 : 1, st);
     const bool tr = (k == 1 || k == 2);
     if (dtype == PE_BF16) {
@@ -656,15 +735,15 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
       if (dtype == PE_BF16) {
         GemmArgs g;
-        g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);
-        g.ntiles = mode == kModeUpdate ? c->n_upd : c->n_sym;
-        g.mats = at<MatDev>(c, c->o_mats);
-        g.tmaps = at<CUtensorMap>(c, c->o_tmaps);
-        g.emaps = at<CUtensorMap>(c, c->o_emaps);
+        g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
+        g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
+        g.mats = at<MatDev>(P, P->o_mats);
+        g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
+        g.emaps = at<CUtensorMap>(P, P->o_emaps);
         g.imaps = d_imaps;
         g.omaps = d_omaps;
-        g.mflags = at<int>(c, c->o_flags);
-        g.inv = at<float>(c, c->o_inv);
+        g.mflags = at<int>(P, P->o_flags);
+        g.inv = at<float>(P, P->o_inv);
         g.first_iter = (t == 0);
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
@@ -678,7 +757,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         ProfScope ps(c, 2 + mode, st);
         const bool edge = (t == 0) || (t == T - 1);
         const size_t sm_long = gemm_smem_bytes<kLongStages>(), sm_short = gemm_smem_bytes<kShortStages>();
-        if (c->long_k[mode]) {
+        if (P->long_k[mode]) {
           if (edge) launch(pe_gemm_sm100<kLongStages, true>, grid, kGemmThreads, sm_long, st, g);
           else launch(pe_gemm_sm100<kLongStages, false>, grid, kGemmThreads, sm_long, st, g);
         } else {
@@ -687,9 +766,9 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         }
       } else {
         GemmF32Args g;
-        g.tiles = at<Tile>(c, mode == kModeUpdate ? c->o_upd : c->o_sym);
-        g.ntiles = mode == kModeUpdate ? c->n_upd : c->n_sym;
-        g.mats = at<MatDev>(c, c->o_mats);
+        g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
+        g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
+        g.mats = at<MatDev>(P, P->o_mats);
         g.outs = d_outs_direct;
         g.mode = mode; g.xin = xin; g.final_iter = fin;
         g.a = fa; g.b = fb; g.c = fc;
@@ -709,6 +788,10 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   return PE_OK;
 }
 
+// End-to-end entry on host buffers.  The batch is cut into G groups of about
+// equal bytes and software-pipelined over three streams: H2D copies of group
+// g+1 and D2H copies of group g-1 overlap the compute of group g (PCIe is full
+// duplex, so both directions also overlap each other).
 extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
                                    int count, int iters, pe_dtype dtype, void* stream_) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
@@ -719,31 +802,75 @@ extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const*
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   PE_CUDA(cudaSetDevice(c->device));
   const size_t es = (dtype == PE_BF16) ? 2 : 4;
-  std::vector<size_t> off(count);
+  std::vector<size_t> off(count), nb(count);
   size_t total = 0;
   for (int i = 0; i < count; ++i) {
     if (!in[i] || !out[i]) return PE_ERR_INVALID_ARG;
+    nb[i] = (size_t)shapes[2 * i] * shapes[2 * i + 1] * es;
     off[i] = total;
-    total += rup((size_t)shapes[2 * i] * shapes[2 * i + 1] * es, 256);
+    total += rup(nb[i], 256);
   }
   if (total > c->staging_bytes) {
     if (c->staging) { PE_CUDA(cudaDeviceSynchronize()); cudaFree(c->staging); c->staging = nullptr; }
     if (cudaMalloc(&c->staging, total) != cudaSuccess) { cudaGetLastError(); c->staging_bytes = 0; return PE_ERR_WORKSPACE; }
     c->staging_bytes = total;
   }
+  if (!c->s_h2d) {
+    PE_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    PE_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  }
+  // groups: contiguous index ranges of ~equal bytes, ~16 MB or more each, at
+  // most 8 (GPT-2 S set on B200 / PCIe 5: G=1 8.1 ms, G=4 7.2 ms, G=8 6.4 ms)
+  int G = (int)std::max<size_t>(1, std::min<size_t>({(size_t)count, (size_t)8, total / (16u << 20)}));
+  if (const char* gv = getenv("PE_HOST_GROUPS")) G = std::max(1, std::min(count, atoi(gv)));   // experiments
+  const bool skip_compute = getenv("PE_HOST_NOCOMPUTE") != nullptr;                          // experiments
+  std::vector<int> gbeg(G + 1, count);
+  gbeg[0] = 0;
+  {
+    size_t acc = 0;
+    int g = 1;
+    for (int i = 0; i < count && g < G; ++i) {
+      acc += nb[i];
+      if (acc * G >= total * (size_t)g) gbeg[g++] = i + 1;
+    }
+  }
+  while ((int)c->host_ev.size() < 3 * G + 1) {
+    cudaEvent_t e;
+    PE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->host_ev.push_back(e);
+  }
+  cudaEvent_t ev_start = c->host_ev[3 * G];
+  PE_CUDA(cudaEventRecord(ev_start, st));           // after earlier work on the caller's stream
+  PE_CUDA(cudaStreamWaitEvent(c->s_h2d, ev_start, 0));
+  PE_CUDA(cudaStreamWaitEvent(c->s_d2h, ev_start, 0));
   std::vector<void*> dptr(count);
   uint8_t* base = reinterpret_cast<uint8_t*>(c->staging);
-  for (int i = 0; i < count; ++i) {
-    dptr[i] = base + off[i];
-    PE_CUDA(cudaMemcpyAsync(dptr[i], in[i], (size_t)shapes[2 * i] * shapes[2 * i + 1] * es,
-                            cudaMemcpyHostToDevice, st));
+  for (int i = 0; i < count; ++i) dptr[i] = base + off[i];
+  int launches = 0;
+  cudaEvent_t last_ed = nullptr;
+  for (int g = 0; g < G; ++g) {
+    const int b = gbeg[g], e = gbeg[g + 1];
+    if (b >= e) continue;
+    cudaEvent_t eh = c->host_ev[3 * g], ec = c->host_ev[3 * g + 1], ed = c->host_ev[3 * g + 2];
+    for (int i = b; i < e; ++i)
+      PE_CUDA(cudaMemcpyAsync(dptr[i], in[i], nb[i], cudaMemcpyHostToDevice, c->s_h2d));
+    PE_CUDA(cudaEventRecord(eh, c->s_h2d));
+    PE_CUDA(cudaStreamWaitEvent(st, eh, 0));
+    if (!skip_compute) {
+      s = pe_polar(c, dptr.data() + b, dptr.data() + b, shapes + 2 * b, e - b, iters, dtype, stream_);
+      if (s != PE_OK) return s;
+      launches += c->last_launches;
+    }
+    PE_CUDA(cudaEventRecord(ec, st));
+    PE_CUDA(cudaStreamWaitEvent(c->s_d2h, ec, 0));
+    for (int i = b; i < e; ++i)
+      PE_CUDA(cudaMemcpyAsync(out[i], dptr[i], nb[i], cudaMemcpyDeviceToHost, c->s_d2h));
+    PE_CUDA(cudaEventRecord(ed, c->s_d2h));
+    last_ed = ed;
   }
-  s = pe_polar(c, dptr.data(), dptr.data(), shapes, count, iters, dtype, stream_);
-  if (s != PE_OK) return s;
-  for (int i = 0; i < count; ++i)
-    PE_CUDA(cudaMemcpyAsync(out[i], dptr[i], (size_t)shapes[2 * i] * shapes[2 * i + 1] * es,
-                            cudaMemcpyDeviceToHost, st));
+  if (last_ed) PE_CUDA(cudaStreamWaitEvent(st, last_ed, 0));
   PE_CUDA(cudaStreamSynchronize(st));
+  c->last_launches = launches;
   return PE_OK;
 }
 

@@ -316,3 +316,40 @@ def test_full_llama_set_sampled(ctx):
             assert om.rel_frobenius(Y, ref) <= 2e-2
         else:
             check_g1_g3(Y, M)
+
+
+def test_plan_cache_and_async_calls(ctx):
+    """Alternating shape lists reuse cached plans; back-to-back asynchronous
+    calls with different buffers (no sync between them) each see their own
+    pointers (per-call upload ring)."""
+    A = [bf16_values(syn.gaussian(256, 512, seed=21 + i, std=0.02)) for i in range(3)]
+    B = [bf16_values(syn.gaussian(384, 128, seed=31 + i, std=0.02)) for i in range(2)]
+    ref_a = run(ctx, A)
+    ref_b = run(ctx, B)
+    xa = [[to_dev_bf16(M) for M in A] for _ in range(6)]
+    xb = [[to_dev_bf16(M) for M in B] for _ in range(6)]
+    ya = [ctx.polar(x, iters=5) for x in xa[:3]] + [None] * 3
+    yb = [ctx.polar(x, iters=5) for x in xb[:3]]
+    for k in range(3, 6):                      # interleave shape lists, no synchronisation
+        ya[k] = ctx.polar(xa[k], iters=5)
+        yb.append(ctx.polar(xb[k], iters=5))
+    torch.cuda.synchronize()
+    for ys in ya:
+        for y, r in zip(ys, ref_a):
+            assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
+    for ys in yb:
+        for y, r in zip(ys, ref_b):
+            assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
+
+
+def test_host_entry_point_pipelined_groups(ctx):
+    """pe_polar_host on a batch large enough to be split into several pipelined
+    groups (>= 32 MB per group) equals pe_polar on device buffers."""
+    shapes = [(1024, 4096)] * 12 + [(4096, 1024)] * 4
+    mats = [bf16_values(syn.gaussian(r, c, seed=50 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    dev = run(ctx, mats)
+    ins = [to_dev_bf16(M).cpu().pin_memory() for M in mats]
+    outs = [torch.empty_like(x).pin_memory() for x in ins]
+    ctx.polar_host(ins, outs, iters=5)
+    for a, b in zip(outs, dev):
+        assert np.array_equal(a.float().numpy().astype(np.float64), b)
