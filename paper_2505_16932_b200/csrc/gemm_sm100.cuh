@@ -74,6 +74,7 @@ struct TileCfg {
   const CUtensorMap* B;
   int nk, row_a, col_b;        // k-blocks; this CTA's first row of A and of B
   bool a_mn, b_mn;             // operand stored MN-major (else K-major)
+  bool a_wide, b_wide;         // operand map has 128-row boxes (one TMA per 128-row half)
   bool diag;                   // symmetric phase, I == J: one panel serves both operands
   const CUtensorMap* ein;      // epilogue operand chunk map (update: X, poly: A)
   bool ein_tr;                 // operand chunk is M^T of a tall caller matrix
@@ -94,6 +95,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   const bool tall = kEdge && (fl & kFlagTall) != 0;
   TileCfg c;
   c.scaled = fold;
+  c.a_wide = c.b_wide = false;
   c.ein = nullptr;
   c.ein_tr = false;
   c.eout_tr = false;
@@ -105,12 +107,14 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   } else if (g.mode == kModePoly) {
     c.A = c.B = maps + 2;
     c.a_mn = c.b_mn = false;
+    c.a_wide = c.b_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
     c.ein = em + 2;
     c.eout = em + 3;
   } else {
     c.A = maps + 3;
     c.a_mn = false;
+    c.a_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
     if (fold) {
       c.B = g.imaps + 2 * tl.mat;
@@ -268,7 +272,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   const bool leader = (rank == 0);
   const int cid = blockIdx.x >> 1;
   const int ncl = gridDim.x >> 1;
-  long long st_wait_tempty = 0, st_wait_full = 0, st_wait_tfull = 0;
+  long long st_wait_tempty = 0, st_wait_full = 0, st_wait_tfull = 0, st_lat = 0, st_nstage = 0;
+  __shared__ long long st_issue[8];     // debug: producer issue time per stage (leader CTA)
   const long long st_begin = clock64();
 
   if (warp == 0 && lane == 0) {
@@ -307,11 +312,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         for (int kb = 0; kb < o.nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], o.diag ? 2 * kABytes : 2 * kStageBytes);
+          if (args.stats != nullptr && leader) st_issue[stage] = clock64();
           const uint32_t bar = full_leader0 + stage * sizeof(uint64_t);
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * kBBytes;
           const int k0 = (args.dbg & 8) ? 0 : kb * kBK;   // dbg 8: every load hits the same (L2-resident) boxes
-          if (!o.a_mn) {
+          if (o.a_wide) {
+            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a);           // one 64 x 128 box
+          } else if (!o.a_mn) {
             tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a);
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, k0, o.row_a + 64);
           } else {
@@ -319,7 +327,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, o.row_a + 64, k0);
           }
           if (!o.diag) {          // diagonal tiles: the right operand is the left one
-            if (!o.b_mn) {
+            if (o.b_wide) {
+              tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b);
+            } else if (!o.b_mn) {
               tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b);
               tma_load_2d_pair(b_dst + kBoxBytes, o.B, bar, k0, o.col_b + 64);
             } else {
@@ -352,7 +362,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         for (int kb = 0; kb < o.nk; ++kb) {
           long long t1 = clock64();
           mbar_wait(&full[stage], phase);
-          st_wait_full += clock64() - t1;
+          const long long t1e = clock64();
+          st_wait_full += t1e - t1;
+          if (args.stats != nullptr) { st_lat += t1e - *(volatile long long*)&st_issue[stage]; ++st_nstage; }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a_addr = smem_u32(sA + stage * kABytes);
@@ -511,7 +523,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   if (warp == 1) tmem_dealloc_pair(tmem_base, kTmemCols);
   if (args.stats != nullptr && lane == 0 && (warp == 1 || warp == 2)) {
     long long* st = args.stats + blockIdx.x * 8;
-    if (warp == 1) { st[0] = clock64() - st_begin; st[1] = st_wait_tempty; st[2] = st_wait_full; }
+    if (warp == 1) {
+      st[0] = clock64() - st_begin; st[1] = st_wait_tempty; st[2] = st_wait_full;
+      st[4] = st_lat; st[5] = st_nstage;
+    }
     else { st[3] = st_wait_tfull; }
   }
 }

@@ -473,8 +473,8 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
       const MatDev& md = mats[i];
       if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
           (s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
-          (s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK ||
-          (s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK ||
+          (s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm, 64, 128)) != PE_OK ||
+          (s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm, 64, 128)) != PE_OK ||
           (s = make_emap(&emaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
           (s = make_emap(&emaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
           (s = make_emap(&emaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK ||
