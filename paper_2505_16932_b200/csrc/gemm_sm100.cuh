@@ -250,8 +250,11 @@ __device__ __forceinline__ void read_operand_half(const uint8_t* slot, int lane,
   }
 }
 
-// kSt: smem pipeline stages; kEdge: first/last-iteration specialisation.
-template <int kSt, bool kEdge>
+// kSt: smem pipeline stages; kSl: 4 KB epilogue slots per warp (2 = one per
+// chunk, whole-tile operand prefetch; 1 = a single staging slot, for the Gram
+// which has no epilogue operand and takes a deeper ring); kEdge:
+// first/last-iteration specialisation.
+template <int kSt, int kSl, bool kEdge>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -261,9 +264,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;
   uint64_t* tempty = tfull + 2;
-  uint64_t* xbars = tempty + 2;                              // kEpiWarps x kEpiChunks
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbars + kEpiWarps * kEpiChunks);
-  uint8_t* epi_smem = smem + kSt * kStageBytes + kBarrierBytes;   // kEpiWarps x kEpiChunks x 4 KB
+  uint64_t* xbars = tempty + 2;                              // kEpiWarps x kSl
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbars + kEpiWarps * kSl);
+  uint8_t* epi_smem = smem + kSt * kStageBytes + kBarrierBytes;   // kEpiWarps x kSl x 4 KB
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -285,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 2 * kEpiWarps);
     }
-    for (int s = 0; s < kEpiWarps * kEpiChunks; ++s) mbar_init(&xbars[s], 1);
+    for (int s = 0; s < kEpiWarps * kSl; ++s) mbar_init(&xbars[s], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, kTmemCols);
@@ -403,8 +406,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     const int ew = warp - 2;
     const int q = warp & 3;
     const int half = ew >> 2;
-    uint8_t* slots = epi_smem + ew * kEpiChunks * kEpiSlotBytes;
-    uint64_t* xbar = xbars + ew * kEpiChunks;
+    uint8_t* slots = epi_smem + ew * kSl * kEpiSlotBytes;
+    uint64_t* xbar = xbars + ew * kSl;
     const bool need_load = (mode != kModeGram) && !(args.dbg & 3);
     const bool do_work = !(args.dbg & 1);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
@@ -467,7 +470,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
           phase_bits ^= 1u << k;
         }
-        uint8_t* slot = slots + k * kEpiSlotBytes;
+        uint8_t* slot = slots + (kSl == 1 ? 0 : k) * kEpiSlotBytes;
+        if (kSl == 1 && k > 0) {
+          // single staging slot (Gram: no epilogue operand): the previous
+          // chunk's store must have left smem before this chunk is written
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
         if (kEdge && need_load && cfg.ein_tr != cfg.eout_tr) {
           // operand and result layouts differ (tall caller matrix, first or
           // last iteration): read the whole operand chunk before the in-place
@@ -494,6 +503,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             if (mirror) mirror_chunk32(mdst, md.m, md.ldm, r, c0 + 32 * h, w);
           }
         }
+        if (kSl == 1) {
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slot, c0, r0);
+            else tma_store_2d(cfg.eout, slot, r0, c0);
+            bulk_commit();
+          }
+        }
         ++nvalid;
       }
       // one proxy fence and one bulk group for the whole tile
@@ -502,11 +520,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-        for (int k = 0; k < nvalid; ++k) {
-          if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
-          else tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, r0, col0(tl, k));
+        if (kSl > 1) {
+          for (int k = 0; k < nvalid; ++k) {
+            if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
+            else tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, r0, col0(tl, k));
+          }
+          bulk_commit();
         }
-        bulk_commit();
         bulk_wait_read<0>();          // this tile's stores have left smem: slots are free
         if (has_next && need_load) issue_tile(ntl, ncfg, nnc);
       }
@@ -531,8 +551,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   }
 }
 
-template <int kSt> constexpr size_t gemm_smem_bytes() {
-  return 1024 + (size_t)kSt * kStageBytes + kBarrierBytes + (size_t)kEpiWarps * kEpiChunks * kEpiSlotBytes;
+template <int kSt, int kSl> constexpr size_t gemm_smem_bytes() {
+  return 1024 + (size_t)kSt * kStageBytes + kBarrierBytes + (size_t)kEpiWarps * kSl * kEpiSlotBytes;
 }
 
 }  // namespace pe

@@ -45,6 +45,11 @@ using namespace pe;
 #define PE_SHORT_STAGES 4
 #endif
 constexpr int kLongStages = PE_LONG_STAGES;
+// the Gram (no epilogue operand, one 4 KB staging slot per warp) takes 6
+#ifndef PE_GRAM_STAGES
+#define PE_GRAM_STAGES 6
+#endif
+constexpr int kGramStages = PE_GRAM_STAGES;
 constexpr int kShortStages = PE_SHORT_STAGES;
 
 namespace {
@@ -272,14 +277,18 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
     return PE_ERR_UNSUPPORTED;
   }
   PE_CUDA(cudaSetDevice(device));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kLongStages>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kLongStages>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kShortStages>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kShortStages>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kGramStages, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kGramStages, 1>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kGramStages, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kGramStages, 1>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages, 2>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages, 2>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kShortStages, 2>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kShortStages, 2>()));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -756,13 +765,18 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
         const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
         ProfScope ps(c, 2 + mode, st);
         const bool edge = (t == 0) || (t == T - 1);
-        const size_t sm_long = gemm_smem_bytes<kLongStages>(), sm_short = gemm_smem_bytes<kShortStages>();
-        if (P->long_k[mode]) {
-          if (edge) launch(pe_gemm_sm100<kLongStages, true>, grid, kGemmThreads, sm_long, st, g);
-          else launch(pe_gemm_sm100<kLongStages, false>, grid, kGemmThreads, sm_long, st, g);
+        if (mode == kModeGram) {
+          const size_t sm = gemm_smem_bytes<kGramStages, 1>();
+          if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
+          else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
+        } else if (P->long_k[mode]) {
+          const size_t sm = gemm_smem_bytes<kLongStages, 2>();
+          if (edge) launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, sm, st, g);
+          else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
         } else {
-          if (edge) launch(pe_gemm_sm100<kShortStages, true>, grid, kGemmThreads, sm_short, st, g);
-          else launch(pe_gemm_sm100<kShortStages, false>, grid, kGemmThreads, sm_short, st, g);
+          const size_t sm = gemm_smem_bytes<kShortStages, 2>();
+          if (edge) launch(pe_gemm_sm100<kShortStages, 2, true>, grid, kGemmThreads, sm, st, g);
+          else launch(pe_gemm_sm100<kShortStages, 2, false>, grid, kGemmThreads, sm, st, g);
         }
       } else {
         GemmF32Args g;
