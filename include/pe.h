@@ -102,7 +102,9 @@ pe_status pe_coeffs_ex(double ell, int degree, int T, double safety, double cush
 
 /* ------------------------------------------------------------------------ */
 /* Online stage (device).  One context per device; a context is not          */
-/* thread-safe (serialise calls on it).                                      */
+/* thread-safe (serialise calls on it) and its calls must be ordered on one  */
+/* stream (it caches up to 8 plans over one workspace and keeps a ring of 4  */
+/* pinned per-call upload buffers, so up to 4 calls may be in flight).       */
 /* ------------------------------------------------------------------------ */
 typedef struct pe_ctx_s* pe_ctx;
 
@@ -153,9 +155,12 @@ pe_status pe_polar(pe_ctx ctx, const void* const* in, void* const* out, const in
 
 /*
  * End-to-end variant on HOST buffers: copies in[i] (host) to device staging
- * owned by the context, runs pe_polar on `stream`, copies the results back to
- * out[i] (host) and synchronises `stream`.  Same semantics and errors as
- * pe_polar; host buffers should be pinned for full PCIe bandwidth.
+ * owned by the context, runs pe_polar, copies the results back to out[i]
+ * (host) and synchronises `stream` before returning.  The batch is cut into
+ * up to 8 groups of about equal bytes that are software-pipelined over the
+ * caller's stream and two context-owned copy streams (H2D of group g+1 and
+ * D2H of group g-1 overlap the compute of group g).  Same semantics and
+ * errors as pe_polar; host buffers should be pinned for full PCIe bandwidth.
  */
 pe_status pe_polar_host(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
                         int count, int iters, pe_dtype dtype, void* stream);

@@ -353,3 +353,16 @@ def test_host_entry_point_pipelined_groups(ctx):
     ctx.polar_host(ins, outs, iters=5)
     for a, b in zip(outs, dev):
         assert np.array_equal(a.float().numpy().astype(np.float64), b)
+
+
+@pytest.mark.parametrize("T", [1, 2])
+@pytest.mark.parametrize("shape", [(1024, 256), (520, 200), (256, 1024)])
+def test_first_and_last_iteration_edges(ctx, T, shape):
+    """T = 1 makes the first iteration also the last (folded input read and
+    direct, possibly transposed, output in one launch); T = 2 exercises them
+    in consecutive launches.  Both orientations, aligned and ragged."""
+    M = bf16_values(syn.gaussian(*shape, seed=77 + T, std=0.02))
+    X = run(ctx, [M], T=T)[0]
+    ref = oi.polar_express(M, TABLE, T)
+    assert np.all(np.isfinite(X))
+    assert om.rel_frobenius(X, ref) <= 3e-2     # early iterates: chaotic bf16 sensitivity (see test_iteration_counts)
