@@ -126,8 +126,9 @@ pe_status pe_set_coeffs(pe_ctx ctx, const double* coeffs, int ntuples, int degre
 
 /* Pre-size the workspace for a batch so that a later pe_polar with the same
  * (or smaller) batch performs no allocation (required before CUDA-graph
- * capture).  Workspace per matrix (m = min side, n = max side): two bf16 (or
- * fp32) m x n iterate buffers, two m x m buffers (A, B), a norm slot.
+ * capture).  Workspace per matrix (m = min side, n = max side): two bf16 m x n
+ * iterate buffers, two m x m buffers (A, B), a norm slot; PE_FP32 holds each
+ * buffer as three bf16 planes (3x the bytes).
  * Errors: PE_ERR_INVALID_ARG, PE_ERR_WORKSPACE. */
 pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtype);
 
@@ -135,7 +136,10 @@ pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtyp
  * Polar Express on a batch of `count` matrices (Listing 2).
  *   in[i], out[i]  device pointers to rows_i x cols_i row-major matrices of
  *                  element type `dtype` (PE_BF16: bf16 tensor-core path with
- *                  fp32 accumulation; PE_FP32: fp32 path).  in[i] == out[i]
+ *                  fp32 accumulation; PE_FP32: fp32 values, every product
+ *                  on the same tensor cores as six bf16 plane products
+ *                  P_i Q_j^T, i + j <= 2, of the three-plane split
+ *                  v = p0 + p1 + p2; relF <= 1e-5).  in[i] == out[i]
  *                  (in place) is allowed; distinct matrices must not overlap.
  *   iters          T >= 1; tuples past the table repeat its last tuple
  *                  (P:495-496).
@@ -176,7 +180,7 @@ pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
  * their durations into ms[kind] and launch counts into counts[kind] for the
  * first `nkinds` kinds, and clears the pending list.  Kinds:
  *   0 norm (pe_norm_kernel)     1 scale/orient (pe_copy_kernel)
- *   2 Gram  3 poly  4 update (pe_gemm_sm100 / pe_gemm_f32)
+ *   2 Gram  3 poly  4 update (pe_gemm_sm100; fp32 calls: the three-plane instantiation)
  *   5 transpose-back (pe_copy_kernel)
  */
 #define PE_PROFILE_KINDS 6

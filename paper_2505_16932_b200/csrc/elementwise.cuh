@@ -9,6 +9,9 @@
 //                        inputs (transpose trick) and the transpose
 //                        back of tall results.  16-byte vectors on
 //                        both the read and the write side.
+//   pe_planes_kernel     fp32 path: X_0 = M/s split into three bf16 planes
+//                        (gemm_sm100.cuh, kP = 3), and the final fp32 result
+//                        p0 + p1 + p2; optionally transposed (tall inputs).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
 struct CopyMat {
   int rows, cols;        // source shape
   int sld, dld;          // leading dims (elements)
-  int pad0, pad1;
+  int64_t pstride;       // fp32 path: elements between the three bf16 planes of the workspace side
 };
 
 // Work item of the copy passes: a band of rows (row kernel) or a 64x64 tile
@@ -261,6 +264,65 @@ __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// fp32 path, one 64x64 tile of the source per item.
+//   kSplit: src fp32 caller matrix (rows x cols, ld sld), dst three bf16
+//           planes (ld dld, plane stride pstride): dst = split3(scale * src)
+//   else:   src three bf16 planes (ld sld, plane stride pstride), dst fp32:
+//           dst = p0 + p1 + p2
+// kTr: dst is the transpose (cols x rows) of src.
+template <bool kSplit, bool kTr>
+__global__ void __launch_bounds__(256) pe_planes_kernel(const CopyArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float tile[64][65];
+  for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    const CopyItem ci = a.items[it];
+    const CopyMat cm = a.mats[ci.mat];
+    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const int r0 = ci.a * 64, c0 = ci.b * 64;
+    auto put = [&](int dr, int dc, float f) {
+      if (kSplit) {
+        __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(a.dsts[ci.mat]) + (size_t)dr * cm.dld + dc;
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(f);
+        const float r1 = __fsub_rn(f, __bfloat162float(h0));
+        const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
+        d[0] = h0;
+        d[cm.pstride] = h1;
+        d[2 * cm.pstride] = __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(h1)));
+      } else {
+        reinterpret_cast<float*>(a.dsts[ci.mat])[(size_t)dr * cm.dld + dc] = f;
+      }
+    };
+    for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+      const int i = e >> 6, j = e & 63;
+      const int r = r0 + i, c = c0 + j;
+      float f = 0.f;
+      if (r < cm.rows && c < cm.cols) {
+        const size_t o = (size_t)r * cm.sld + c;
+        if (kSplit) {
+          f = reinterpret_cast<const float*>(a.srcs[ci.mat])[o];
+          if (a.scale) f = __fmul_rn(f, sc);
+        } else {
+          const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(a.srcs[ci.mat]) + o;
+          f = __fadd_rn(__fadd_rn(__bfloat162float(p[0]), __bfloat162float(p[cm.pstride])),
+                        __bfloat162float(p[2 * cm.pstride]));
+        }
+        if (!kTr) put(r, c, f);
+      }
+      if (kTr) tile[i][j] = f;
+    }
+    if (kTr) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+        const int i = e >> 6, j = e & 63;
+        const int dr = c0 + i, dc = r0 + j;          // dst row = source column
+        if (dr < cm.cols && dc < cm.rows) put(dr, dc, tile[j][i]);
+      }
+      __syncthreads();
+    }
   }
 }
 

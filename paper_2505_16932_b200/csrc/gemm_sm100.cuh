@@ -32,11 +32,23 @@
 //               = two 256-column fp32 accumulators -> the epilogue of tile i
 //               overlaps the main loop of tile i+1)
 //   warps 2..9  epilogue: lane quadrant (warp % 4) x column half
-//               ((warp-2) / 4), 16-column chunks staged in smem: operand
-//               chunks arrive by TMA, bf16 results leave by TMA store;
+//               ((warp-2) / 4), 32-row x 64-column chunks staged in smem
+//               (128B swizzle): operand chunks arrive by TMA, bf16 results
+//               leave by TMA store;
 //               mirrored stores of the symmetric phases go straight to global.
 // Grouped scheduling: one launch covers every tile of every matrix of the
 // batch; cluster c walks tiles c, c + #clusters, ... of a host-built list.
+//
+// fp32 (kP = 3): every workspace buffer holds three stacked bf16 planes
+// v = p0 + p1 + p2 (p0 = bf16(v), p1 = bf16(v - p0), p2 = bf16(v - p0 - p1);
+// 24 significand bits, i.e. an fp32 value), and each product is the K-
+// concatenation of the six plane products with i + j <= 2:
+//   P Q^T ~ sum_{i+j<=2} P_i Q_j^T  =  [P2 P1 P0 P1 P0 P0] [Q0 Q1 Q2 Q0 Q1 Q0]^T
+// (dropped terms are O(2^-24) relative).  The main loop is the bf16 one over
+// 6x the k-blocks (plane p of a buffer = rows [p m, (p+1) m) of its stacked
+// tensor map); the epilogue sums the operand planes, applies the fp32
+// arithmetic and splits the result into planes again.  No folding, no
+// diagonal single-panel loads.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -55,7 +67,7 @@ struct GemmArgs {
   int ntiles;
   const MatDev* mats;
   const CUtensorMap* tmaps;    // main loop, 4 per matrix: X[0], X[1], A, B (64x64 boxes, 128B swizzle)
-  const CUtensorMap* emaps;    // epilogue, 4 per matrix: X[0], X[1], A, B (16-col x 32-row boxes)
+  const CUtensorMap* emaps;    // epilogue, 4 kP per matrix: X[0], X[1], A, B (64-col x 32-row boxes) x planes
   const CUtensorMap* imaps;    // per call, 2 per matrix: caller input main loop / epilogue chunk
   const CUtensorMap* omaps;    // per call, 1 per matrix: caller output epilogue chunk
   const int* mflags;           // per call, per matrix: kFlag*
@@ -81,15 +93,18 @@ struct TileCfg {
   const CUtensorMap* eout;     // result chunk map
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
   bool scaled;                 // first iteration of a folded matrix
+  int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
 // kEdge: the launch is a first or last iteration (folded input / direct
 // output possible); the middle iterations compile all of that away.
-template <bool kEdge>
+// kP: planes per buffer (1 = bf16, 3 = fp32 as three bf16 planes); the
+// epilogue maps are kP per buffer (one per plane), buffer b plane p at em[kP*b + p].
+template <bool kEdge, int kP = 1>
 __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, uint32_t rank) {
   const MatDev& md = g.mats[tl.mat];
   const CUtensorMap* maps = g.tmaps + 4 * tl.mat;
-  const CUtensorMap* em = g.emaps + 4 * tl.mat;
+  const CUtensorMap* em = g.emaps + 4 * kP * tl.mat;
   const int fl = kEdge ? g.mflags[tl.mat] : 0;
   const bool fold = kEdge && g.first_iter && (fl & kFlagFolded);
   const bool tall = kEdge && (fl & kFlagTall) != 0;
@@ -103,14 +118,14 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.A = c.B = fold ? g.imaps + 2 * tl.mat : maps + g.xin;
     c.a_mn = c.b_mn = fold && tall;
     c.nk = (md.n + kBK - 1) / kBK;
-    c.eout = em + 2;
+    c.eout = em + 2 * kP;
   } else if (g.mode == kModePoly) {
     c.A = c.B = maps + 2;
     c.a_mn = c.b_mn = false;
     c.a_wide = c.b_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
-    c.ein = em + 2;
-    c.eout = em + 3;
+    c.ein = em + 2 * kP;
+    c.eout = em + 3 * kP;
   } else {
     c.A = maps + 3;
     c.a_mn = false;
@@ -124,16 +139,17 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     } else {
       c.B = maps + g.xin;
       c.b_mn = true;
-      c.ein = em + g.xin;
+      c.ein = em + kP * g.xin;
     }
     if (kEdge && g.final_iter && (fl & kFlagDirect)) {
       c.eout = g.omaps + tl.mat;
       c.eout_tr = tall;
     } else {
-      c.eout = em + (g.xin ^ 1);
+      c.eout = em + kP * (g.xin ^ 1);
     }
   }
-  c.diag = (g.mode != kModeUpdate) && (tl.tm == tl.tn);
+  c.diag = (kP == 1) && (g.mode != kModeUpdate) && (tl.tm == tl.tn);
+  c.prow = (kP == 1) ? 0 : md.m;
   c.row_a = tl.tm * kBM + (int)rank * (kBM / 2);
   c.col_b = tl.tn * kBN + (int)rank * (kBN / 2);
   return c;
@@ -250,12 +266,143 @@ __device__ __forceinline__ void read_operand_half(const uint8_t* slot, int lane,
   }
 }
 
+// ---------------------------------------------------------------- fp32 (kP = 3)
+// Split v into three bf16 planes: v - p0 and (v - p0) - p1 are exact in fp32
+// (Sterbenz), so p0 + p1 + p2 carries v's 24 significand bits.
+__device__ __forceinline__ void split3(float v, float& p0, float& p1, float& p2) {
+  p0 = __bfloat162float(__float2bfloat16_rn(v));
+  const float r1 = __fsub_rn(v, p0);
+  p1 = __bfloat162float(__float2bfloat16_rn(r1));
+  p2 = __fsub_rn(r1, p1);
+}
+
+// Epilogue arithmetic of one half (32 columns) of a 32-row x 64-column chunk
+// whose three planes sit in slots[0..2] (128B-swizzled 4 KB each): the operand
+// (poly: A, update: X) is p0 + p1 + p2, the fp32 result is split back into
+// the three slots in place; symmetric phases also store the mirrored planes
+// (plane stride ps elements) when mdst != nullptr.
+__device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slots, int lane, int half32, float* w,
+                                                __nv_bfloat16* mdst, int m, int ld, size_t ps, int r, int c0) {
+#pragma unroll
+  for (int qq = 0; qq < 2; ++qq) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      float* wv = w + 16 * qq + 8 * v;
+      const uint32_t off = sw128_off(lane, half32 * 4 + qq * 2 + v);
+      if (g.mode != kModeGram) {
+        float o0[8], o1[8], o2[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(slots + off), o0);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(slots + kEpiSlotBytes + off), o1);
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(slots + 2 * kEpiSlotBytes + off), o2);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float o = __fadd_rn(__fadd_rn(o0[j], o1[j]), o2[j]);
+          wv[j] = (g.mode == kModePoly) ? __fadd_rn(__fmul_rn(g.b, o), __fmul_rn(g.c, wv[j]))
+                                        : __fadd_rn(__fmul_rn(g.a, o), wv[j]);
+        }
+      }
+      float p0[8], p1[8], p2[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) split3(wv[j], p0[j], p1[j], p2[j]);
+      *reinterpret_cast<uint4*>(slots + off) = pack8_bf16(p0);
+      *reinterpret_cast<uint4*>(slots + kEpiSlotBytes + off) = pack8_bf16(p1);
+      *reinterpret_cast<uint4*>(slots + 2 * kEpiSlotBytes + off) = pack8_bf16(p2);
+      if (mdst != nullptr && r < m) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + 16 * qq + 8 * v + j;
+          if (c < m) {
+            const size_t e = (size_t)c * ld + r;
+            mdst[e] = __float2bfloat16_rn(p0[j]);
+            mdst[ps + e] = __float2bfloat16_rn(p1[j]);
+            mdst[2 * ps + e] = __float2bfloat16_rn(p2[j]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Epilogue role of the fp32 instantiation: chunk by chunk (three 4 KB plane
+// slots per warp): operand planes in by TMA, fp32 arithmetic, result planes
+// out by TMA.  The main loop is 6x longer than the bf16 one, so the
+// per-chunk load latency stays hidden behind the next tile's MMAs.
+__device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* slots, uint64_t* xbar,
+                                                uint64_t* tfull, uint32_t tempty_leader0, uint32_t tmem_base,
+                                                int warp, int lane, uint32_t rank, int cid, int ncl) {
+  const int ew = warp - 2;
+  const int q = warp & 3;
+  const int half = ew >> 2;
+  const int mode = args.mode;
+  const bool need_load = (mode != kModeGram);
+  const int row_off = (int)rank * (kBM / 2) + q * 32;
+  uint32_t acc_phase = 0, xphase = 0;
+  for (int t = cid; t < args.ntiles; t += ncl) {
+    const Tile tl = args.tiles[t];
+    const MatDev md = args.mats[tl.mat];
+    const TileCfg cfg = tile_cfg<false, 3>(args, tl, rank);
+    mbar_wait(&tfull[0], acc_phase);
+    tc_fence_after();
+    const int r0 = tl.tm * kBM + row_off;
+    const int r = r0 + lane;
+    // accumulator = buffer 0 (small terms + first half of the big chain) +
+    // buffer 1 (second half of the big chain)
+    const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
+    const int ncols = (mode == kModeUpdate) ? md.n : md.m;
+    const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
+    __nv_bfloat16* mdst = mirror ? reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B) : nullptr;
+    const size_t ps = (size_t)md.m * md.ldm;
+#pragma unroll 1
+    for (int k = 0; k < kEpiChunks; ++k) {
+      const int c0 = tl.tn * kBN + half * (kBN / 2) + k * kEpiCols;
+      if (c0 >= ncols) break;                                   // warp-uniform
+      if (lane == 0) {
+        bulk_wait_read<0>();                                    // previous chunk's stores left the slots
+        if (need_load) {
+          mbar_arrive_expect_tx(xbar, 3 * kEpiSlotBytes);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) tma_load_2d(slots + p * kEpiSlotBytes, cfg.ein + p, xbar, c0, r0);
+        }
+      }
+      __syncwarp();
+      if (need_load) {
+        mbar_wait(xbar, xphase);
+        xphase ^= 1;
+      }
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        if (c0 + 32 * h >= ncols) break;
+        float w[32], w2[32];
+        tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+        tmem_ld32(t_row + kBN + k * kEpiCols + 32 * h, w2);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
+        epilogue_math_p3(args, slots, lane, h, w, mdst, md.m, md.ldm, ps, r, c0 + 32 * h);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p) tma_store_2d(cfg.eout + p, slots + p * kEpiSlotBytes, c0, r0);
+        bulk_commit();
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_remote(tempty_leader0);
+    acc_phase ^= 1;
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
 // kSt: smem pipeline stages; kSl: 4 KB epilogue slots per warp (2 = one per
 // chunk, whole-tile operand prefetch; 1 = a single staging slot, for the Gram
-// which has no epilogue operand and takes a deeper ring); kEdge:
-// first/last-iteration specialisation.
-template <int kSt, int kSl, bool kEdge>
+// which has no epilogue operand and takes a deeper ring; 3 = the three plane
+// slots of the fp32 instantiation); kEdge: first/last-iteration
+// specialisation; kP: planes per buffer (1 = bf16, 3 = fp32, see top).
+template <int kSt, int kSl, bool kEdge, int kP = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
+  static_assert(kP == 1 || (kP == 3 && kSl == 3 && !kEdge), "fp32 planes: three slots, no folding");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -308,10 +455,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       int stage = 0;
       uint32_t phase = 0;
       TileCfg nxt;
-      if (cid < args.ntiles) nxt = tile_cfg<kEdge>(args, args.tiles[cid], rank);
+      if (cid < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[cid], rank);
       for (int t = cid; t < args.ntiles; t += ncl) {
         const TileCfg o = nxt;
-        if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge>(args, args.tiles[t + ncl], rank);   // off the critical path
+        if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[t + ncl], rank);   // off the critical path
+        // kP = 3: six plane-pair segments (i, j), small terms first:
+        // (2,0) (1,1) (0,2) (1,0) (0,1) (0,0).  The tensor core adds each
+        // K=16 step into the fp32 accumulator with truncation; with the big
+        // (0,0) chain last, the small terms are never truncated against the
+        // big accumulator (256x1024: relF 2.0e-5 big-first, 2.4e-6 now).
+        for (int sg = 0; sg < (kP == 3 ? 6 : 1); ++sg) {
+        const int pa = (kP == 3) ? ((0x001012 >> (4 * sg)) & 0xF) * o.prow : 0;
+        const int pb = (kP == 3) ? ((0x010210 >> (4 * sg)) & 0xF) * o.prow : 0;
         for (int kb = 0; kb < o.nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], o.diag ? 2 * kABytes : 2 * kStageBytes);
@@ -321,26 +476,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           uint8_t* b_dst = sB + stage * kBBytes;
           const int k0 = (args.dbg & 8) ? 0 : kb * kBK;   // dbg 8: every load hits the same (L2-resident) boxes
           if (o.a_wide) {
-            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a);           // one 64 x 128 box
+            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);      // one 64 x 128 box
           } else if (!o.a_mn) {
-            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a);
-            tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, k0, o.row_a + 64);
+            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);
+            tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, k0, o.row_a + pa + 64);
           } else {
             tma_load_2d_pair(a_dst, o.A, bar, o.row_a, k0);
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, o.row_a + 64, k0);
           }
           if (!o.diag) {          // diagonal tiles: the right operand is the left one
             if (o.b_wide) {
-              tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b);
+              tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b + pb);
             } else if (!o.b_mn) {
-              tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b);
-              tma_load_2d_pair(b_dst + kBoxBytes, o.B, bar, k0, o.col_b + 64);
+              tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b + pb);
+              tma_load_2d_pair(b_dst + kBoxBytes, o.B, bar, k0, o.col_b + pb + 64);
             } else {
-              tma_load_2d_pair(b_dst, o.B, bar, o.col_b, k0);
-              tma_load_2d_pair(b_dst + kBoxBytes, o.B, bar, o.col_b + 64, k0);
+              tma_load_2d_pair(b_dst, o.B, bar, o.col_b, k0 + pb);
+              tma_load_2d_pair(b_dst + kBoxBytes, o.B, bar, o.col_b + 64, k0 + pb);
             }
           }
           if (++stage == kSt) { stage = 0; phase ^= 1; }
+        }
         }
       }
     }
@@ -352,17 +508,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       int acc = 0;
       uint32_t acc_phase = 0;
       TileCfg nxt;
-      if (cid < args.ntiles) nxt = tile_cfg<kEdge>(args, args.tiles[cid], rank);
+      if (cid < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[cid], rank);
       for (int t = cid; t < args.ntiles; t += ncl) {
         const TileCfg o = nxt;
-        if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge>(args, args.tiles[t + ncl], rank);
+        if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[t + ncl], rank);
+        const int nkt = o.nk * kP * (kP + 1) / 2;       // kP = 3: six plane-pair segments
         const uint32_t idesc = idesc_bf16(kBM, kBN, o.a_mn, o.b_mn);
         long long t0 = clock64();
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         st_wait_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
-        for (int kb = 0; kb < o.nk; ++kb) {
+        // kP = 3: the big (0,0) chain is split in two K halves, the second
+        // accumulated in the other TMEM buffer (each chain sees half the
+        // truncating adds; the epilogue sums the two).  One tile in flight.
+        const int nsplit = (kP == 3) ? 5 * o.nk + o.nk / 2 : nkt;
+        for (int kb = 0; kb < nkt; ++kb) {
           long long t1 = clock64();
           mbar_wait(&full[stage], phase);
           const long long t1e = clock64();
@@ -381,7 +542,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
                                             : smem_desc_sw128(a_addr + k * 32, 16, 1024);
               const uint64_t bdesc = o.b_mn ? smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024)
                                             : smem_desc_sw128(b_addr + k * 32, 16, 1024);
-              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
+              if (kP == 3 && kb >= nsplit)
+                umma_bf16_pair(tmem_base + kBN, adesc, bdesc, idesc, (kb != nsplit) || k != 0);
+              else
+                umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
             }
             umma_commit_pair(&empty[stage], 0x3);
           }
@@ -390,10 +554,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         }
         if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (kP == 3) {
+          acc_phase ^= 1;          // both buffers belong to one tile
+        } else {
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
       }
     }
+  } else if (kP == 3) {
+    epilogue_role_p3(args, epi_smem + (warp - 2) * kSl * kEpiSlotBytes, xbars + (warp - 2) * kSl, tfull,
+                     mapa_shared(smem_u32(&tempty[0]), 0), tmem_base, warp, lane, rank, cid, ncl);
   } else {
     // ------------------------------------------------------------ epilogue
     // Warp ew owns TMEM lane quadrant q (its 32 output rows) and column half

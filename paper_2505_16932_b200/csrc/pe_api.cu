@@ -2,11 +2,15 @@
 // launch sequence of one Polar Express call (Listing 2):
 //
 //   pe_norm_kernel                       s = ||M||_F*1.01 + 1e-7
-//   pe_copy_kernel                       X_0 = M/s, wide orientation
+//   copy pass (unfolded inputs only)     X_0 = M/s, wide orientation
 //   T x { pe_gemm_sm100 Gram            A = X X^T
 //         pe_gemm_sm100 Poly            B = b A + c A^2
 //         pe_gemm_sm100 Update          X = a X + B X }
-//   pe_copy_kernel (tall inputs only)    transpose back
+//   copy pass (unfolded outputs only)    transpose back
+//
+// bf16 matrices whose rows are 16-byte multiples are folded (no copy passes,
+// gemm_sm100.cuh).  fp32 matrices run the same tensor-core GEMM on three
+// bf16 planes per buffer (kP = 3) between a split pass and a join pass.
 //
 // Every launch covers the whole batch (grouped scheduling).  A plan (tile
 // lists, tensor maps, workspace carve-up) depends only on the shape list; the
@@ -29,7 +33,6 @@
 #include <vector>
 
 #include "elementwise.cuh"
-#include "gemm_f32.cuh"
 #include "gemm_sm100.cuh"
 #include "pe.h"
 #include "pe_types.h"
@@ -51,6 +54,8 @@ constexpr int kLongStages = PE_LONG_STAGES;
 #endif
 constexpr int kGramStages = PE_GRAM_STAGES;
 constexpr int kShortStages = PE_SHORT_STAGES;
+// fp32 (three bf16 planes): 4 x 32 KB ring + 8 warps x 3 plane slots x 4 KB
+constexpr int kP3Stages = 4;
 
 namespace {
 
@@ -289,6 +294,8 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
                                (int)gemm_smem_bytes<kShortStages, 2>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kShortStages, 2>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kP3Stages, 3, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kP3Stages, 3>()));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -412,7 +419,8 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
       *out = p;
       return PE_OK;
     }
-  const size_t es = (dtype == PE_BF16) ? 2 : 4;
+  // workspace element: bf16; fp32 buffers are three stacked bf16 planes
+  const size_t np = (dtype == PE_BF16) ? 1 : 3;
   Plan* P = nullptr;
 
   // workspace carve-up
@@ -428,8 +436,8 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     md.n = md.tall ? md.rows : md.cols;
     md.ldx = (int)rup(md.n, 8);
     md.ldm = (int)rup(md.m, 8);
-    const size_t xb = rup((size_t)md.m * md.ldx * es, 256);
-    const size_t mb = rup((size_t)md.m * md.ldm * es, 256);
+    const size_t xb = rup(np * md.m * md.ldx * 2, 256);
+    const size_t mb = rup(np * md.m * md.ldm * 2, 256);
     offs[4 * i + 0] = total; total += xb;
     offs[4 * i + 1] = total; total += xb;
     offs[4 * i + 2] = total; total += mb;
@@ -449,12 +457,12 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     mats[i].B = ws + offs[4 * i + 3];
   }
 
-  // GEMM tile lists.  bf16: 256x256 pair tiles, symmetric phases only I <= J;
-  // fp32: 64x64 tiles, symmetric phases only tn >= tm.  Update tiles are
-  // generated row-block fastest so concurrently running tiles share a column
-  // panel of X (L2 reuse); lists are then stably sorted longest K first.
+  // GEMM tile lists: 256x256 pair tiles, symmetric phases only I <= J.
+  // Update tiles are generated row-block fastest so concurrently running
+  // tiles share a column panel of X (L2 reuse); lists are then stably sorted
+  // longest K first.
   std::vector<Tile> sym, upd;
-  const int tile = (dtype == PE_BF16) ? kBN : 64;
+  const int tile = kBN;
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
     const int nm = cdiv(md.m, tile), nn = cdiv(md.n, tile);
@@ -473,23 +481,28 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   std::stable_sort(sym.begin(), sym.end(), by_k(true));
   std::stable_sort(upd.begin(), upd.end(), by_k(false));
 
-  // tensor maps (bf16 path)
-  std::vector<CUtensorMap> tmaps, emaps;
-  if (dtype == PE_BF16) {
-    tmaps.resize(4 * (size_t)count);
-    emaps.resize(4 * (size_t)count);
-    for (int i = 0; i < count; ++i) {
-      const MatDev& md = mats[i];
-      if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
-          (s = make_tmap(&tmaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
-          (s = make_tmap(&tmaps[4 * i + 2], md.A, md.m, md.m, md.ldm, 64, 128)) != PE_OK ||
-          (s = make_tmap(&tmaps[4 * i + 3], md.B, md.m, md.m, md.ldm, 64, 128)) != PE_OK ||
-          (s = make_emap(&emaps[4 * i + 0], md.X[0], md.m, md.n, md.ldx)) != PE_OK ||
-          (s = make_emap(&emaps[4 * i + 1], md.X[1], md.m, md.n, md.ldx)) != PE_OK ||
-          (s = make_emap(&emaps[4 * i + 2], md.A, md.m, md.m, md.ldm)) != PE_OK ||
-          (s = make_emap(&emaps[4 * i + 3], md.B, md.m, md.m, md.ldm)) != PE_OK) {
-        delete P;
-        return s;
+  // tensor maps: main loop over all planes of a buffer stacked (plane p =
+  // rows [p m, (p+1) m)), epilogue one map per plane (stores clip at row m)
+  std::vector<CUtensorMap> tmaps(4 * (size_t)count), emaps(4 * np * (size_t)count);
+  for (int i = 0; i < count; ++i) {
+    const MatDev& md = mats[i];
+    const int pr = (int)np * md.m;
+    if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tmaps[4 * i + 1], md.X[1], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tmaps[4 * i + 2], md.A, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
+        (s = make_tmap(&tmaps[4 * i + 3], md.B, pr, md.m, md.ldm, 64, 128)) != PE_OK) {
+      delete P;
+      return s;
+    }
+    void* bufs[4] = {md.X[0], md.X[1], md.A, md.B};
+    for (int b = 0; b < 4; ++b) {
+      const int cols = (b < 2) ? md.n : md.m, ld = (b < 2) ? md.ldx : md.ldm;
+      for (size_t p = 0; p < np; ++p) {
+        void* base = reinterpret_cast<uint8_t*>(bufs[b]) + p * md.m * ld * 2;
+        if ((s = make_emap(&emaps[(4 * i + b) * np + p], base, md.m, cols, ld)) != PE_OK) {
+          delete P;
+          return s;
+        }
       }
     }
   }
@@ -506,7 +519,8 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   // are read by the first iteration straight from the caller's buffer and the
   // last iteration writes the caller's buffer; the others go through the copy
   // passes (see elementwise.cuh): item lists 0 scale-rows, 1 scale-transpose,
-  // 2 finalize-transpose, 3 finalize-rows.
+  // 2 finalize-transpose, 3 finalize-rows.  fp32: every matrix goes through
+  // the split (0/1) and join (2/3) passes, items are 64x64 source tiles.
   std::vector<int> mflags(count, 0);
   std::vector<CopyItem> it[4];
   std::vector<CopyMat> smats(count), fmats(count);
@@ -514,12 +528,20 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
     const bool folded = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
-    const bool direct = (dtype == PE_BF16) ? folded : !md.tall;
+    const bool direct = folded;
     mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0);
     x0[i] = md.X[0];
-    smats[i] = {md.rows, md.cols, md.cols, md.ldx, 0, 0};
-    fmats[i] = {md.m, md.n, md.ldx, md.tall ? md.m : md.n, 0, 0};
+    const int64_t pst = (int64_t)md.m * md.ldx;
+    smats[i] = {md.rows, md.cols, md.cols, md.ldx, pst};
+    fmats[i] = {md.m, md.n, md.ldx, md.tall ? md.m : md.n, pst};
     const int band = std::max(1, 16384 / md.cols);
+    if (dtype == PE_FP32) {
+      for (int a = 0; a < cdiv(md.rows, 64); ++a)
+        for (int b = 0; b < cdiv(md.cols, 64); ++b) it[md.tall ? 1 : 0].push_back({i, a, b, 0});
+      for (int a = 0; a < cdiv(md.m, 64); ++a)
+        for (int b = 0; b < cdiv(md.n, 64); ++b) it[md.tall ? 2 : 3].push_back({i, a, b, 0});
+      continue;
+    }
     if (!folded) {
       if (md.tall) {
         for (int a = 0; a < cdiv(md.rows, 64); ++a)
@@ -688,7 +710,6 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
   const CUtensorMap* d_omaps = d_imaps + 2 * count;
   void** d_in = d_ptrs;
-  void** d_outs_direct = d_ptrs + count;
   void** d_fin_src = d_ptrs + 2 * count;
   void** d_out = d_ptrs + 3 * count;
   const int src_f32 = (dtype == PE_FP32);
@@ -725,9 +746,12 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     if (dtype == PE_BF16) {
       if (tr) launch(pe_transpose_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
       else launch(pe_rows_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
+    } else if (scale) {
+      if (tr) launch(pe_planes_kernel<true, true>, grid, 256, 0, st, ca);
+      else launch(pe_planes_kernel<true, false>, grid, 256, 0, st, ca);
     } else {
-      if (tr) launch(pe_transpose_kernel<float>, grid, 256, 0, st, ca);
-      else launch(pe_rows_kernel<float>, grid, 256, 0, st, ca);
+      if (tr) launch(pe_planes_kernel<false, true>, grid, 256, 0, st, ca);
+      else launch(pe_planes_kernel<false, false>, grid, 256, 0, st, ca);
     }
     ++launches;
   };
@@ -742,53 +766,42 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     const int xin = t & 1;
     const int fin = (t == T - 1);
     for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
-      if (dtype == PE_BF16) {
-        GemmArgs g;
-        g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
-        g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
-        g.mats = at<MatDev>(P, P->o_mats);
-        g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
-        g.emaps = at<CUtensorMap>(P, P->o_emaps);
-        g.imaps = d_imaps;
-        g.omaps = d_omaps;
-        g.mflags = at<int>(P, P->o_flags);
-        g.inv = at<float>(P, P->o_inv);
-        g.first_iter = (t == 0);
-        g.mode = mode; g.xin = xin; g.final_iter = fin;
-        g.a = fa; g.b = fb; g.c = fc;
-        g.dbg = c->dbg;
-        g.stats = nullptr;
-        if (c->dbg & 4) {
-          if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
-          g.stats = c->stats + (size_t)mode * 2048;
-        }
-        const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
-        ProfScope ps(c, 2 + mode, st);
-        const bool edge = (t == 0) || (t == T - 1);
-        if (mode == kModeGram) {
-          const size_t sm = gemm_smem_bytes<kGramStages, 1>();
-          if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
-          else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
-        } else if (P->long_k[mode]) {
-          const size_t sm = gemm_smem_bytes<kLongStages, 2>();
-          if (edge) launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, sm, st, g);
-          else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
-        } else {
-          const size_t sm = gemm_smem_bytes<kShortStages, 2>();
-          if (edge) launch(pe_gemm_sm100<kShortStages, 2, true>, grid, kGemmThreads, sm, st, g);
-          else launch(pe_gemm_sm100<kShortStages, 2, false>, grid, kGemmThreads, sm, st, g);
-        }
+      GemmArgs g;
+      g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
+      g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
+      g.mats = at<MatDev>(P, P->o_mats);
+      g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
+      g.emaps = at<CUtensorMap>(P, P->o_emaps);
+      g.imaps = d_imaps;
+      g.omaps = d_omaps;
+      g.mflags = at<int>(P, P->o_flags);
+      g.inv = at<float>(P, P->o_inv);
+      g.first_iter = (t == 0);
+      g.mode = mode; g.xin = xin; g.final_iter = fin;
+      g.a = fa; g.b = fb; g.c = fc;
+      g.dbg = c->dbg;
+      g.stats = nullptr;
+      if (c->dbg & 4) {
+        if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
+        g.stats = c->stats + (size_t)mode * 2048;
+      }
+      const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
+      ProfScope ps(c, 2 + mode, st);
+      const bool edge = (t == 0) || (t == T - 1);
+      if (dtype == PE_FP32) {
+        launch(pe_gemm_sm100<kP3Stages, 3, false, 3>, grid, kGemmThreads, gemm_smem_bytes<kP3Stages, 3>(), st, g);
+      } else if (mode == kModeGram) {
+        const size_t sm = gemm_smem_bytes<kGramStages, 1>();
+        if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
+      } else if (P->long_k[mode]) {
+        const size_t sm = gemm_smem_bytes<kLongStages, 2>();
+        if (edge) launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
       } else {
-        GemmF32Args g;
-        g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
-        g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
-        g.mats = at<MatDev>(P, P->o_mats);
-        g.outs = d_outs_direct;
-        g.mode = mode; g.xin = xin; g.final_iter = fin;
-        g.a = fa; g.b = fb; g.c = fc;
-        const int grid = std::min(g.ntiles, c->num_sms * 4);
-        ProfScope ps(c, 2 + mode, st);
-        launch(pe_gemm_f32, grid, 256, 0, st, g);
+        const size_t sm = gemm_smem_bytes<kShortStages, 2>();
+        if (edge) launch(pe_gemm_sm100<kShortStages, 2, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kShortStages, 2, false>, grid, kGemmThreads, sm, st, g);
       }
       ++launches;
     }

@@ -8,8 +8,6 @@ namespace pe {
 // bf16 tensor-core path: one 256x256 output tile per CTA pair (cta_group::2)
 constexpr int kBM = 256;        // UMMA M of the pair (128 rows per CTA = TMEM lanes)
 constexpr int kBN = 256;        // UMMA N (each CTA stages 128 of the right operand)
-constexpr int kPrefetch = 0;    // L2 prefetch distance of the producer (k-blocks); 0 = off
-                                // (measured slower: the extra bulk-prefetch requests compete with the ring's loads)
 constexpr int kBK = 64;         // K per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kBoxBytes = 64 * 64 * 2;                 // one TMA box (64 x 64 bf16)
 constexpr int kABytes = (kBM / 2) * kBK * 2;           // 16 KB per CTA
