@@ -20,7 +20,10 @@
 
 namespace pe {
 
-constexpr int kNormChunk = 65536;   // elements per norm block
+#ifndef PE_NORM_CHUNK
+#define PE_NORM_CHUNK 65536
+#endif
+constexpr int kNormChunk = PE_NORM_CHUNK;   // elements per norm block
 constexpr int kNormThreads = 256;
 
 struct NormArgs {

@@ -2,15 +2,18 @@
 // products of one Polar Express iteration (Listing 2), bf16 in /
 // fp32 accumulate:
 //
-//   kModeGram   A  = X X^T           both operands rows of X; only 256x256
-//                                    tiles with I <= J are computed and
-//                                    off-diagonal tiles are also stored
-//                                    transposed at (J, I).
+//   kModeGram   A  = X X^T           both operands rows of X; only the
+//                                    256x256 tiles with I <= J are computed
+//                                    and stored (upper block triangle).
 //   kModePoly   B  = b A + c (A A^T) A symmetric so A A = A A^T (SYRK on A);
 //                                    the epilogue reads the same bf16 A
-//                                    (reading R8); mirrored like the Gram.
+//                                    (reading R8); upper block triangle.
 //   kModeUpdate X' = a X + B X       left operand B (K-major), right operand
 //                                    X (MN-major: row-major X is N-contiguous).
+// The blocks of A and B below the diagonal are never written: a consumer
+// that needs block (I, P) with P < I loads the stored block (P, I) and feeds
+// it to the MMA as an MN-major operand (the transpose is free in the UMMA
+// descriptor), so the symmetric phases write half the bytes.
 //
 // Normalisation and orientation are folded into the first and last
 // iteration (no X_0 buffer, no transpose-back pass) for caller matrices whose
@@ -34,8 +37,7 @@
 //   warps 2..9  epilogue: lane quadrant (warp % 4) x column half
 //               ((warp-2) / 4), 32-row x 64-column chunks staged in smem
 //               (128B swizzle): operand chunks arrive by TMA, bf16 results
-//               leave by TMA store;
-//               mirrored stores of the symmetric phases go straight to global.
+//               leave by TMA store.
 // Grouped scheduling: one launch covers every tile of every matrix of the
 // batch; cluster c walks tiles c, c + #clusters, ... of a host-built list.
 //
@@ -66,17 +68,22 @@ struct GemmArgs {
   const Tile* tiles;
   int ntiles;
   const MatDev* mats;
-  const CUtensorMap* tmaps;    // main loop, 4 per matrix: X[0], X[1], A, B (64x64 boxes, 128B swizzle)
+  const CUtensorMap* tmaps;    // main loop, 6 per matrix: X[0], X[1] (64x64 boxes), A, B (64 x 128-row
+                               // boxes), A, B (64x64 boxes, for transposed reads); 128B swizzle
   const CUtensorMap* emaps;    // epilogue, 4 kP per matrix: X[0], X[1], A, B (64-col x 32-row boxes) x planes
   const CUtensorMap* imaps;    // per call, 2 per matrix: caller input main loop / epilogue chunk
   const CUtensorMap* omaps;    // per call, 1 per matrix: caller output epilogue chunk
   const int* mflags;           // per call, per matrix: kFlag*
+  void* const* outs;           // per call, per matrix: caller output if kFlagDirect, else nullptr
   const float* inv;            // per matrix fp32(1/s)
   int mode;
   int xin;                     // which X buffer holds the current iterate
   int first_iter, final_iter;
   float a, b, c;
-  int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads
+  int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
+                               // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
+                               // stores, 128 = results by plain row stores instead of TMA
+                               // (results are wrong with any of 1, 2, 8, 16, 32)
   long long* stats;            // optional per-CTA wait-cycle counters (8 per CTA) or nullptr
 };
 
@@ -86,13 +93,21 @@ struct TileCfg {
   const CUtensorMap* B;
   int nk, row_a, col_b;        // k-blocks; this CTA's first row of A and of B
   bool a_mn, b_mn;             // operand stored MN-major (else K-major)
-  bool a_wide, b_wide;         // operand map has 128-row boxes (one TMA per 128-row half)
+  bool a_wide, b_wide;         // operand is a symmetric m x m buffer (A or B) of which only the
+                               // 256x256 blocks on or above the diagonal are stored; K-major
+                               // 128-row boxes, and blocks below the diagonal are read as the
+                               // transpose of the stored block (MN-major, 64x64 boxes, maps *mn)
+  const CUtensorMap* Amn;
+  const CUtensorMap* Bmn;
+  int pan_a, pan_b;            // 256-row panel index of the left / right operand rows
   bool diag;                   // symmetric phase, I == J: one panel serves both operands
   const CUtensorMap* ein;      // epilogue operand chunk map (update: X, poly: A)
   bool ein_tr;                 // operand chunk is M^T of a tall caller matrix
   const CUtensorMap* eout;     // result chunk map
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
   bool scaled;                 // first iteration of a folded matrix
+  __nv_bfloat16* optr;         // result buffer (row-major, leading dim old) for direct row stores
+  int old;
   int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
@@ -103,7 +118,7 @@ struct TileCfg {
 template <bool kEdge, int kP = 1>
 __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, uint32_t rank) {
   const MatDev& md = g.mats[tl.mat];
-  const CUtensorMap* maps = g.tmaps + 4 * tl.mat;
+  const CUtensorMap* maps = g.tmaps + 6 * tl.mat;
   const CUtensorMap* em = g.emaps + 4 * kP * tl.mat;
   const int fl = kEdge ? g.mflags[tl.mat] : 0;
   const bool fold = kEdge && g.first_iter && (fl & kFlagFolded);
@@ -111,6 +126,9 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   TileCfg c;
   c.scaled = fold;
   c.a_wide = c.b_wide = false;
+  c.Amn = c.Bmn = nullptr;
+  c.pan_a = tl.tm;
+  c.pan_b = tl.tn;
   c.ein = nullptr;
   c.ein_tr = false;
   c.eout_tr = false;
@@ -119,15 +137,21 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.a_mn = c.b_mn = fold && tall;
     c.nk = (md.n + kBK - 1) / kBK;
     c.eout = em + 2 * kP;
+    c.optr = reinterpret_cast<__nv_bfloat16*>(md.A);
+    c.old = md.ldm;
   } else if (g.mode == kModePoly) {
     c.A = c.B = maps + 2;
+    c.Amn = c.Bmn = maps + 4;
     c.a_mn = c.b_mn = false;
     c.a_wide = c.b_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
     c.ein = em + 2 * kP;
     c.eout = em + 3 * kP;
+    c.optr = reinterpret_cast<__nv_bfloat16*>(md.B);
+    c.old = md.ldm;
   } else {
     c.A = maps + 3;
+    c.Amn = maps + 5;
     c.a_mn = false;
     c.a_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
@@ -144,8 +168,12 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     if (kEdge && g.final_iter && (fl & kFlagDirect)) {
       c.eout = g.omaps + tl.mat;
       c.eout_tr = tall;
+      c.optr = reinterpret_cast<__nv_bfloat16*>(g.outs[tl.mat]);
+      c.old = md.n;                   // wide caller matrix: rows of n = cols
     } else {
       c.eout = em + kP * (g.xin ^ 1);
+      c.optr = reinterpret_cast<__nv_bfloat16*>(md.X[g.xin ^ 1]);
+      c.old = md.ldx;
     }
   }
   c.diag = (kP == 1) && (g.mode != kModeUpdate) && (tl.tm == tl.tn);
@@ -171,17 +199,6 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* f) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   return u;
-}
-
-// Mirrored store of a symmetric-output chunk: element (r, c0+j) -> (c0+j, r).
-// Lanes hold consecutive r, so each store instruction writes 64 contiguous bytes.
-__device__ __forceinline__ void mirror_chunk32(__nv_bfloat16* dst, int m, int ld, int r, int c0, const float* w) {
-  if (r >= m) return;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int c = c0 + j;
-    if (c < m) dst[(size_t)c * ld + r] = __float2bfloat16_rn(w[j]);
-  }
 }
 
 // Epilogue arithmetic of one half (32 columns) of a 32-row x 64-column chunk
@@ -249,6 +266,22 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
   }
 }
 
+// Store a finished 32 x 64 chunk from its (128B-swizzled) slot with plain
+// 16-byte global stores, 8 lanes per 128-byte row (coalesced): rows r0..r0+31
+// (< m), columns c0.. (16-byte units starting below ncols; the workspace rows
+// are padded to 8 elements and direct outputs have cols % 8 == 0).
+__device__ __forceinline__ void store_chunk_rows(const uint8_t* slot, __nv_bfloat16* dst, int ld, int r0, int c0,
+                                                 int m, int ncols, int lane) {
+  const int j = lane & 7;
+  const int c = c0 + 8 * j;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = 4 * i + (lane >> 3);
+    const uint4 v = *reinterpret_cast<const uint4*>(slot + sw128_off(row, j));
+    if (r0 + row < m && c < ncols) *reinterpret_cast<uint4*>(dst + (size_t)(r0 + row) * ld + c) = v;
+  }
+}
+
 // Operand half (32 values of row `lane`) of a chunk, packed as bf16 pairs.
 template <bool kTr>
 __device__ __forceinline__ void read_operand_half(const uint8_t* slot, int lane, int half32, uint32_t* pre) {
@@ -279,10 +312,8 @@ __device__ __forceinline__ void split3(float v, float& p0, float& p1, float& p2)
 // Epilogue arithmetic of one half (32 columns) of a 32-row x 64-column chunk
 // whose three planes sit in slots[0..2] (128B-swizzled 4 KB each): the operand
 // (poly: A, update: X) is p0 + p1 + p2, the fp32 result is split back into
-// the three slots in place; symmetric phases also store the mirrored planes
-// (plane stride ps elements) when mdst != nullptr.
-__device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slots, int lane, int half32, float* w,
-                                                __nv_bfloat16* mdst, int m, int ld, size_t ps, int r, int c0) {
+// the three slots in place.
+__device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slots, int lane, int half32, float* w) {
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq) {
 #pragma unroll
@@ -307,18 +338,6 @@ __device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slo
       *reinterpret_cast<uint4*>(slots + off) = pack8_bf16(p0);
       *reinterpret_cast<uint4*>(slots + kEpiSlotBytes + off) = pack8_bf16(p1);
       *reinterpret_cast<uint4*>(slots + 2 * kEpiSlotBytes + off) = pack8_bf16(p2);
-      if (mdst != nullptr && r < m) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = c0 + 16 * qq + 8 * v + j;
-          if (c < m) {
-            const size_t e = (size_t)c * ld + r;
-            mdst[e] = __float2bfloat16_rn(p0[j]);
-            mdst[ps + e] = __float2bfloat16_rn(p1[j]);
-            mdst[2 * ps + e] = __float2bfloat16_rn(p2[j]);
-          }
-        }
-      }
     }
   }
 }
@@ -349,9 +368,6 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
     // buffer 1 (second half of the big chain)
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
     const int ncols = (mode == kModeUpdate) ? md.n : md.m;
-    const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
-    __nv_bfloat16* mdst = mirror ? reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B) : nullptr;
-    const size_t ps = (size_t)md.m * md.ldm;
 #pragma unroll 1
     for (int k = 0; k < kEpiChunks; ++k) {
       const int c0 = tl.tn * kBN + half * (kBN / 2) + k * kEpiCols;
@@ -377,7 +393,7 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
         tmem_ld32(t_row + kBN + k * kEpiCols + 32 * h, w2);
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
-        epilogue_math_p3(args, slots, lane, h, w, mdst, md.m, md.ldm, ps, r, c0 + 32 * h);
+        epilogue_math_p3(args, slots, lane, h, w);
       }
       fence_async_smem();
       __syncwarp();
@@ -475,7 +491,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * kBBytes;
           const int k0 = (args.dbg & 8) ? 0 : kb * kBK;   // dbg 8: every load hits the same (L2-resident) boxes
-          if (o.a_wide) {
+          if (o.a_wide && (kb >> 2) < o.pan_a) {                    // block below the diagonal
+            tma_load_2d_pair(a_dst, o.Amn, bar, o.row_a, k0 + pa);
+            tma_load_2d_pair(a_dst + kBoxBytes, o.Amn, bar, o.row_a + 64, k0 + pa);
+          } else if (o.a_wide) {
             tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);      // one 64 x 128 box
           } else if (!o.a_mn) {
             tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);
@@ -485,7 +504,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, o.row_a + 64, k0);
           }
           if (!o.diag) {          // diagonal tiles: the right operand is the left one
-            if (o.b_wide) {
+            if (o.b_wide && (kb >> 2) < o.pan_b) {
+              tma_load_2d_pair(b_dst, o.Bmn, bar, o.col_b, k0 + pb);
+              tma_load_2d_pair(b_dst + kBoxBytes, o.Bmn, bar, o.col_b + 64, k0 + pb);
+            } else if (o.b_wide) {
               tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b + pb);
             } else if (!o.b_mn) {
               tma_load_2d_pair(b_dst, o.B, bar, k0, o.col_b + pb);
@@ -513,7 +535,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         const TileCfg o = nxt;
         if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[t + ncl], rank);
         const int nkt = o.nk * kP * (kP + 1) / 2;       // kP = 3: six plane-pair segments
-        const uint32_t idesc = idesc_bf16(kBM, kBN, o.a_mn, o.b_mn);
+
         long long t0 = clock64();
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         st_wait_tempty += clock64() - t0;
@@ -523,7 +545,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         // accumulated in the other TMEM buffer (each chain sees half the
         // truncating adds; the epilogue sums the two).  One tile in flight.
         const int nsplit = (kP == 3) ? 5 * o.nk + o.nk / 2 : nkt;
+        int kin = 0;                  // k-block index within the current plane-pair segment
         for (int kb = 0; kb < nkt; ++kb) {
+          // per k-block operand layout: blocks of a symmetric buffer below
+          // the diagonal arrive transposed (MN-major)
+          const bool amn = o.a_mn || (o.a_wide && (kin >> 2) < o.pan_a);
+          const bool bmn = o.b_mn || (o.b_wide && (kin >> 2) < o.pan_b);
+          const uint32_t idesc = idesc_bf16(kBM, kBN, amn, bmn);
+          if (++kin == o.nk) kin = 0;
           long long t1 = clock64();
           mbar_wait(&full[stage], phase);
           const long long t1e = clock64();
@@ -538,10 +567,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
               // K-major: advance 32 bytes inside the 128B swizzle row;
               // MN-major: advance 16 K-rows (2 KB); LBO = 8 KB between the
               // two 64-element MN atoms of a 128-wide operand.
-              const uint64_t adesc = o.a_mn ? smem_desc_sw128(a_addr + k * 2048, kBoxBytes, 1024)
-                                            : smem_desc_sw128(a_addr + k * 32, 16, 1024);
-              const uint64_t bdesc = o.b_mn ? smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024)
-                                            : smem_desc_sw128(b_addr + k * 32, 16, 1024);
+              const uint64_t adesc = amn ? smem_desc_sw128(a_addr + k * 2048, kBoxBytes, 1024)
+                                         : smem_desc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bdesc = bmn ? smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024)
+                                         : smem_desc_sw128(b_addr + k * 32, 16, 1024);
               if (kP == 3 && kb >= nsplit)
                 umma_bf16_pair(tmem_base + kBN, adesc, bdesc, idesc, (kb != nsplit) || k != 0);
               else
@@ -572,8 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     // chunks, each staged in a 4 KB smem slot (128B-swizzled, so the
     // row-per-thread accesses are conflict-free).  The whole tile's operand
     // chunks (A for poly, X for update) are loaded by TMA while the tile's MMA
-    // runs; results leave by TMA store; the mirrored half of a symmetric
-    // output is stored directly (64 contiguous bytes per warp store).
+    // runs; results leave by TMA store.
     const int ew = warp - 2;
     const int q = warp & 3;
     const int half = ew >> 2;
@@ -630,8 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       const int r = r0 + lane;
       const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
       const int ncols = (mode == kModeUpdate) ? md.n : md.m;
-      const bool mirror = (mode != kModeUpdate) && (tl.tn != tl.tm);
-      __nv_bfloat16* mdst = reinterpret_cast<__nv_bfloat16*>(mode == kModeGram ? md.A : md.B);
+      const bool rowst = (args.dbg & 128) && !(kEdge && cfg.eout_tr);   // results by plain row stores
       int nvalid = 0;
 #pragma unroll 1
       for (int k = 0; k < kEpiChunks; ++k) {
@@ -645,7 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         if (kSl == 1 && k > 0) {
           // single staging slot (Gram: no epilogue operand): the previous
           // chunk's store must have left smem before this chunk is written
-          if (lane == 0) bulk_wait_read<0>();
+          if (lane == 0 && !rowst) bulk_wait_read<0>();
           __syncwarp();
         }
         if (kEdge && need_load && cfg.ein_tr != cfg.eout_tr) {
@@ -669,15 +696,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           for (int h = 0; h < 2; ++h) {
             if (c0 + 32 * h >= ncols) break;
             float w[32];
-            tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+            if (args.dbg & 16) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = 0.f;
+            } else {
+              tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+            }
             epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr);
-            if (mirror) mirror_chunk32(mdst, md.m, md.ldm, r, c0 + 32 * h, w);
           }
         }
-        if (kSl == 1) {
+        if (rowst) {
+          __syncwarp();
+          if (!(args.dbg & 32)) store_chunk_rows(slot, cfg.optr, cfg.old, r0, c0, md.m, ncols, lane);
+        } else if (kSl == 1) {
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(args.dbg & 32)) {
             if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slot, c0, r0);
             else tma_store_2d(cfg.eout, slot, r0, c0);
             bulk_commit();
@@ -691,7 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-        if (kSl > 1) {
+        if (kSl > 1 && !rowst && !(args.dbg & 32)) {
           for (int k = 0; k < nvalid; ++k) {
             if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
             else tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, r0, col0(tl, k));

@@ -134,7 +134,7 @@ struct Plan {
   void* meta = nullptr;         // device blob
   size_t meta_bytes = 0;
   // offsets into meta
-  size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0;
+  size_t o_mats = 0, o_tmaps = 0, o_emaps = 0, o_sym = 0, o_upd = 0, o_sym_r = 0, o_upd_r = 0;
   size_t o_elems = 0, o_cmat = 0, o_cidx = 0, o_nch = 0, o_part = 0, o_cnt = 0, o_inv = 0;
   // copy passes: scale/orient (rows: wide inputs, tr: tall inputs) and
   // finalize (tr: tall outputs, rows: wide outputs whose rows are not 16-byte multiples)
@@ -483,14 +483,18 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
 
   // tensor maps: main loop over all planes of a buffer stacked (plane p =
   // rows [p m, (p+1) m)), epilogue one map per plane (stores clip at row m)
-  std::vector<CUtensorMap> tmaps(4 * (size_t)count), emaps(4 * np * (size_t)count);
+  // (A and B: 128-row boxes for the stored blocks, 64x64 boxes for the
+  // transposed reads of the blocks below the diagonal, gemm_sm100.cuh)
+  std::vector<CUtensorMap> tmaps(6 * (size_t)count), emaps(4 * np * (size_t)count);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
     const int pr = (int)np * md.m;
-    if ((s = make_tmap(&tmaps[4 * i + 0], md.X[0], pr, md.n, md.ldx)) != PE_OK ||
-        (s = make_tmap(&tmaps[4 * i + 1], md.X[1], pr, md.n, md.ldx)) != PE_OK ||
-        (s = make_tmap(&tmaps[4 * i + 2], md.A, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
-        (s = make_tmap(&tmaps[4 * i + 3], md.B, pr, md.m, md.ldm, 64, 128)) != PE_OK) {
+    if ((s = make_tmap(&tmaps[6 * i + 0], md.X[0], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tmaps[6 * i + 1], md.X[1], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tmaps[6 * i + 2], md.A, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
+        (s = make_tmap(&tmaps[6 * i + 3], md.B, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
+        (s = make_tmap(&tmaps[6 * i + 4], md.A, pr, md.m, md.ldm)) != PE_OK ||
+        (s = make_tmap(&tmaps[6 * i + 5], md.B, pr, md.m, md.ldm)) != PE_OK) {
       delete P;
       return s;
     }
@@ -566,6 +570,12 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->o_emaps = bl.add(emaps, 128);
   P->o_sym = bl.add(sym);
   P->o_upd = bl.add(upd);
+  // the same lists reversed: consecutive phases walk the batch in opposite
+  // directions, so each phase starts on the buffers the previous one wrote
+  // last (still in L2)
+  std::vector<Tile> sym_r(sym.rbegin(), sym.rend()), upd_r(upd.rbegin(), upd.rend());
+  P->o_sym_r = bl.add(sym_r);
+  P->o_upd_r = bl.add(upd_r);
   for (int k = 0; k < 4; ++k) P->o_it[k] = bl.add(it[k]);
   P->o_smats = bl.add(smats);
   P->o_fmats = bl.add(fmats);
@@ -710,6 +720,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
   const CUtensorMap* d_omaps = d_imaps + 2 * count;
   void** d_in = d_ptrs;
+  void** d_outs_direct = d_ptrs + count;
   void** d_fin_src = d_ptrs + 2 * count;
   void** d_out = d_ptrs + 3 * count;
   const int src_f32 = (dtype == PE_FP32);
@@ -767,7 +778,9 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     const int fin = (t == T - 1);
     for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
       GemmArgs g;
-      g.tiles = at<Tile>(P, mode == kModeUpdate ? P->o_upd : P->o_sym);
+      static const bool alt = !(getenv("PE_ORDER") && !strcmp(getenv("PE_ORDER"), "fwd"));   // A/B knob
+      const bool rev = alt && ((3 * t + mode) & 1);
+      g.tiles = at<Tile>(P, mode == kModeUpdate ? (rev ? P->o_upd_r : P->o_upd) : (rev ? P->o_sym_r : P->o_sym));
       g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
       g.mats = at<MatDev>(P, P->o_mats);
       g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
@@ -775,6 +788,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
       g.imaps = d_imaps;
       g.omaps = d_omaps;
       g.mflags = at<int>(P, P->o_flags);
+      g.outs = d_outs_direct;
       g.inv = at<float>(P, P->o_inv);
       g.first_iter = (t == 0);
       g.mode = mode; g.xin = xin; g.final_iter = fin;
