@@ -127,6 +127,7 @@ def kind_work(shapes, T):
         by["scale"] += 4.0 * m * n
         if r > c:
             by["transpose_back"] += 4.0 * m * n
+    fl["fused"] = T * (fl["gram"] + fl["poly"] + fl["update"])    # one launch runs all 3T phases
     return fl, by
 
 

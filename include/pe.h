@@ -180,10 +180,12 @@ pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
  * their durations into ms[kind] and launch counts into counts[kind] for the
  * first `nkinds` kinds, and clears the pending list.  Kinds:
  *   0 norm (pe_norm_kernel)     1 scale/orient (pe_copy_kernel)
- *   2 Gram  3 poly  4 update (pe_gemm_sm100; fp32 calls: the three-plane instantiation)
- *   5 transpose-back (pe_copy_kernel)
+ *   2 Gram  3 poly  4 update (pe_gemm_sm100, one launch per phase; fp32 calls:
+ *   the three-plane instantiation)   5 transpose-back (pe_copy_kernel)
+ *   6 fused (pe_gemm_sm100 running every phase of the call in one launch;
+ *     bf16 with PE_FUSED=1 set in the environment, otherwise one launch per phase)
  */
-#define PE_PROFILE_KINDS 6
+#define PE_PROFILE_KINDS 7
 pe_status pe_profile_enable(pe_ctx ctx, int on);
 pe_status pe_profile_read(pe_ctx ctx, double* ms, int* counts, int nkinds);
 

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = [
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
 ]
-PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back"]
+PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PE_LIB_OVERRIDE") or os.path.join(_HERE, "libpe.so")   # override: A/B experiments only

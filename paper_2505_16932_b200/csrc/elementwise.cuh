@@ -36,6 +36,8 @@ struct NormArgs {
   unsigned int* counters;      // per matrix, zero at rest (self-resetting)
   float* inv;                  // per matrix: fp32(1 / s)
   int src_f32;                 // 1: fp32 input, 0: bf16
+  int* zero;                   // fused GEMM schedule: completion counters to clear, or nullptr
+  int nzero;
 };
 
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
@@ -52,6 +54,7 @@ __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
 __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a) {
   pdl_trigger();
   pdl_wait();
+  for (int i = blockIdx.x * kNormThreads + threadIdx.x; i < a.nzero; i += gridDim.x * kNormThreads) a.zero[i] = 0;
   const int blk = blockIdx.x;
   const int mat = a.chunk_mat[blk];
   const int ci = a.chunk_idx[blk];

@@ -74,21 +74,36 @@ struct GemmArgs {
   const CUtensorMap* imaps;    // per call, 2 per matrix: caller input main loop / epilogue chunk
   const CUtensorMap* omaps;    // per call, 1 per matrix: caller output epilogue chunk
   const int* mflags;           // per call, per matrix: kFlag*
-  void* const* outs;           // per call, per matrix: caller output if kFlagDirect, else nullptr
   const float* inv;            // per matrix fp32(1/s)
+  // one phase per launch (nphase == 0): the phase of every tile
   int mode;
   int xin;                     // which X buffer holds the current iterate
   int first_iter, final_iter;
   float a, b, c;
+  // fused schedule (nphase = 3T > 0): one launch runs every phase of every
+  // matrix; Tile::pad is the phase p (iteration p / 3, mode p % 3), tiles are
+  // listed in a dependency-respecting order and a tile of phase p > 0 waits
+  // until done[mat * nphase + p - 1] reaches need[mat * 3 + (p - 1) % 3]
+  // (every epilogue warp of every tile of that phase has published)
+  int nphase;
+  const float* coef;           // per iteration fp32 (a, b, c)
+  int* done;                   // per (matrix, phase) completion counters, zero at launch
+  const int* need;             // per (matrix, mode): 2 * kEpiWarps * tiles
   int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
                                // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
-                               // stores, 128 = results by plain row stores instead of TMA
-                               // (results are wrong with any of 1, 2, 8, 16, 32)
+                               // stores, 256 = every result store to the same box (results are
+                               // wrong with any of these)
   long long* stats;            // optional per-CTA wait-cycle counters (8 per CTA) or nullptr
 };
 
 // Everything the three roles need to know about one tile.
 struct TileCfg {
+  int mode, xin;               // phase of the tile (see GemmArgs)
+  bool first, last;            // first / last iteration
+  float a, b, c;               // the iteration's coefficients
+  const int* dep;              // fused: counter to wait for before reading operands, or nullptr
+  int dep_need;
+  int* pub;                    // fused: counter to publish this tile's results to, or nullptr
   const CUtensorMap* A;        // main-loop maps of the left / right operand
   const CUtensorMap* B;
   int nk, row_a, col_b;        // k-blocks; this CTA's first row of A and of B
@@ -106,8 +121,6 @@ struct TileCfg {
   const CUtensorMap* eout;     // result chunk map
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
   bool scaled;                 // first iteration of a folded matrix
-  __nv_bfloat16* optr;         // result buffer (row-major, leading dim old) for direct row stores
-  int old;
   int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
@@ -120,10 +133,36 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   const MatDev& md = g.mats[tl.mat];
   const CUtensorMap* maps = g.tmaps + 6 * tl.mat;
   const CUtensorMap* em = g.emaps + 4 * kP * tl.mat;
-  const int fl = kEdge ? g.mflags[tl.mat] : 0;
-  const bool fold = kEdge && g.first_iter && (fl & kFlagFolded);
-  const bool tall = kEdge && (fl & kFlagTall) != 0;
   TileCfg c;
+  c.dep = nullptr;
+  c.pub = nullptr;
+  c.dep_need = 0;
+  if (g.nphase > 0) {
+    const int p = tl.pad, t = p / 3;
+    c.mode = p - 3 * t;
+    c.xin = t & 1;
+    c.first = (t == 0);
+    c.last = (3 * t + 3 == g.nphase);
+    c.a = g.coef[3 * t];
+    c.b = g.coef[3 * t + 1];
+    c.c = g.coef[3 * t + 2];
+    c.pub = g.done + tl.mat * g.nphase + p;
+    if (p > 0) {
+      c.dep = c.pub - 1;
+      c.dep_need = g.need[tl.mat * 3 + (p - 1) % 3];
+    }
+  } else {
+    c.mode = g.mode;
+    c.xin = g.xin;
+    c.first = g.first_iter != 0;
+    c.last = g.final_iter != 0;
+    c.a = g.a;
+    c.b = g.b;
+    c.c = g.c;
+  }
+  const int fl = kEdge ? g.mflags[tl.mat] : 0;
+  const bool fold = kEdge && c.first && (fl & kFlagFolded);
+  const bool tall = kEdge && (fl & kFlagTall) != 0;
   c.scaled = fold;
   c.a_wide = c.b_wide = false;
   c.Amn = c.Bmn = nullptr;
@@ -132,14 +171,12 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   c.ein = nullptr;
   c.ein_tr = false;
   c.eout_tr = false;
-  if (g.mode == kModeGram) {
-    c.A = c.B = fold ? g.imaps + 2 * tl.mat : maps + g.xin;
+  if (c.mode == kModeGram) {
+    c.A = c.B = fold ? g.imaps + 2 * tl.mat : maps + c.xin;
     c.a_mn = c.b_mn = fold && tall;
     c.nk = (md.n + kBK - 1) / kBK;
     c.eout = em + 2 * kP;
-    c.optr = reinterpret_cast<__nv_bfloat16*>(md.A);
-    c.old = md.ldm;
-  } else if (g.mode == kModePoly) {
+  } else if (c.mode == kModePoly) {
     c.A = c.B = maps + 2;
     c.Amn = c.Bmn = maps + 4;
     c.a_mn = c.b_mn = false;
@@ -147,8 +184,6 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.nk = (md.m + kBK - 1) / kBK;
     c.ein = em + 2 * kP;
     c.eout = em + 3 * kP;
-    c.optr = reinterpret_cast<__nv_bfloat16*>(md.B);
-    c.old = md.ldm;
   } else {
     c.A = maps + 3;
     c.Amn = maps + 5;
@@ -161,22 +196,18 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
       c.ein = g.imaps + 2 * tl.mat + 1;
       c.ein_tr = tall;
     } else {
-      c.B = maps + g.xin;
+      c.B = maps + c.xin;
       c.b_mn = true;
-      c.ein = em + kP * g.xin;
+      c.ein = em + kP * c.xin;
     }
-    if (kEdge && g.final_iter && (fl & kFlagDirect)) {
+    if (kEdge && c.last && (fl & kFlagDirect)) {
       c.eout = g.omaps + tl.mat;
       c.eout_tr = tall;
-      c.optr = reinterpret_cast<__nv_bfloat16*>(g.outs[tl.mat]);
-      c.old = md.n;                   // wide caller matrix: rows of n = cols
     } else {
-      c.eout = em + kP * (g.xin ^ 1);
-      c.optr = reinterpret_cast<__nv_bfloat16*>(md.X[g.xin ^ 1]);
-      c.old = md.ldx;
+      c.eout = em + kP * (c.xin ^ 1);
     }
   }
-  c.diag = (kP == 1) && (g.mode != kModeUpdate) && (tl.tm == tl.tn);
+  c.diag = (kP == 1) && (c.mode != kModeUpdate) && (tl.tm == tl.tn);
   c.prow = (kP == 1) ? 0 : md.m;
   c.row_a = tl.tm * kBM + (int)rank * (kBM / 2);
   c.col_b = tl.tn * kBN + (int)rank * (kBN / 2);
@@ -220,7 +251,7 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq) {           // 16 columns at a time (register pressure)
     float* wq = w + 16 * qq;
-    if (g.mode != kModeGram) {
+    if (cfg.mode != kModeGram) {
       float o[16];
       if (kEdge && pre != nullptr) {
 #pragma unroll
@@ -238,12 +269,12 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = __bfloat162float(sp[(half32 * 32 + qq * 16 + j) * 32]);
       }
-      if (g.mode == kModePoly) {
+      if (cfg.mode == kModePoly) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(g.b, o[j]), __fmul_rn(g.c, wq[j]));
+        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.b, o[j]), __fmul_rn(cfg.c, wq[j]));
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(g.a, o[j]), wq[j]);
+        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.a, o[j]), wq[j]);
         if (kEdge && cfg.scaled) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv);
@@ -263,22 +294,6 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
       for (int j = 0; j < 16; ++j) sp[(half32 * 32 + qq * 16 + j) * 32] = __float2bfloat16_rn(wq[j]);
     }
-  }
-}
-
-// Store a finished 32 x 64 chunk from its (128B-swizzled) slot with plain
-// 16-byte global stores, 8 lanes per 128-byte row (coalesced): rows r0..r0+31
-// (< m), columns c0.. (16-byte units starting below ncols; the workspace rows
-// are padded to 8 elements and direct outputs have cols % 8 == 0).
-__device__ __forceinline__ void store_chunk_rows(const uint8_t* slot, __nv_bfloat16* dst, int ld, int r0, int c0,
-                                                 int m, int ncols, int lane) {
-  const int j = lane & 7;
-  const int c = c0 + 8 * j;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = 4 * i + (lane >> 3);
-    const uint4 v = *reinterpret_cast<const uint4*>(slot + sw128_off(row, j));
-    if (r0 + row < m && c < ncols) *reinterpret_cast<uint4*>(dst + (size_t)(r0 + row) * ld + c) = v;
   }
 }
 
@@ -313,14 +328,14 @@ __device__ __forceinline__ void split3(float v, float& p0, float& p1, float& p2)
 // whose three planes sit in slots[0..2] (128B-swizzled 4 KB each): the operand
 // (poly: A, update: X) is p0 + p1 + p2, the fp32 result is split back into
 // the three slots in place.
-__device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slots, int lane, int half32, float* w) {
+__device__ __forceinline__ void epilogue_math_p3(const TileCfg& cfg, uint8_t* slots, int lane, int half32, float* w) {
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       float* wv = w + 16 * qq + 8 * v;
       const uint32_t off = sw128_off(lane, half32 * 4 + qq * 2 + v);
-      if (g.mode != kModeGram) {
+      if (cfg.mode != kModeGram) {
         float o0[8], o1[8], o2[8];
         bf16x8_to_f32(*reinterpret_cast<const uint4*>(slots + off), o0);
         bf16x8_to_f32(*reinterpret_cast<const uint4*>(slots + kEpiSlotBytes + off), o1);
@@ -328,8 +343,8 @@ __device__ __forceinline__ void epilogue_math_p3(const GemmArgs& g, uint8_t* slo
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float o = __fadd_rn(__fadd_rn(o0[j], o1[j]), o2[j]);
-          wv[j] = (g.mode == kModePoly) ? __fadd_rn(__fmul_rn(g.b, o), __fmul_rn(g.c, wv[j]))
-                                        : __fadd_rn(__fmul_rn(g.a, o), wv[j]);
+          wv[j] = (cfg.mode == kModePoly) ? __fadd_rn(__fmul_rn(cfg.b, o), __fmul_rn(cfg.c, wv[j]))
+                                        : __fadd_rn(__fmul_rn(cfg.a, o), wv[j]);
         }
       }
       float p0[8], p1[8], p2[8];
@@ -352,14 +367,15 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
   const int ew = warp - 2;
   const int q = warp & 3;
   const int half = ew >> 2;
-  const int mode = args.mode;
-  const bool need_load = (mode != kModeGram);
   const int row_off = (int)rank * (kBM / 2) + q * 32;
   uint32_t acc_phase = 0, xphase = 0;
   for (int t = cid; t < args.ntiles; t += ncl) {
     const Tile tl = args.tiles[t];
     const MatDev md = args.mats[tl.mat];
     const TileCfg cfg = tile_cfg<false, 3>(args, tl, rank);
+    const int mode = cfg.mode;
+    const bool need_load = (mode != kModeGram);
+    if (lane == 0 && need_load && cfg.dep != nullptr) acquire_counter(cfg.dep, cfg.dep_need);
     mbar_wait(&tfull[0], acc_phase);
     tc_fence_after();
     const int r0 = tl.tm * kBM + row_off;
@@ -393,7 +409,7 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
         tmem_ld32(t_row + kBN + k * kEpiCols + 32 * h, w2);
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
-        epilogue_math_p3(args, slots, lane, h, w);
+        epilogue_math_p3(cfg, slots, lane, h, w);
       }
       fence_async_smem();
       __syncwarp();
@@ -405,7 +421,10 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive_remote(tempty_leader0);
+    if (lane == 0) {
+      mbar_arrive_remote(tempty_leader0);
+      if (cfg.pub != nullptr) publish_stores(cfg.pub);
+    }
     acc_phase ^= 1;
   }
   if (lane == 0) bulk_wait<0>();
@@ -433,7 +452,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int mode = args.mode;
   const uint32_t rank = cluster_rank();
   const bool leader = (rank == 0);
   const int cid = blockIdx.x >> 1;
@@ -475,6 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       for (int t = cid; t < args.ntiles; t += ncl) {
         const TileCfg o = nxt;
         if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[t + ncl], rank);   // off the critical path
+        if (o.dep != nullptr) acquire_counter(o.dep, o.dep_need);    // fused: operands are complete
         // kP = 3: six plane-pair segments (i, j), small terms first:
         // (2,0) (1,1) (0,2) (1,0) (0,1) (0,0).  The tensor core adds each
         // K=16 step into the fp32 accumulator with truncation; with the big
@@ -607,17 +626,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     const int half = ew >> 2;
     uint8_t* slots = epi_smem + ew * kSl * kEpiSlotBytes;
     uint64_t* xbar = xbars + ew * kSl;
-    const bool need_load = (mode != kModeGram) && !(args.dbg & 3);
+    auto needs_load = [&](const TileCfg& c2) { return c2.mode != kModeGram && !(args.dbg & 3); };
     const bool do_work = !(args.dbg & 1);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const int row_off = (int)rank * (kBM / 2) + q * 32;
 
     auto col0 = [&](const Tile& tl2, int kk) { return tl2.tn * kBN + half * (kBN / 2) + kk * kEpiCols; };
-    auto ncols_of = [&](const Tile& tl2) {
+    auto ncols_of = [&](const Tile& tl2, const TileCfg& c2) {
       const MatDev& m2 = args.mats[tl2.mat];
-      return (mode == kModeUpdate) ? m2.n : m2.m;
+      return (c2.mode == kModeUpdate) ? m2.n : m2.m;
     };
     auto issue_tile = [&](const Tile& tl2, const TileCfg& c2, int nc) {
+      if (c2.dep != nullptr) acquire_counter(c2.dep, c2.dep_need);   // fused: the operand is complete
       const int r0 = tl2.tm * kBM + row_off;
       for (int kk = 0; kk < kEpiChunks && col0(tl2, kk) < nc; ++kk) {
         const int c0 = col0(tl2, kk);
@@ -636,8 +656,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     if (cid < args.ntiles) {
       ntl = args.tiles[cid];
       ncfg = tile_cfg<kEdge>(args, ntl, rank);
-      nnc = ncols_of(ntl);
-      if (lane == 0 && need_load) issue_tile(ntl, ncfg, nnc);
+      nnc = ncols_of(ntl, ncfg);
+      if (lane == 0 && needs_load(ncfg)) issue_tile(ntl, ncfg, nnc);
     }
     for (int t = cid; t < args.ntiles; t += ncl) {
       const Tile tl = ntl;
@@ -647,8 +667,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       if (has_next) {                        // next tile's description, loaded early
         ntl = args.tiles[t + ncl];
         ncfg = tile_cfg<kEdge>(args, ntl, rank);
-        nnc = ncols_of(ntl);
+        nnc = ncols_of(ntl, ncfg);
       }
+      const bool need_load = needs_load(cfg);
       const float inv = cfg.scaled ? args.inv[tl.mat] : 1.0f;
       long long t2 = clock64();
       mbar_wait(&tfull[acc], acc_phase);
@@ -657,8 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       const int r0 = tl.tm * kBM + row_off;
       const int r = r0 + lane;
       const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
-      const int ncols = (mode == kModeUpdate) ? md.n : md.m;
-      const bool rowst = (args.dbg & 128) && !(kEdge && cfg.eout_tr);   // results by plain row stores
+      const int ncols = (cfg.mode == kModeUpdate) ? md.n : md.m;
       int nvalid = 0;
 #pragma unroll 1
       for (int k = 0; k < kEpiChunks; ++k) {
@@ -672,7 +692,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         if (kSl == 1 && k > 0) {
           // single staging slot (Gram: no epilogue operand): the previous
           // chunk's store must have left smem before this chunk is written
-          if (lane == 0 && !rowst) bulk_wait_read<0>();
+          if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
         }
         if (kEdge && need_load && cfg.ein_tr != cfg.eout_tr) {
@@ -705,10 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr);
           }
         }
-        if (rowst) {
-          __syncwarp();
-          if (!(args.dbg & 32)) store_chunk_rows(slot, cfg.optr, cfg.old, r0, c0, md.m, ncols, lane);
-        } else if (kSl == 1) {
+        if (kSl == 1) {
           fence_async_smem();
           __syncwarp();
           if (lane == 0 && !(args.dbg & 32)) {
@@ -725,15 +742,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
-        if (kSl > 1 && !rowst && !(args.dbg & 32)) {
+        if (kSl > 1 && !(args.dbg & 32)) {
           for (int k = 0; k < nvalid; ++k) {
-            if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
+            if (args.dbg & 256) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, k * kEpiCols, row_off);
+            else if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, col0(tl, k), r0);
             else tma_store_2d(cfg.eout, slots + k * kEpiSlotBytes, r0, col0(tl, k));
           }
           bulk_commit();
         }
-        bulk_wait_read<0>();          // this tile's stores have left smem: slots are free
-        if (has_next && need_load) issue_tile(ntl, ncfg, nnc);
+        if (cfg.pub != nullptr) publish_stores(cfg.pub);   // fused: stores complete, counted
+        else bulk_wait_read<0>();     // this tile's stores have left smem: slots are free
+        if (has_next && needs_load(ncfg)) issue_tile(ntl, ncfg, nnc);
       }
       __syncwarp();
       acc ^= 1;

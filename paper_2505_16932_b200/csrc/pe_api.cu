@@ -141,6 +141,11 @@ struct Plan {
   size_t o_smats = 0, o_fmats = 0, o_x0 = 0, o_flags = 0, o_it[4] = {0, 0, 0, 0};
   int n_it[4] = {0, 0, 0, 0};
   int n_sym = 0, n_upd = 0, n_chunks = 0;
+  size_t o_need = 0;            // per (matrix, mode) completion target of the fused schedule
+  // fused schedule (one launch for all 3T phases), built for one T at a time
+  int fused_T = 0, n_fused = 0;
+  Tile* fused = nullptr;
+  size_t fused_cap = 0;
   bool long_k[3] = {true, true, true};   // per GEMM mode: 5-stage (else 4-stage) instantiation
   size_t ws_needed = 0;
   uint64_t last_use = 0;
@@ -181,6 +186,8 @@ struct pe_ctx_s {
   std::vector<cudaEvent_t> host_ev;
 
   int last_launches = 0;
+  int* done = nullptr;          // fused schedule completion counters (cleared by the norm kernel)
+  size_t done_cap = 0;
   int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1/3 are set)
   long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
 
@@ -194,6 +201,7 @@ struct pe_ctx_s {
 
 static void free_plan(Plan* p) {
   if (p->meta) cudaFree(p->meta);
+  if (p->fused) cudaFree(p->fused);
   delete p;
 }
 
@@ -330,6 +338,7 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   for (auto e : c->host_ev) cudaEventDestroy(e);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->stats) cudaFree(c->stats);
+  if (c->done) cudaFree(c->done);
   delete c;
   return PE_OK;
 }
@@ -409,7 +418,8 @@ static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
 // per-call upload: 4*count pointers, then 3 tensor maps per matrix (caller
 // input main loop, caller input epilogue chunk, caller output epilogue chunk)
 static size_t call_ptr_bytes(int count) { return rup((size_t)4 * count * sizeof(void*), 128); }
-static size_t call_bytes(int count) { return call_ptr_bytes(count) + (size_t)3 * count * sizeof(CUtensorMap); }
+static size_t call_coef_off(int count) { return call_ptr_bytes(count) + (size_t)3 * count * sizeof(CUtensorMap); }
+static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size_t)3 * T * sizeof(float); }
 
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
@@ -591,6 +601,13 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->o_cnt = bl.add(cnt);
   std::vector<float> inv(count, 0.f);
   P->o_inv = bl.add(inv);
+  std::vector<int> need(3 * (size_t)count);
+  for (int i = 0; i < count; ++i) {
+    const int nm = cdiv(mats[i].m, kBN), nn = cdiv(mats[i].n, kBN);
+    need[3 * i + kModeGram] = need[3 * i + kModePoly] = 2 * kEpiWarps * nm * (nm + 1) / 2;
+    need[3 * i + kModeUpdate] = 2 * kEpiWarps * nm * nn;
+  }
+  P->o_need = bl.add(need);
 
   if (cudaMalloc(&P->meta, bl.host.size()) != cudaSuccess) {
     cudaGetLastError();
@@ -628,6 +645,77 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->last_use = ++c->use_clock;
   c->plans.push_back(P);
   *out = P;
+  return PE_OK;
+}
+
+// Tile order of the fused schedule (GemmArgs::nphase): a window of matrices
+// advances one phase per round, every matrix of the window emitting all tiles
+// of its next phase; matrices join (largest cost first) while a round has
+// fewer than ~3 tiles per cluster or fewer than two matrices.  Phase p of a
+// matrix is emitted one round after phase p - 1, so the list is in dependency
+// order (no deadlock under static round-robin assignment) and the tiles a
+// cluster waits for were issued about a round earlier; the window's buffers
+// stay L2-resident across its phases.
+static void build_fused_order(const std::vector<MatDev>& mats, int T, int nclusters, std::vector<Tile>& out) {
+  const int count = (int)mats.size();
+  auto ntiles = [&](int i, int mode) {
+    const int nm = cdiv(mats[i].m, kBN), nn = cdiv(mats[i].n, kBN);
+    return mode == kModeUpdate ? nm * nn : nm * (nm + 1) / 2;
+  };
+  auto emit = [&](int i, int p) {
+    const int nm = cdiv(mats[i].m, kBN), nn = cdiv(mats[i].n, kBN);
+    if (p % 3 == kModeUpdate) {
+      for (int tn = 0; tn < nn; ++tn)
+        for (int tm = 0; tm < nm; ++tm) out.push_back({i, tm, tn, p});
+    } else {
+      for (int tm = 0; tm < nm; ++tm)
+        for (int tn = tm; tn < nm; ++tn) out.push_back({i, tm, tn, p});
+    }
+  };
+  std::vector<double> cost(count);
+  for (int i = 0; i < count; ++i) cost[i] = 3.0 * mats[i].m * (double)mats[i].m * mats[i].n + (double)mats[i].m * mats[i].m * mats[i].m;
+  std::vector<int> order(count);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  const int nph = 3 * T;
+  static const int round_mult = getenv("PE_FUSED_ROUND") ? atoi(getenv("PE_FUSED_ROUND")) : 3;   // experiments
+  const int round_min = round_mult * nclusters;
+  std::vector<int> ph(count, 0), window, keep;
+  size_t next = 0;
+  out.clear();
+  while (next < order.size() || !window.empty()) {
+    int est = 0;
+    for (int i : window) est += ntiles(i, ph[i] % 3);
+    while (next < order.size() && (est < round_min || window.size() < 2)) {
+      const int i = order[next++];
+      window.push_back(i);
+      est += ntiles(i, 0);
+    }
+    keep.clear();
+    for (int i : window) {
+      emit(i, ph[i]);
+      if (++ph[i] < nph) keep.push_back(i);
+    }
+    window.swap(keep);
+  }
+}
+
+static pe_status ensure_fused(pe_ctx c, Plan* P, int T) {
+  if (P->fused_T == T) return PE_OK;
+  std::vector<Tile> order;
+  build_fused_order(P->mats, T, c->num_sms / 2, order);
+  const size_t bytes = order.size() * sizeof(Tile);
+  PE_CUDA(cudaDeviceSynchronize());          // the previous list may still be in use
+  if (bytes > P->fused_cap) {
+    if (P->fused) cudaFree(P->fused);
+    P->fused = nullptr;
+    P->fused_cap = 0;
+    if (cudaMalloc(&P->fused, bytes) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+    P->fused_cap = bytes;
+  }
+  PE_CUDA(cudaMemcpy(P->fused, order.data(), bytes, cudaMemcpyHostToDevice));
+  P->n_fused = (int)order.size();
+  P->fused_T = T;
   return PE_OK;
 }
 
@@ -691,8 +779,27 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   // per-call pointers: [in | outs_direct | fin_src | out] + caller tensor maps
   const int T = iters;
   const int xfinal = T & 1;
+  // fused schedule: every GEMM phase in one launch (bf16, opt-in with
+  // PE_FUSED=1; measured equal to one launch per phase on the GPT-2 sets and
+  // within noise on Llama, profiles/r1_variants.md)
+  static const bool fused_on = getenv("PE_FUSED") && strcmp(getenv("PE_FUSED"), "0") != 0;
+  const bool fused = fused_on && dtype == PE_BF16;
+  const int nq = (c->degree + 1) / 2;
+  if (fused) {
+    if ((s = ensure_fused(c, P, T)) != PE_OK) return s;
+    const size_t need_done = (size_t)count * 3 * T;
+    if (need_done > c->done_cap) {
+      PE_CUDA(cudaDeviceSynchronize());
+      if (c->done) cudaFree(c->done);
+      c->done = nullptr;
+      c->done_cap = 0;
+      if (cudaMalloc(&c->done, need_done * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+      PE_CUDA(cudaMemset(c->done, 0, need_done * sizeof(int)));
+      c->done_cap = need_done;
+    }
+  }
   CallSlot* cs = nullptr;
-  if ((s = take_call_slot(c, call_bytes(count), &cs)) != PE_OK) return s;
+  if ((s = take_call_slot(c, call_bytes(count, T), &cs)) != PE_OK) return s;
   void** h = reinterpret_cast<void**>(cs->h);
   const size_t omap_off = call_ptr_bytes(count);
   CUtensorMap* h_maps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
@@ -711,8 +818,14 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     if (dtype == PE_BF16 && (fl & kFlagDirect))
       if ((s = make_emap(&h_maps[2 * count + i], out[i], md.rows, md.cols, md.cols, md.tall)) != PE_OK) return s;
   }
-  PE_CUDA(cudaMemcpyAsync(cs->d, h, dtype == PE_BF16 ? call_bytes(count) : 4 * count * sizeof(void*),
-                          cudaMemcpyHostToDevice, st));
+  float* h_coef = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(h) + call_coef_off(count));
+  for (int t = 0; t < T; ++t) {
+    const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
+    h_coef[3 * t] = (float)tup[0];
+    h_coef[3 * t + 1] = (float)tup[1];
+    h_coef[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
+  }
+  PE_CUDA(cudaMemcpyAsync(cs->d, h, call_bytes(count, T), cudaMemcpyHostToDevice, st));
   PE_CUDA(cudaEventRecord(cs->done, st));
   cs->armed = true;
   void** d_ptrs = reinterpret_cast<void**>(cs->d);
@@ -720,7 +833,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
   const CUtensorMap* d_omaps = d_imaps + 2 * count;
   void** d_in = d_ptrs;
-  void** d_outs_direct = d_ptrs + count;
+  const float* d_coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + call_coef_off(count));
   void** d_fin_src = d_ptrs + 2 * count;
   void** d_out = d_ptrs + 3 * count;
   const int src_f32 = (dtype == PE_FP32);
@@ -737,6 +850,8 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   na.counters = at<unsigned>(P, P->o_cnt);
   na.inv = at<float>(P, P->o_inv);
   na.src_f32 = src_f32;
+  na.zero = fused ? c->done : nullptr;
+  na.nzero = fused ? count * 3 * T : 0;
   { ProfScope ps(c, 0, st);
     launch(pe_norm_kernel, P->n_chunks, kNormThreads, 0, st, na); }
   ++launches;
@@ -770,31 +885,50 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   copy_pass(1, true, false);
 
   // 3) T iterations
-  const int nq = (c->degree + 1) / 2;
-  for (int t = 0; t < T; ++t) {
+  auto base_args = [&](GemmArgs& g) {
+    g.mats = at<MatDev>(P, P->o_mats);
+    g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
+    g.emaps = at<CUtensorMap>(P, P->o_emaps);
+    g.imaps = d_imaps;
+    g.omaps = d_omaps;
+    g.mflags = at<int>(P, P->o_flags);
+    g.inv = at<float>(P, P->o_inv);
+    g.nphase = 0;
+    g.coef = d_coef;
+    g.done = c->done;
+    g.need = at<int>(P, P->o_need);
+    g.dbg = c->dbg;
+    g.stats = nullptr;
+  };
+  if (fused) {
+    // one persistent launch: all 3T phases of all matrices, dataflow-ordered
+    GemmArgs g;
+    base_args(g);
+    g.tiles = P->fused;
+    g.ntiles = P->n_fused;
+    g.nphase = 3 * T;
+    g.mode = 0; g.xin = 0; g.first_iter = 0; g.final_iter = 0;
+    g.a = g.b = g.c = 0.f;
+    const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);
+    ProfScope ps(c, 6, st);
+    launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, gemm_smem_bytes<kLongStages, 2>(), st, g);
+    ++launches;
+  }
+  for (int t = 0; t < T && !fused; ++t) {
     const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
     const float fa = (float)tup[0], fb = (float)tup[1], fc = (nq == 3) ? (float)tup[2] : 0.0f;
     const int xin = t & 1;
     const int fin = (t == T - 1);
     for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
       GemmArgs g;
+      base_args(g);
       static const bool alt = !(getenv("PE_ORDER") && !strcmp(getenv("PE_ORDER"), "fwd"));   // A/B knob
       const bool rev = alt && ((3 * t + mode) & 1);
       g.tiles = at<Tile>(P, mode == kModeUpdate ? (rev ? P->o_upd_r : P->o_upd) : (rev ? P->o_sym_r : P->o_sym));
       g.ntiles = mode == kModeUpdate ? P->n_upd : P->n_sym;
-      g.mats = at<MatDev>(P, P->o_mats);
-      g.tmaps = at<CUtensorMap>(P, P->o_tmaps);
-      g.emaps = at<CUtensorMap>(P, P->o_emaps);
-      g.imaps = d_imaps;
-      g.omaps = d_omaps;
-      g.mflags = at<int>(P, P->o_flags);
-      g.outs = d_outs_direct;
-      g.inv = at<float>(P, P->o_inv);
       g.first_iter = (t == 0);
       g.mode = mode; g.xin = xin; g.final_iter = fin;
       g.a = fa; g.b = fb; g.c = fc;
-      g.dbg = c->dbg;
-      g.stats = nullptr;
       if (c->dbg & 4) {
         if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
         g.stats = c->stats + (size_t)mode * 2048;

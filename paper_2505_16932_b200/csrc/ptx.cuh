@@ -230,4 +230,35 @@ template <int N> __device__ __forceinline__ void bulk_wait() {
 // make this thread's generic-proxy smem writes visible to the async proxy (TMA)
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// ---- cross-CTA dataflow (fused schedule): a tile's TMA stores are published
+// through a global counter, and consumers acquire it before their TMA loads.
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Called by the thread that issued (and committed) the bulk stores: wait until
+// they are complete, order them before the release, count them.
+__device__ __forceinline__ void publish_stores(int* ctr) {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  fence_async_global();
+  red_release_add_gpu(ctr, 1);
+}
+// Wait until *ctr >= need, then order the caller's later TMA loads after it.
+// A wait of more than 2^24 polls (several seconds) traps instead of hanging the GPU.
+__device__ __forceinline__ void acquire_counter(const int* ctr, int need) {
+  if (ld_acquire_gpu(ctr) < need) {
+    uint32_t spins = 0;
+    while (ld_acquire_gpu(ctr) < need) {
+      __nanosleep(32);
+      if (++spins == (1u << 24)) __trap();
+    }
+  }
+  fence_async_global();
+}
+
 }  // namespace pe
