@@ -50,7 +50,11 @@
 // 6x the k-blocks (plane p of a buffer = rows [p m, (p+1) m) of its stacked
 // tensor map); the epilogue sums the operand planes, applies the fp32
 // arithmetic and splits the result into planes again.  No folding, no
-// diagonal single-panel loads.
+// diagonal single-panel loads.  The tensor core adds every K=16 step into the
+// fp32 accumulator with truncation, so the accumulation order is arranged to
+// keep each truncating chain short (small plane products first, the big
+// p0 q0 chain in passes of <= 16 K blocks split over both TMEM buffers, an
+// fp32 running sum across passes; see p3_passes).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -75,6 +79,7 @@ struct GemmArgs {
   const CUtensorMap* omaps;    // per call, 1 per matrix: caller output epilogue chunk
   const int* mflags;           // per call, per matrix: kFlag*
   const float* inv;            // per matrix fp32(1/s)
+  float* scratch;              // kP = 3: 128 x 256 fp32 per CTA (running sum of the K passes)
   // one phase per launch (nphase == 0): the phase of every tile
   int mode;
   int xin;                     // which X buffer holds the current iterate
@@ -315,6 +320,12 @@ __device__ __forceinline__ void read_operand_half(const uint8_t* slot, int lane,
 }
 
 // ---------------------------------------------------------------- fp32 (kP = 3)
+// The big (0,0) plane chain of a tile is cut into passes of at most 16 K
+// blocks; within a pass it is split over the two TMEM buffers, and the
+// epilogue carries the fp32 running sum of the passes in a per-CTA global
+// scratch tile.  Every truncating accumulator chain is <= 8 K blocks (32
+// MMA steps) long whatever K is.
+__host__ __device__ constexpr int p3_passes(int nk) { return nk > 16 ? (nk + 15) / 16 : 1; }
 // Split v into three bf16 planes: v - p0 and (v - p0) - p1 are exact in fp32
 // (Sterbenz), so p0 + p1 + p2 carries v's 24 significand bits.
 __device__ __forceinline__ void split3(float v, float& p0, float& p1, float& p2) {
@@ -368,6 +379,10 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
   const int q = warp & 3;
   const int half = ew >> 2;
   const int row_off = (int)rank * (kBM / 2) + q * 32;
+  // per-CTA fp32 running sum of the passes, [64 column quads][128 rows][4]:
+  // a warp's 32 rows of one column quad are 512 contiguous bytes
+  float4* scr = reinterpret_cast<float4*>(args.scratch) + (size_t)blockIdx.x * (kBM / 2) * (kBN / 4);
+  const int srow = q * 32 + lane;
   uint32_t acc_phase = 0, xphase = 0;
   for (int t = cid; t < args.ntiles; t += ncl) {
     const Tile tl = args.tiles[t];
@@ -376,56 +391,82 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
     const int mode = cfg.mode;
     const bool need_load = (mode != kModeGram);
     if (lane == 0 && need_load && cfg.dep != nullptr) acquire_counter(cfg.dep, cfg.dep_need);
-    mbar_wait(&tfull[0], acc_phase);
-    tc_fence_after();
     const int r0 = tl.tm * kBM + row_off;
-    const int r = r0 + lane;
-    // accumulator = buffer 0 (small terms + first half of the big chain) +
-    // buffer 1 (second half of the big chain)
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
     const int ncols = (mode == kModeUpdate) ? md.n : md.m;
+    const int npass = p3_passes(cfg.nk);
+    for (int ps = 0; ps < npass; ++ps) {
+      // accumulator of the pass = buffer 0 (+ buffer 1 when the pass's big
+      // chain has >= 2 K blocks), plus the running sum of earlier passes
+      const int k_lo = ps * cfg.nk / npass, k_hi = (ps + 1) * cfg.nk / npass;
+      const bool b1 = (k_hi - k_lo) >= 2;
+      const bool last = (ps == npass - 1);
+      mbar_wait(&tfull[0], acc_phase);
+      tc_fence_after();
 #pragma unroll 1
-    for (int k = 0; k < kEpiChunks; ++k) {
-      const int c0 = tl.tn * kBN + half * (kBN / 2) + k * kEpiCols;
-      if (c0 >= ncols) break;                                   // warp-uniform
-      if (lane == 0) {
-        bulk_wait_read<0>();                                    // previous chunk's stores left the slots
-        if (need_load) {
-          mbar_arrive_expect_tx(xbar, 3 * kEpiSlotBytes);
+      for (int k = 0; k < kEpiChunks; ++k) {
+        const int c0 = tl.tn * kBN + half * (kBN / 2) + k * kEpiCols;
+        if (c0 >= ncols) break;                                   // warp-uniform
+        if (last) {
+          if (lane == 0) {
+            bulk_wait_read<0>();                                  // previous chunk's stores left the slots
+            if (need_load) {
+              mbar_arrive_expect_tx(xbar, 3 * kEpiSlotBytes);
 #pragma unroll
-          for (int p = 0; p < 3; ++p) tma_load_2d(slots + p * kEpiSlotBytes, cfg.ein + p, xbar, c0, r0);
+              for (int p = 0; p < 3; ++p) tma_load_2d(slots + p * kEpiSlotBytes, cfg.ein + p, xbar, c0, r0);
+            }
+          }
+          __syncwarp();
+          if (need_load) {
+            mbar_wait(xbar, xphase);
+            xphase ^= 1;
+          }
+        }
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (c0 + 32 * h >= ncols) break;
+          float w[32];
+          tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+          if (b1) {
+            float w2[32];
+            tmem_ld32(t_row + kBN + k * kEpiCols + 32 * h, w2);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
+          }
+          float4* sp = scr + (size_t)((half * (kBN / 2) + k * kEpiCols + 32 * h) >> 2) * (kBM / 2) + srow;
+          if (ps > 0) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const float4 o = sp[v * (kBM / 2)];
+              w[4 * v] = __fadd_rn(w[4 * v], o.x);
+              w[4 * v + 1] = __fadd_rn(w[4 * v + 1], o.y);
+              w[4 * v + 2] = __fadd_rn(w[4 * v + 2], o.z);
+              w[4 * v + 3] = __fadd_rn(w[4 * v + 3], o.w);
+            }
+          }
+          if (!last) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) sp[v * (kBM / 2)] = make_float4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+          } else {
+            epilogue_math_p3(cfg, slots, lane, h, w);
+          }
+        }
+        if (last) {
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < 3; ++p) tma_store_2d(cfg.eout + p, slots + p * kEpiSlotBytes, c0, r0);
+            bulk_commit();
+          }
         }
       }
+      tc_fence_before();
       __syncwarp();
-      if (need_load) {
-        mbar_wait(xbar, xphase);
-        xphase ^= 1;
-      }
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        if (c0 + 32 * h >= ncols) break;
-        float w[32], w2[32];
-        tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
-        tmem_ld32(t_row + kBN + k * kEpiCols + 32 * h, w2);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
-        epilogue_math_p3(cfg, slots, lane, h, w);
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int p = 0; p < 3; ++p) tma_store_2d(cfg.eout + p, slots + p * kEpiSlotBytes, c0, r0);
-        bulk_commit();
-      }
+      if (lane == 0) mbar_arrive_remote(tempty_leader0);
+      acc_phase ^= 1;
     }
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive_remote(tempty_leader0);
-      if (cfg.pub != nullptr) publish_stores(cfg.pub);
-    }
-    acc_phase ^= 1;
+    if (lane == 0 && cfg.pub != nullptr) publish_stores(cfg.pub);
   }
   if (lane == 0) bulk_wait<0>();
 }
@@ -499,10 +540,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         // K=16 step into the fp32 accumulator with truncation; with the big
         // (0,0) chain last, the small terms are never truncated against the
         // big accumulator (256x1024: relF 2.0e-5 big-first, 2.4e-6 now).
-        for (int sg = 0; sg < (kP == 3 ? 6 : 1); ++sg) {
+        // (kP = 3: the small segments run in pass 0 over all of K, the big
+        // (0,0) segment pass by pass, see p3_passes)
+        const int npass = (kP == 3) ? p3_passes(o.nk) : 1;
+        for (int ps = 0; ps < npass; ++ps)
+        for (int sg = (kP == 3 && ps > 0) ? 5 : 0; sg < (kP == 3 ? 6 : 1); ++sg) {
         const int pa = (kP == 3) ? ((0x001012 >> (4 * sg)) & 0xF) * o.prow : 0;
         const int pb = (kP == 3) ? ((0x010210 >> (4 * sg)) & 0xF) * o.prow : 0;
-        for (int kb = 0; kb < o.nk; ++kb) {
+        const bool bigseg = (kP == 1) || sg == 5;
+        const int kb_lo = bigseg ? ps * o.nk / npass : 0;
+        const int kb_hi = bigseg ? (ps + 1) * o.nk / npass : o.nk;
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], o.diag ? 2 * kABytes : 2 * kStageBytes);
           if (args.stats != nullptr && leader) st_issue[stage] = clock64();
@@ -553,25 +601,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       for (int t = cid; t < args.ntiles; t += ncl) {
         const TileCfg o = nxt;
         if (t + ncl < args.ntiles) nxt = tile_cfg<kEdge, kP>(args, args.tiles[t + ncl], rank);
-        const int nkt = o.nk * kP * (kP + 1) / 2;       // kP = 3: six plane-pair segments
-
+        const int npass = (kP == 3) ? p3_passes(o.nk) : 1;
+        for (int ps = 0; ps < npass; ++ps) {
         long long t0 = clock64();
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         st_wait_tempty += clock64() - t0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
-        // kP = 3: the big (0,0) chain is split in two K halves, the second
-        // accumulated in the other TMEM buffer (each chain sees half the
-        // truncating adds; the epilogue sums the two).  One tile in flight.
-        const int nsplit = (kP == 3) ? 5 * o.nk + o.nk / 2 : nkt;
-        int kin = 0;                  // k-block index within the current plane-pair segment
-        for (int kb = 0; kb < nkt; ++kb) {
+        // kP = 3: pass ps = [small segments over all K (pass 0 only)] + the
+        // big chain over K blocks [k_lo, k_hi): its first half continues in
+        // buffer 0, the second half starts buffer 1 (one tile in flight).
+        const int k_lo = ps * o.nk / npass, k_hi = (ps + 1) * o.nk / npass;
+        const int n_small = (kP == 3 && ps == 0) ? 5 * o.nk : 0;
+        const int n_first = (kP == 3) ? n_small + (k_hi - k_lo + 1) / 2 : o.nk;
+        const int nst = n_small + (k_hi - k_lo);
+        int kin = (n_small > 0) ? 0 : k_lo;   // K block index within the current segment
+        for (int kb = 0; kb < nst; ++kb) {
+          if (kb == n_small) kin = k_lo;
           // per k-block operand layout: blocks of a symmetric buffer below
           // the diagonal arrive transposed (MN-major)
           const bool amn = o.a_mn || (o.a_wide && (kin >> 2) < o.pan_a);
           const bool bmn = o.b_mn || (o.b_wide && (kin >> 2) < o.pan_b);
           const uint32_t idesc = idesc_bf16(kBM, kBN, amn, bmn);
-          if (++kin == o.nk) kin = 0;
+          if (++kin == o.nk && kb < n_small) kin = 0;
           long long t1 = clock64();
           mbar_wait(&full[stage], phase);
           const long long t1e = clock64();
@@ -590,8 +642,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
                                          : smem_desc_sw128(a_addr + k * 32, 16, 1024);
               const uint64_t bdesc = bmn ? smem_desc_sw128(b_addr + k * 2048, kBoxBytes, 1024)
                                          : smem_desc_sw128(b_addr + k * 32, 16, 1024);
-              if (kP == 3 && kb >= nsplit)
-                umma_bf16_pair(tmem_base + kBN, adesc, bdesc, idesc, (kb != nsplit) || k != 0);
+              if (kP == 3 && kb >= n_first)
+                umma_bf16_pair(tmem_base + kBN, adesc, bdesc, idesc, (kb != n_first) || k != 0);
               else
                 umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0);
             }
@@ -603,10 +655,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
         if (kP == 3) {
-          acc_phase ^= 1;          // both buffers belong to one tile
+          acc_phase ^= 1;          // both buffers belong to one pass
         } else {
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
+        }
         }
       }
     }

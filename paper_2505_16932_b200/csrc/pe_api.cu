@@ -187,6 +187,7 @@ struct pe_ctx_s {
 
   int last_launches = 0;
   int* done = nullptr;          // fused schedule completion counters (cleared by the norm kernel)
+  float* scratch = nullptr;     // fp32 path: per-CTA running sums of the K passes (gemm_sm100.cuh)
   size_t done_cap = 0;
   int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1/3 are set)
   long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
@@ -339,6 +340,7 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->stats) cudaFree(c->stats);
   if (c->done) cudaFree(c->done);
+  if (c->scratch) cudaFree(c->scratch);
   delete c;
   return PE_OK;
 }
@@ -798,6 +800,10 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
       c->done_cap = need_done;
     }
   }
+  if (dtype == PE_FP32 && !c->scratch) {
+    const size_t sb = (size_t)c->num_sms * (kBM / 2) * kBN * sizeof(float);
+    if (cudaMalloc(&c->scratch, sb) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+  }
   CallSlot* cs = nullptr;
   if ((s = take_call_slot(c, call_bytes(count, T), &cs)) != PE_OK) return s;
   void** h = reinterpret_cast<void**>(cs->h);
@@ -893,6 +899,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     g.omaps = d_omaps;
     g.mflags = at<int>(P, P->o_flags);
     g.inv = at<float>(P, P->o_inv);
+    g.scratch = c->scratch;
     g.nphase = 0;
     g.coef = d_coef;
     g.done = c->done;

@@ -213,6 +213,17 @@ def test_fp32_parity(ctx, shape):
     assert om.rel_frobenius(X, oi.polar_express(M, TABLE, 5)) <= 1e-5
 
 
+@pytest.mark.parametrize("shape", [(2048, 2048), (128, 8192), (1024, 4096), (4096, 1024), (4096, 4096)])
+def test_fp32_long_k(ctx, shape):
+    """fp32 with long contractions (K up to 8192): the tensor core's truncating
+    accumulation is kept to <= 32-step chains by the K passes, so the error
+    stays at numpy-fp32 level (CPU numpy fp32 of the same iteration:
+    1.6e-6 .. 4.1e-6 on these shapes) and within the 1e-5 contract."""
+    M = syn.gaussian(*shape, seed=0).astype(np.float32).astype(np.float64)
+    X = run(ctx, [M], dtype="f32")[0]
+    assert om.rel_frobenius(X, oi.polar_express(M, TABLE, 5)) <= 1e-5
+
+
 def test_fp32_mixed_batch_and_spectra(ctx):
     """One fp32 call over a mixed batch (several tiles per matrix, both
     orientations, prescribed spectra kappa 1e2 / 1e3): each matrix within
