@@ -169,6 +169,26 @@ pe_status pe_polar(pe_ctx ctx, const void* const* in, void* const* out, const in
 pe_status pe_polar_host(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
                         int count, int iters, pe_dtype dtype, void* stream);
 
+/*
+ * One Muon optimizer step on a batch of `count` bf16 layer
+ * matrices, with the polar factor computed exactly as pe_polar computes it:
+ *   M <- bf16(fp32(beta) * M + fp32(1 - beta) * G)      (fp32 arithmetic,
+ *                                                         no FMA contraction)
+ *   X  = pe_polar(M) (bf16, T = iters, the context's table)
+ *   W <- bf16(fp32(W) - fp32(lr) * X)
+ * W[i], M[i], G[i]: device pointers to rows_i x cols_i row-major bf16
+ * matrices, 16-byte aligned; W and M are updated in place, G is read; the
+ * three sets must not overlap. beta, lr: finite (the paper's default beta =
+ * 0.9). The momentum update is fused into the norm pass and the weight
+ * update into the last update GEMM's epilogue (matrices with cols % 8 == 0;
+ * the others update W in the final copy pass), so neither M_t nor X makes an
+ * extra HBM round trip. Asynchronous on `stream` like pe_polar.
+ * Errors: PE_ERR_INVALID_ARG (NULL or overlapping pointers, misalignment,
+ * bad shapes, iters < 1, non-finite beta/lr), PE_ERR_WORKSPACE, PE_ERR_CUDA.
+ */
+pe_status pe_muon_step(pe_ctx ctx, void* const* W, void* const* M, const void* const* G,
+                       const int64_t* shapes, int count, double beta, double lr, int iters, void* stream);
+
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */
 pe_status pe_last_launch_count(pe_ctx ctx, int* launches);

@@ -89,3 +89,15 @@ def via_scalar_map(M, table, T, norm="listing2"):
     else:
         sh = s
     return (U * composite(sh, table, T)) @ Vt
+
+
+def muon_step(W, M, G, beta, lr, table, T):
+    """One Muon step in fp64, with polar(M_t) replaced by the Polar
+    Express iteration exactly as ``polar_express`` computes it (the method's
+    use inside Muon, Listing 2):
+        M_t     = beta M_{t-1} + (1 - beta) G_t
+        W_{t+1} = W_t - lambda polar(M_t)
+    Returns (W_{t+1}, M_t)."""
+    W = np.asarray(W, dtype=np.float64)
+    Mt = beta * np.asarray(M, dtype=np.float64) + (1.0 - beta) * np.asarray(G, dtype=np.float64)
+    return W - lr * polar_express(Mt, table, T), Mt

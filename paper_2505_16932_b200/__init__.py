@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = [
     "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
+    "pe_muon_step",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused"]
 
@@ -76,6 +77,7 @@ def lib():
         "pe_flops": (I, [I64P, I, I, I, DP]),
         "pe_profile_enable": (I, [P, I]),
         "pe_profile_read": (I, [P, DP, ctypes.POINTER(I), I]),
+        "pe_muon_step": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, D, D, I, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -209,6 +211,29 @@ class Context:
         _check(lib().pe_polar(self._h, ins, outs, shp, n, int(iters), dt, ctypes.c_void_p(stream.cuda_stream)),
                "pe_polar")
         return outputs
+
+    def muon_step(self, weights, momenta, grads, beta=0.9, lr=0.02, iters=5, stream=None):
+        """pe_muon_step on bf16 CUDA tensors: momenta <- beta*momenta +
+        (1-beta)*grads, weights <- weights - lr * polar(momenta); in place."""
+        import torch
+        n = len(weights)
+        if not (len(momenta) == n and len(grads) == n):
+            raise ValueError("muon_step takes equally long weight / momentum / gradient lists")
+        for w, m, g in zip(weights, momenta, grads):
+            for t in (w, m, g):
+                if t.dim() != 2 or not t.is_contiguous() or not t.is_cuda or t.dtype != torch.bfloat16:
+                    raise ValueError("muon_step takes contiguous 2-D bf16 CUDA tensors")
+            if not (w.shape == m.shape == g.shape):
+                raise ValueError("muon_step: weight, momentum and gradient shapes differ")
+        W = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in weights])
+        M = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in momenta])
+        G = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in grads])
+        shp = _shapes_arr([tuple(t.shape) for t in weights])
+        if stream is None:
+            stream = torch.cuda.current_stream(weights[0].device if n else self.device)
+        _check(lib().pe_muon_step(self._h, W, M, G, shp, n, float(beta), float(lr), int(iters),
+                                  ctypes.c_void_p(stream.cuda_stream)), "pe_muon_step")
+        return weights
 
     def polar_host(self, inputs, outputs, iters=5, stream=None):
         """pe_polar_host on host (pinned) CPU tensors; synchronous."""

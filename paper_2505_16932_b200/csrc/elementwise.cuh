@@ -38,6 +38,11 @@ struct NormArgs {
   int src_f32;                 // 1: fp32 input, 0: bf16
   int* zero;                   // fused GEMM schedule: completion counters to clear, or nullptr
   int nzero;
+  // Muon step (pe_muon_step, bf16 only): srcs are the momentum buffers M,
+  // updated in place to M = bf16(beta M + (1 - beta) G) before the norm of
+  // the new M is taken
+  const void* const* grads;    // G per matrix, or nullptr (plain pe_polar)
+  float beta, omb;             // fp32(beta), fp32(1 - beta)
 };
 
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
@@ -62,7 +67,39 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
   const int64_t begin = (int64_t)ci * kNormChunk;
   const int64_t end = min(begin + (int64_t)kNormChunk, total);
   double acc = 0.0;
-  if (a.src_f32) {
+  if (a.grads != nullptr) {
+    // momentum update fused into the norm pass: reads M and G, writes M
+    __nv_bfloat16* p = const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(a.srcs[mat]));
+    const __nv_bfloat16* gp = reinterpret_cast<const __nv_bfloat16*>(a.grads[mat]);
+    const bool al = (((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(gp)) & 15) == 0);
+    int64_t i = begin + (int64_t)threadIdx.x * 8;
+    constexpr int64_t kStride = (int64_t)kNormThreads * 8;
+    auto upd = [&](float m, float g) { return __float2bfloat16_rn(__fadd_rn(__fmul_rn(a.beta, m), __fmul_rn(a.omb, g))); };
+    if (al) {
+      for (; i + 8 <= end; i += kStride) {
+        const uint4 mu = *reinterpret_cast<const uint4*>(p + i);
+        const uint4 gu = __ldg(reinterpret_cast<const uint4*>(gp + i));
+        const __nv_bfloat162* mh = reinterpret_cast<const __nv_bfloat162*>(&mu);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
+        uint4 ou;
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&ou);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 mf = __bfloat1622float2(mh[q]), gf = __bfloat1622float2(gh[q]);
+          oh[q] = __halves2bfloat162(upd(mf.x, gf.x), upd(mf.y, gf.y));
+        }
+        *reinterpret_cast<uint4*>(p + i) = ou;
+        acc += sumsq8_bf16(ou);
+      }
+    }
+    for (; i < end; i += kStride)
+      for (int64_t j = i; j < min(i + 8, end); ++j) {
+        const __nv_bfloat16 v = upd(__bfloat162float(p[j]), __bfloat162float(gp[j]));
+        p[j] = v;
+        const float f = __bfloat162float(v);
+        acc += (double)(f * f);
+      }
+  } else if (a.src_f32) {
     const float* p = reinterpret_cast<const float*>(a.srcs[mat]);
     const bool al = ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
     int64_t i = begin + (int64_t)threadIdx.x * 4;
@@ -144,6 +181,8 @@ struct CopyArgs {
   const void* const* srcs;     // per matrix source
   void* const* dsts;           // per matrix destination
   const float* scale;          // per matrix multiplier or nullptr
+  int muon;                    // finalize of pe_muon_step: dst = bf16(dst - lr * src) (Muon W update)
+  float lr;
 };
 
 template <typename T> struct VecT;
@@ -206,6 +245,12 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
 #pragma unroll
           for (int j = 0; j < V; ++j) f[j] = __fmul_rn(f[j], sc);
         }
+        if (a.muon) {
+          float w[V];
+          unpack(*reinterpret_cast<const uint4*>(dst + (size_t)rr * cm.dld + cc), w, (T*)nullptr);
+#pragma unroll
+          for (int j = 0; j < V; ++j) f[j] = __fsub_rn(w[j], __fmul_rn(a.lr, f[j]));
+        }
         *reinterpret_cast<uint4*>(dst + (size_t)rr * cm.dld + cc) = pack(f, (T*)nullptr);
       }
     } else {
@@ -215,6 +260,7 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
         const int cc = (int)(e % cm.cols);
         float f = to_f(src[(size_t)rr * cm.sld + cc]);
         if (a.scale) f = __fmul_rn(f, sc);
+        if (a.muon) f = __fsub_rn(to_f(dst[(size_t)rr * cm.dld + cc]), __fmul_rn(a.lr, f));
         dst[(size_t)rr * cm.dld + cc] = from_f<T>(f);
       }
     }
@@ -262,11 +308,21 @@ __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
 #pragma unroll
       for (int j = 0; j < V; ++j) f[j] = tile[jv + j][i];
       if (vout && dc + V <= cm.rows) {
+        if (a.muon) {
+          float w[V];
+          unpack(*reinterpret_cast<const uint4*>(dst + (size_t)dr * cm.dld + dc), w, (T*)nullptr);
+#pragma unroll
+          for (int j = 0; j < V; ++j) f[j] = __fsub_rn(w[j], __fmul_rn(a.lr, f[j]));
+        }
         *reinterpret_cast<uint4*>(dst + (size_t)dr * cm.dld + dc) = pack(f, (T*)nullptr);
       } else {
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          if (dc + j < cm.rows) dst[(size_t)dr * cm.dld + dc + j] = from_f<T>(f[j]);
+          if (dc + j < cm.rows) {
+            float v = f[j];
+            if (a.muon) v = __fsub_rn(to_f(dst[(size_t)dr * cm.dld + dc + j]), __fmul_rn(a.lr, v));
+            dst[(size_t)dr * cm.dld + dc + j] = from_f<T>(v);
+          }
       }
     }
     __syncthreads();

@@ -80,6 +80,8 @@ struct GemmArgs {
   const int* mflags;           // per call, per matrix: kFlag*
   const float* inv;            // per matrix fp32(1/s)
   float* scratch;              // kP = 3: 128 x 256 fp32 per CTA (running sum of the K passes)
+  int muon;                    // pe_muon_step: the last update's direct output is the weight W,
+  float lr;                    // updated to bf16(W - lr * bf16(X'))
   // one phase per launch (nphase == 0): the phase of every tile
   int mode;
   int xin;                     // which X buffer holds the current iterate
@@ -126,6 +128,7 @@ struct TileCfg {
   const CUtensorMap* eout;     // result chunk map
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
   bool scaled;                 // first iteration of a folded matrix
+  bool muon;                   // result chunk is a Muon weight update of the chunk already at eout
   int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
@@ -169,6 +172,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   const bool fold = kEdge && c.first && (fl & kFlagFolded);
   const bool tall = kEdge && (fl & kFlagTall) != 0;
   c.scaled = fold;
+  c.muon = false;
   c.a_wide = c.b_wide = false;
   c.Amn = c.Bmn = nullptr;
   c.pan_a = tl.tm;
@@ -208,6 +212,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     if (kEdge && c.last && (fl & kFlagDirect)) {
       c.eout = g.omaps + tl.mat;
       c.eout_tr = tall;
+      c.muon = g.muon != 0;
     } else {
       c.eout = em + kP * (c.xin ^ 1);
     }
@@ -290,7 +295,29 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
       for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv2);
     }
-    if (!tr_out) {
+    if (kEdge && cfg.muon) {
+      // Muon: the slot holds the weight chunk; W <- bf16(W - lr * bf16(X'))
+      if (!tr_out) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          uint4* up = reinterpret_cast<uint4*>(slot + sw128_off(lane, half32 * 4 + qq * 2 + v));
+          float wo[8];
+          bf16x8_to_f32(*up, wo);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            wo[j] = __fsub_rn(wo[j], __fmul_rn(g.lr, __bfloat162float(__float2bfloat16_rn(wq[8 * v + j]))));
+          *up = pack8_bf16(wo);
+        }
+      } else {
+        __nv_bfloat16* sp = reinterpret_cast<__nv_bfloat16*>(slot) + lane;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          __nv_bfloat16* e = sp + (half32 * 32 + qq * 16 + j) * 32;
+          *e = __float2bfloat16_rn(
+              __fsub_rn(__bfloat162float(*e), __fmul_rn(g.lr, __bfloat162float(__float2bfloat16_rn(wq[j])))));
+        }
+      }
+    } else if (!tr_out) {
 #pragma unroll
       for (int v = 0; v < 2; ++v)
         *reinterpret_cast<uint4*>(slot + sw128_off(lane, half32 * 4 + qq * 2 + v)) = pack8_bf16(wq + 8 * v);
@@ -748,14 +775,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
         }
-        if (kEdge && need_load && cfg.ein_tr != cfg.eout_tr) {
+        if (kEdge && need_load && (cfg.ein_tr != cfg.eout_tr || cfg.muon)) {
           // operand and result layouts differ (tall caller matrix, first or
-          // last iteration): read the whole operand chunk before the in-place
-          // result writes can overwrite any of it
+          // last iteration), or the result updates another chunk (Muon): read
+          // the whole operand chunk before the slot is overwritten
           uint32_t pre[2][16];
           if (cfg.ein_tr) { read_operand_half<true>(slot, lane, 0, pre[0]); read_operand_half<true>(slot, lane, 1, pre[1]); }
           else { read_operand_half<false>(slot, lane, 0, pre[0]); read_operand_half<false>(slot, lane, 1, pre[1]); }
           __syncwarp();
+          if (cfg.muon) {
+            // bring the weight chunk into the slot (same map and box as the store)
+            if (lane == 0) {
+              fence_async_smem();
+              mbar_arrive_expect_tx(&xbar[k], kEpiSlotBytes);
+              if (!cfg.eout_tr) tma_load_2d(slot, cfg.eout, &xbar[k], c0, r0);
+              else tma_load_2d(slot, cfg.eout, &xbar[k], r0, c0);
+            }
+            __syncwarp();
+            mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
+            phase_bits ^= 1u << k;
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (c0 + 32 * h < ncols) {

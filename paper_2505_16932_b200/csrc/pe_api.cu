@@ -419,7 +419,7 @@ static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
 
 // per-call upload: 4*count pointers, then 3 tensor maps per matrix (caller
 // input main loop, caller input epilogue chunk, caller output epilogue chunk)
-static size_t call_ptr_bytes(int count) { return rup((size_t)4 * count * sizeof(void*), 128); }
+static size_t call_ptr_bytes(int count) { return rup((size_t)5 * count * sizeof(void*), 128); }
 static size_t call_coef_off(int count) { return call_ptr_bytes(count) + (size_t)3 * count * sizeof(CUtensorMap); }
 static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size_t)3 * T * sizeof(float); }
 
@@ -758,16 +758,25 @@ static pe_status take_call_slot(pe_ctx c, size_t bytes, CallSlot** out) {
   return PE_OK;
 }
 
-extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
-                              int count, int iters, pe_dtype dtype, void* stream_) {
+// pe_polar and pe_muon_step.  Muon (grads != nullptr, bf16): `in` are the
+// momentum buffers M, updated in place by the norm kernel to
+// bf16(beta M + (1 - beta) G); `out` are the weights W, updated to
+// bf16(W - lr bf16(polar(M))) by the last update's epilogue (folded
+// matrices) or the finalize pass (the others).
+static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, const void* const* grads,
+                            const int64_t* shapes, int count, int iters, pe_dtype dtype, void* stream_,
+                            double beta, double lr) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   if (count == 0) { c->last_launches = 0; return PE_OK; }
   if (!in || !out) return PE_ERR_INVALID_ARG;
+  const bool muon = grads != nullptr;
+  if (muon && dtype != PE_BF16) return PE_ERR_UNSUPPORTED;
   pe_status s = validate_shapes(shapes, count);
   if (s != PE_OK) return s;
   for (int i = 0; i < count; ++i) {
-    if (!in[i] || !out[i]) return PE_ERR_INVALID_ARG;
-    if ((reinterpret_cast<uintptr_t>(in[i]) & 15) || (reinterpret_cast<uintptr_t>(out[i]) & 15)) {
+    if (!in[i] || !out[i] || (muon && !grads[i])) return PE_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(in[i]) & 15) || (reinterpret_cast<uintptr_t>(out[i]) & 15) ||
+        (muon && (reinterpret_cast<uintptr_t>(grads[i]) & 15))) {
       g_last_error = "buffers must be 16-byte aligned";
       return PE_ERR_INVALID_ARG;
     }
@@ -816,6 +825,7 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     h[count + i] = (fl & kFlagDirect) ? out[i] : nullptr;
     h[2 * count + i] = md.X[xfinal];
     h[3 * count + i] = out[i];
+    h[4 * count + i] = muon ? const_cast<void*>(grads[i]) : nullptr;
     if (fl & kFlagFolded) {
       void* src = const_cast<void*>(in[i]);
       if ((s = make_tmap(&h_maps[2 * i], src, md.rows, md.cols, md.cols)) != PE_OK) return s;
@@ -858,6 +868,9 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   na.src_f32 = src_f32;
   na.zero = fused ? c->done : nullptr;
   na.nzero = fused ? count * 3 * T : 0;
+  na.grads = muon ? d_ptrs + 4 * count : nullptr;
+  na.beta = (float)beta;
+  na.omb = (float)(1.0 - beta);
   { ProfScope ps(c, 0, st);
     launch(pe_norm_kernel, P->n_chunks, kNormThreads, 0, st, na); }
   ++launches;
@@ -872,6 +885,8 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     ca.srcs = fin ? d_fin_src : d_in;
     ca.dsts = fin ? d_out : at<void*>(P, P->o_x0);
     ca.scale = scale ? at<float>(P, P->o_inv) : nullptr;
+    ca.muon = (muon && fin) ? 1 : 0;
+    ca.lr = (float)lr;
     const int grid = std::min(P->n_it[k], c->num_sms * 8);
     ProfScope ps(c, fin ? 5 : 1, st);
     const bool tr = (k == 1 || k == 2);
@@ -900,6 +915,8 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
     g.mflags = at<int>(P, P->o_flags);
     g.inv = at<float>(P, P->o_inv);
     g.scratch = c->scratch;
+    g.muon = muon ? 1 : 0;
+    g.lr = (float)lr;
     g.nphase = 0;
     g.coef = d_coef;
     g.done = c->done;
@@ -968,6 +985,25 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   PE_CUDA(cudaGetLastError());
   c->last_launches = launches;
   return PE_OK;
+}
+
+extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
+                              int count, int iters, pe_dtype dtype, void* stream) {
+  return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
+}
+
+extern "C" pe_status pe_muon_step(pe_ctx c, void* const* W, void* const* M, const void* const* G,
+                                  const int64_t* shapes, int count, double beta, double lr, int iters,
+                                  void* stream) {
+  if (!c || count < 0 || (count > 0 && (!W || !M || !G))) return PE_ERR_INVALID_ARG;
+  if (!std::isfinite(beta) || !std::isfinite(lr)) return PE_ERR_INVALID_ARG;
+  for (int i = 0; i < count; ++i)
+    for (int j = 0; j < count; ++j)
+      if (W[i] == M[j] || W[i] == G[j] || M[i] == G[j]) {
+        g_last_error = "pe_muon_step: W, M and G buffers must be distinct";
+        return PE_ERR_INVALID_ARG;
+      }
+  return polar_impl(c, M, W, count > 0 ? G : nullptr, shapes, count, iters, PE_BF16, stream, beta, lr);
 }
 
 // End-to-end entry on host buffers.  The batch is cut into G groups of about

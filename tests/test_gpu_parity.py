@@ -444,3 +444,72 @@ def test_fused_schedule_bit_identical(tmp_path):
         assert np.array_equal(res["0"][k], res["1"][k]), k
     # T = 5: norm + copy passes + one fused GEMM launch vs 15 GEMM launches
     assert launches["0"] - launches["1"] == 14
+
+
+def _bits(t):
+    return t.view(torch.int16).cpu().numpy()
+
+
+def _bf16_rne(x32):
+    """fp32 array -> bf16 values (RNE), as float32."""
+    return syn.to_bf16_values(np.asarray(x32, dtype=np.float32)).astype(np.float32)
+
+
+MUON_SHAPES = [(768, 768), (768, 3072), (3072, 768), (520, 200), (200, 521), (300, 700), (1, 64), (1100, 260)]
+
+
+@pytest.mark.parametrize("T", [1, 5])
+def test_muon_step_bit_identical_to_composition(ctx, T):
+    """pe_muon_step (momentum fused into the norm pass, weight update fused
+    into the last update epilogue / the finalize pass) equals the unfused
+    composition bit for bit: M1 = bf16(fp32(beta) M + fp32(1-beta) G) (numpy
+    fp32 emulation, no FMA), then W1 = bf16(fp32(W) - fp32(lr) X) with
+    X = pe_polar(M1) from the same library.  Mixed batch: folded wide/tall,
+    unfolded (cols % 8 != 0) wide/tall, rank one."""
+    beta, lr = 0.9, 0.02
+    rng = np.random.default_rng(11)
+    Ws = [bf16_values(rng.standard_normal((r, c)) * 0.05) for r, c in MUON_SHAPES]
+    Ms = [bf16_values(syn.gaussian(r, c, seed=80 + i, std=0.02)) for i, (r, c) in enumerate(MUON_SHAPES)]
+    Gs = [bf16_values(syn.gaussian(r, c, seed=90 + i, std=0.05)) for i, (r, c) in enumerate(MUON_SHAPES)]
+    w = [to_dev_bf16(x) for x in Ws]
+    m = [to_dev_bf16(x) for x in Ms]
+    g = [to_dev_bf16(x) for x in Gs]
+    ctx.muon_step(w, m, g, beta=beta, lr=lr, iters=T)
+    torch.cuda.synchronize()
+    b32, omb32, lr32 = np.float32(beta), np.float32(1.0 - beta), np.float32(lr)
+    m_ref = [_bf16_rne(b32 * M.astype(np.float32) + omb32 * G.astype(np.float32)) for M, G in zip(Ms, Gs)]
+    for mi, mr in zip(m, m_ref):
+        assert np.array_equal(mi.float().cpu().numpy(), mr)
+    xs = ctx.polar([mi.clone() for mi in m], iters=T)
+    torch.cuda.synchronize()
+    for wi, W0, x in zip(w, Ws, xs):
+        w_ref = _bf16_rne(W0.astype(np.float32) - lr32 * x.float().cpu().numpy())
+        assert np.array_equal(wi.float().cpu().numpy(), w_ref)
+
+
+def test_muon_step_against_oracle(ctx):
+    """From W = 0 the Muon step direction -(W1 - W0) / lr is the bf16 polar
+    factor of the new momentum: G1/G3 gates against oracle.muon_step on the
+    same inputs; the momentum matches the fp64 recursion to bf16 rounding."""
+    beta, lr = 0.9, 0.5
+    shapes = [(768, 3072), (3072, 768), (520, 200)]
+    Ms = [bf16_values(syn.gaussian(r, c, seed=100 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    Gs = [bf16_values(syn.gaussian(r, c, seed=110 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    w = [torch.zeros((r, c), dtype=torch.bfloat16, device="cuda") for r, c in shapes]
+    m = [to_dev_bf16(x) for x in Ms]
+    ctx.muon_step(w, m, [to_dev_bf16(x) for x in Gs], beta=beta, lr=lr, iters=5)
+    torch.cuda.synchronize()
+    for wi, mi, M, G in zip(w, m, Ms, Gs):
+        W1, Mt = oi.muon_step(np.zeros(M.shape), M, G, beta, lr, TABLE, 5)
+        m1 = mi.float().cpu().numpy().astype(np.float64)
+        assert om.rel_frobenius(m1, Mt) <= 2.0 ** -8
+        step = -wi.float().cpu().numpy().astype(np.float64) / lr
+        check_g1_g3(step, m1)
+        assert om.rel_frobenius(step, -W1 / lr) <= 3e-2
+
+
+def test_muon_step_rejects_aliasing(ctx):
+    x = torch.zeros((64, 64), dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros_like(x)
+    with pytest.raises(pe.PeError):
+        ctx.muon_step([x], [x], [y])

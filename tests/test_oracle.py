@@ -404,3 +404,43 @@ def test_bf16_diagonal_emulation_tracks_fp64_oracle():
         ref = np.diag(oi.polar_express(syn.diagonal(64, 96, sig), tab, T))
         assert np.max(np.abs(emu - ref)) < tol, T
         assert np.all(np.isfinite(emu))
+
+
+def test_muon_step_pins():
+    """oracle.iteration.muon_step against what P:41-49 fixes independently of
+    the code: (i) the momentum recursion from M_0 = 0 unrolls to
+    M_k = (1 - beta) sum_j beta^(k-j) G_j; (ii) on a diagonal gradient the
+    step is W - lambda diag(p*(sigma_hat)) with p* the scalar composite
+    (P:107, P:121-124) and sigma_hat = sigma / (||sigma|| 1.01 + 1e-7);
+    (iii) beta = 1 keeps M and moves W by -lambda polar_express(M); (iv) for a
+    rank-one 1 x n gradient and enough iterations the step direction is the
+    exact polar factor g / |g|."""
+    table = oc.pe_coeffs(1e-3, 5, 8, 1.01)[0]
+    rng = np.random.default_rng(3)
+    beta = 0.9
+    Gs = [rng.standard_normal((6, 9)) for _ in range(4)]
+    M = np.zeros((6, 9))
+    W = rng.standard_normal((6, 9))
+    for G in Gs:
+        W, M = oi.muon_step(W, M, G, beta, 0.01, table, 5)
+    closed = (1 - beta) * sum(beta ** (len(Gs) - 1 - j) * G for j, G in enumerate(Gs))
+    assert np.allclose(M, closed, rtol=0, atol=1e-14)
+    # (ii) diagonal gradient, zero momentum, beta = 0
+    sig = np.array([3.0, 1.0, 0.25, 0.01])
+    G = np.zeros((4, 7))
+    G[np.arange(4), np.arange(4)] = sig
+    W0 = rng.standard_normal((4, 7))
+    W1, M1 = oi.muon_step(W0, np.zeros_like(G), G, 0.0, 0.5, table, 5)
+    shat = sig / (np.sqrt(np.sum(sig ** 2)) * 1.01 + 1e-7)
+    expect = W0.copy()
+    expect[np.arange(4), np.arange(4)] -= 0.5 * oi.composite(shat, table, 5)
+    assert np.allclose(M1, G) and np.allclose(W1, expect, rtol=0, atol=1e-12)
+    # (iii) beta = 1
+    Mb = rng.standard_normal((5, 3))
+    W2, M2 = oi.muon_step(np.zeros((5, 3)), Mb, rng.standard_normal((5, 3)), 1.0, 2.0, table, 5)
+    assert np.array_equal(M2, Mb)
+    assert np.allclose(W2, -2.0 * oi.polar_express(Mb, table, 5), rtol=0, atol=1e-14)
+    # (iv) rank one: converges to g / |g|
+    g = rng.standard_normal((1, 50))
+    W3, _ = oi.muon_step(np.zeros((1, 50)), np.zeros((1, 50)), g, 0.0, 1.0, table, 12)
+    assert np.allclose(-W3, g / np.linalg.norm(g), rtol=0, atol=1e-6)
