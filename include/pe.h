@@ -124,12 +124,19 @@ pe_status pe_destroy(pe_ctx ctx);
  * PE_ERR_UNSUPPORTED (degree). */
 pe_status pe_set_coeffs(pe_ctx ctx, const double* coeffs, int ntuples, int degree);
 
-/* Pre-size the workspace for a batch so that a later pe_polar with the same
- * (or smaller) batch performs no allocation (required before CUDA-graph
- * capture).  Workspace per matrix (m = min side, n = max side): two bf16 m x n
- * iterate buffers, two m x m buffers (A, B), a norm slot; PE_FP32 holds each
- * buffer as three bf16 planes (3x the bytes).
- * Errors: PE_ERR_INVALID_ARG, PE_ERR_WORKSPACE. */
+/* Pre-size the workspace and build the plan for a batch (shape list and
+ * dtype) so that a later pe_polar / pe_muon_step on it performs no allocation
+ * or synchronisation.  Workspace per matrix (m = min side, n = max side): two
+ * bf16 m x n iterate buffers, two m x m buffers (A, B), a norm slot; PE_FP32
+ * holds each buffer as three bf16 planes (3x the bytes).
+ * CUDA graphs: a pe_polar / pe_muon_step issued on a stream that is being
+ * captured requires a prior pe_reserve of the same shape list and dtype; it
+ * then allocates nothing, does not synchronise, and consumes one of the
+ * upload slots pe_reserve keeps in reserve (4 per call of pe_reserve,
+ * iters <= 64) for the lifetime of the context, since the graph's copy node
+ * re-reads it at every replay. Graph replays see the current contents of the
+ * captured buffers. Errors: PE_ERR_INVALID_ARG, PE_ERR_WORKSPACE (also: a
+ * captured call without a reservation). */
 pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtype);
 
 /*

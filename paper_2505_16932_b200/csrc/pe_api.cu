@@ -178,6 +178,11 @@ struct pe_ctx_s {
 
   CallSlot calls[kCallSlots];
   int next_call = 0;
+  // CUDA-graph capture: every captured call consumes one of these for good
+  // (the graph's memcpy node re-reads its pinned host buffer at each replay);
+  // pe_reserve keeps kCaptureSpare unused ones of the reserved batch's size
+  std::vector<CallSlot> cap_slots;
+  size_t cap_used = 0;
 
   // pe_polar_host: staging + copy streams
   void* staging = nullptr;
@@ -332,6 +337,10 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
     if (cs.d) cudaFree(cs.d);
     if (cs.h) cudaFreeHost(cs.h);
     if (cs.done) cudaEventDestroy(cs.done);
+  }
+  for (CallSlot& cs : c->cap_slots) {
+    if (cs.d) cudaFree(cs.d);
+    if (cs.h) cudaFreeHost(cs.h);
   }
   if (c->staging) cudaFree(c->staging);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
@@ -721,13 +730,48 @@ static pe_status ensure_fused(pe_ctx c, Plan* P, int T) {
   return PE_OK;
 }
 
+constexpr int kCaptureSpare = 4;
+constexpr int kCaptureMaxIters = 64;
+
 extern "C" pe_status pe_reserve(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype) {
   if (!c || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   pe_status s = validate_shapes(shapes, count);
   if (s != PE_OK) return s;
   PE_CUDA(cudaSetDevice(c->device));
   Plan* P = nullptr;
-  return build_plan(c, shapes, count, dtype, &P);
+  if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) return s;
+  if (dtype == PE_FP32 && !c->scratch) {
+    const size_t sb = (size_t)c->num_sms * (kBM / 2) * kBN * sizeof(float);
+    if (cudaMalloc(&c->scratch, sb) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+  }
+  // spare upload slots for calls captured into CUDA graphs
+  const size_t need = call_bytes(count, kCaptureMaxIters);
+  size_t spare = 0;
+  for (size_t i = c->cap_used; i < c->cap_slots.size(); ++i) {
+    CallSlot& cs = c->cap_slots[i];
+    if (cs.bytes < need) {
+      if (cs.d) cudaFree(cs.d);
+      if (cs.h) cudaFreeHost(cs.h);
+      cs = CallSlot();
+      if (cudaMalloc(&cs.d, need) != cudaSuccess || cudaMallocHost(&cs.h, need) != cudaSuccess) {
+        cudaGetLastError();
+        return PE_ERR_WORKSPACE;
+      }
+      cs.bytes = need;
+    }
+    ++spare;
+  }
+  while (spare < (size_t)kCaptureSpare) {
+    CallSlot cs;
+    if (cudaMalloc(&cs.d, need) != cudaSuccess || cudaMallocHost(&cs.h, need) != cudaSuccess) {
+      cudaGetLastError();
+      return PE_ERR_WORKSPACE;
+    }
+    cs.bytes = need;
+    c->cap_slots.push_back(cs);
+    ++spare;
+  }
+  return PE_OK;
 }
 
 // ---------------------------------------------------------------- online
@@ -784,8 +828,23 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
   PE_CUDA(cudaSetDevice(c->device));
   PE_CUDA(cudaGetLastError());
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  PE_CUDA(cudaStreamIsCapturing(st, &cap_status));
+  const bool capturing = cap_status == cudaStreamCaptureStatusActive;
   Plan* P = nullptr;
-  if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) return s;
+  if (capturing) {
+    // no allocation or synchronisation is allowed: the plan must be cached
+    std::vector<int64_t> key(shapes, shapes + 2 * count);
+    for (Plan* q : c->plans)
+      if (q->dtype == dtype && q->key == key) P = q;
+    if (!P || (dtype == PE_FP32 && !c->scratch)) {
+      g_last_error = "pe_polar under CUDA-graph capture: call pe_reserve for this batch before capturing";
+      return PE_ERR_WORKSPACE;
+    }
+    P->last_use = ++c->use_clock;
+  } else if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) {
+    return s;
+  }
 
   // per-call pointers: [in | outs_direct | fin_src | out] + caller tensor maps
   const int T = iters;
@@ -794,7 +853,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   // PE_FUSED=1; measured equal to one launch per phase on the GPT-2 sets and
   // within noise on Llama, profiles/r1_variants.md)
   static const bool fused_on = getenv("PE_FUSED") && strcmp(getenv("PE_FUSED"), "0") != 0;
-  const bool fused = fused_on && dtype == PE_BF16;
+  const bool fused = fused_on && dtype == PE_BF16 && !capturing;   // (its setup may synchronise)
   const int nq = (c->degree + 1) / 2;
   if (fused) {
     if ((s = ensure_fused(c, P, T)) != PE_OK) return s;
@@ -814,7 +873,19 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     if (cudaMalloc(&c->scratch, sb) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
   }
   CallSlot* cs = nullptr;
-  if ((s = take_call_slot(c, call_bytes(count, T), &cs)) != PE_OK) return s;
+  if (capturing) {
+    // a captured call keeps its upload buffer for the graph's lifetime
+    const size_t need = call_bytes(count, T);
+    while (c->cap_used < c->cap_slots.size() && c->cap_slots[c->cap_used].bytes < need) ++c->cap_used;
+    if (c->cap_used == c->cap_slots.size() || T > kCaptureMaxIters) {
+      g_last_error = "pe_polar under CUDA-graph capture: call pe_reserve for this batch before capturing "
+                     "(it keeps 4 upload slots per reservation; iters <= 64)";
+      return PE_ERR_WORKSPACE;
+    }
+    cs = &c->cap_slots[c->cap_used++];
+  } else if ((s = take_call_slot(c, call_bytes(count, T), &cs)) != PE_OK) {
+    return s;
+  }
   void** h = reinterpret_cast<void**>(cs->h);
   const size_t omap_off = call_ptr_bytes(count);
   CUtensorMap* h_maps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);
@@ -842,8 +913,10 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     h_coef[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
   }
   PE_CUDA(cudaMemcpyAsync(cs->d, h, call_bytes(count, T), cudaMemcpyHostToDevice, st));
-  PE_CUDA(cudaEventRecord(cs->done, st));
-  cs->armed = true;
+  if (!capturing) {
+    PE_CUDA(cudaEventRecord(cs->done, st));
+    cs->armed = true;
+  }
   void** d_ptrs = reinterpret_cast<void**>(cs->d);
   const CUtensorMap* d_imaps =
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
