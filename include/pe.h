@@ -211,8 +211,11 @@ pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
  *   the three-plane instantiation)   5 transpose-back (pe_copy_kernel)
  *   6 fused (pe_gemm_sm100 running every phase of the call in one launch;
  *     bf16 with PE_FUSED=1 set in the environment, otherwise one launch per phase)
+ *   7 small (pe_small_sm100: the whole call in one launch, one CTA per
+ *     matrix, when every matrix has min side <= 128 and max side <= 640
+ *     (bf16) / 128 (fp32); PE_SMALL=0 disables it)
  */
-#define PE_PROFILE_KINDS 7
+#define PE_PROFILE_KINDS 8
 pe_status pe_profile_enable(pe_ctx ctx, int on);
 pe_status pe_profile_read(pe_ctx ctx, double* ms, int* counts, int nkinds);
 

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = [
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
     "pe_muon_step",
 ]
-PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused"]
+PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PE_LIB_OVERRIDE") or os.path.join(_HERE, "libpe.so")   # override: A/B experiments only

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpe.so")
 SOURCES = ["pe_api.cu", "pe_coeffs.cpp"]
-HEADERS = ["ptx.cuh", "pe_types.h", "gemm_sm100.cuh", "elementwise.cuh"]
+HEADERS = ["ptx.cuh", "pe_types.h", "gemm_sm100.cuh", "small_sm100.cuh", "elementwise.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

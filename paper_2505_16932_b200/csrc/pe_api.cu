@@ -34,6 +34,7 @@
 
 #include "elementwise.cuh"
 #include "gemm_sm100.cuh"
+#include "small_sm100.cuh"
 #include "pe.h"
 #include "pe_types.h"
 
@@ -310,6 +311,10 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
                                (int)gemm_smem_bytes<kShortStages, 2>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kP3Stages, 3, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kP3Stages, 3>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)small_smem_bytes<1>(640)));
+  PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)small_smem_bytes<3>(128)));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -802,6 +807,91 @@ static pe_status take_call_slot(pe_ctx c, size_t bytes, CallSlot** out) {
   return PE_OK;
 }
 
+// Upload buffer of one call: the next ring slot, or -- while the stream is
+// being captured into a CUDA graph -- a reserved slot the graph keeps.
+static pe_status upload_slot(pe_ctx c, size_t bytes, bool capturing, int T, CallSlot** out) {
+  if (!capturing) return take_call_slot(c, bytes, out);
+  while (c->cap_used < c->cap_slots.size() && c->cap_slots[c->cap_used].bytes < bytes) ++c->cap_used;
+  if (c->cap_used == c->cap_slots.size() || T > kCaptureMaxIters) {
+    g_last_error = "pe_polar under CUDA-graph capture: call pe_reserve for this batch before capturing "
+                   "(it keeps 4 upload slots per reservation; iters <= 64)";
+    return PE_ERR_WORKSPACE;
+  }
+  *out = &c->cap_slots[c->cap_used++];
+  return PE_OK;
+}
+
+// Small-matrix fused path (small_sm100.cuh): every matrix of the call has
+// min side <= 128 and max side <= 640 (bf16) / 128 (fp32): one CTA per
+// matrix runs the whole call.
+static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int* max_npad) {
+  static const bool on = !(getenv("PE_SMALL") && !strcmp(getenv("PE_SMALL"), "0"));   // A/B knob
+  if (!on || count < 1) return false;
+  int mx = 64;
+  for (int i = 0; i < count; ++i) {
+    const int64_t r = shapes[2 * i], cc = shapes[2 * i + 1];
+    const int64_t m = std::min(r, cc), npad = rup(std::max(r, cc), 64);
+    if (m > kSmallMaxM || npad > (dtype == PE_BF16 ? 640 : 128)) return false;
+    mx = std::max<int>(mx, (int)npad);
+  }
+  *max_npad = mx;
+  return true;
+}
+
+static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
+                            int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad) {
+  static SmallArgs a;                               // ~2.6 KB: keep it off the stack
+  const bool inl = count <= kSmallInlineMats && T <= kSmallInlineIters;
+  CallSlot* cs = nullptr;
+  const size_t mats_bytes = rup((size_t)count * sizeof(SmallMat), 128);
+  if (!inl) {
+    pe_status s = upload_slot(c, std::max(call_bytes(count, T), mats_bytes + (size_t)3 * T * sizeof(float)),
+                              capturing, T, &cs);
+    if (s != PE_OK) return s;
+  }
+  SmallMat* hm = inl ? a.inl : reinterpret_cast<SmallMat*>(cs->h);
+  for (int i = 0; i < count; ++i) {
+    SmallMat& sm = hm[i];
+    sm.in = in[i];
+    sm.out = out[i];
+    sm.rows = (int)shapes[2 * i];
+    sm.cols = (int)shapes[2 * i + 1];
+    sm.tall = sm.rows > sm.cols;                    // P:493, strict (R10)
+    sm.m = sm.tall ? sm.cols : sm.rows;
+    sm.n = sm.tall ? sm.rows : sm.cols;
+    sm.n_pad = (int)rup(sm.n, 64);
+    sm.fold = (dtype == PE_BF16) && (sm.cols % 8 == 0) && !getenv("PE_NO_FOLD");   // as build_plan
+    sm.pad = 0;
+  }
+  float* hc = inl ? a.inl_coef : reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(cs->h) + mats_bytes);
+  const int nq = (c->degree + 1) / 2;
+  for (int t = 0; t < T; ++t) {
+    const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
+    hc[3 * t] = (float)tup[0];
+    hc[3 * t + 1] = (float)tup[1];
+    hc[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
+  }
+  a.T = T;
+  if (inl) {
+    a.mats = nullptr;
+    a.coef = nullptr;
+  } else {
+    PE_CUDA(cudaMemcpyAsync(cs->d, cs->h, mats_bytes + (size_t)3 * T * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (!capturing) {
+      PE_CUDA(cudaEventRecord(cs->done, st));
+      cs->armed = true;
+    }
+    a.mats = reinterpret_cast<const SmallMat*>(cs->d);
+    a.coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + mats_bytes);
+  }
+  { ProfScope ps(c, 7, st);
+    if (dtype == PE_BF16) launch(pe_small_sm100<1>, count, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
+    else launch(pe_small_sm100<3>, count, kSmallThreads, small_smem_bytes<3>(max_npad), st, a); }
+  PE_CUDA(cudaGetLastError());
+  c->last_launches = 1;
+  return PE_OK;
+}
+
 // pe_polar and pe_muon_step.  Muon (grads != nullptr, bf16): `in` are the
 // momentum buffers M, updated in place by the norm kernel to
 // bf16(beta M + (1 - beta) G); `out` are the weights W, updated to
@@ -831,6 +921,9 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
   PE_CUDA(cudaStreamIsCapturing(st, &cap_status));
   const bool capturing = cap_status == cudaStreamCaptureStatusActive;
+  int max_npad = 0;
+  if (!muon && small_eligible(shapes, count, dtype, &max_npad))
+    return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad);
   Plan* P = nullptr;
   if (capturing) {
     // no allocation or synchronisation is allowed: the plan must be cached
@@ -873,19 +966,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     if (cudaMalloc(&c->scratch, sb) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
   }
   CallSlot* cs = nullptr;
-  if (capturing) {
-    // a captured call keeps its upload buffer for the graph's lifetime
-    const size_t need = call_bytes(count, T);
-    while (c->cap_used < c->cap_slots.size() && c->cap_slots[c->cap_used].bytes < need) ++c->cap_used;
-    if (c->cap_used == c->cap_slots.size() || T > kCaptureMaxIters) {
-      g_last_error = "pe_polar under CUDA-graph capture: call pe_reserve for this batch before capturing "
-                     "(it keeps 4 upload slots per reservation; iters <= 64)";
-      return PE_ERR_WORKSPACE;
-    }
-    cs = &c->cap_slots[c->cap_used++];
-  } else if ((s = take_call_slot(c, call_bytes(count, T), &cs)) != PE_OK) {
-    return s;
-  }
+  if ((s = upload_slot(c, call_bytes(count, T), capturing, T, &cs)) != PE_OK) return s;
   void** h = reinterpret_cast<void**>(cs->h);
   const size_t omap_off = call_ptr_bytes(count);
   CUtensorMap* h_maps = reinterpret_cast<CUtensorMap*>(reinterpret_cast<uint8_t*>(h) + omap_off);

@@ -1,0 +1,432 @@
+// Small-matrix fused path: the whole Polar Express
+// call for one matrix with min side m <= 128 in ONE CTA -- Frobenius norm,
+// orientation, T x (Gram, b A + c A^2, a X + B X) (Listing 2) and
+// the write-back -- with X and A/B resident in shared memory and every
+// product on tcgen05 (cta_group::1, M = 128, fp32 accumulators in TMEM).  One
+// launch per call instead of 3T + 1..3, for latency-bound problems (BASELINE
+// config 1, per-head Muon slices).
+//
+// The arithmetic is the large kernel's, step for step, so results are
+// bit-identical to it (tests/test_gpu_parity.py::test_small_path_*):
+//   bf16 (kP = 1): R8 rounding points, the folded first iteration
+//     (A = bf16(acc inv^2), X1 = bf16((a m + acc) inv)) exactly when the large
+//     path folds (cols % 8 == 0), else X_0 = bf16(m inv); K accumulated in
+//     64-wide blocks of four K=16 steps in ascending order;
+//   fp32 (kP = 3): three bf16 planes per buffer, the six plane products small
+//     terms first, the big p0 q0 chain split over two TMEM buffers at the
+//     same K block, X_0 = split3(fp32(m inv)), result = (p0 + p1) + p2.
+//
+// Shared memory (one CTA per matrix, 128 threads = 4 warps; thread r owns
+// TMEM lane / row r): X as kP planes of [128 rows][n_pad/64 blocks of 64
+// columns] bf16 in the 128-byte-swizzled layout the UMMA descriptors read
+// (K-major for the Gram, the same bytes MN-major for the update), A/B as kP
+// planes of [128][128]; rows >= m and columns >= n are zero, so padded
+// products contribute nothing.  B overwrites A in place (the poly epilogue
+// reads A_ij and writes B_ij at the same position after the MMA completed),
+// X' overwrites X chunk by chunk.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+
+namespace pe {
+
+constexpr int kSmallThreads = 128;
+constexpr int kSmallMaxM = 128;
+constexpr int kSmallTmemCols = 256;
+
+struct SmallMat {
+  const void* in;        // caller matrix (rows x cols, row-major)
+  void* out;
+  int rows, cols;
+  int m, n;              // wide orientation (m <= n)
+  int n_pad;             // n rounded up to 64
+  int tall;
+  int fold;              // bf16 with cols % 8 == 0: the large path folds 1/s into iteration 1
+  int pad;
+};
+
+// Small calls pass their descriptors as kernel parameters (no upload copy in
+// the call's critical path); larger ones point to an uploaded array.
+constexpr int kSmallInlineMats = 48;
+constexpr int kSmallInlineIters = 16;
+struct SmallArgs {
+  SmallMat inl[kSmallInlineMats];
+  float inl_coef[3 * kSmallInlineIters];
+  const SmallMat* mats;  // nullptr: use inl
+  const float* coef;     // per iteration fp32 (a, b, c); nullptr: use inl_coef
+  int T;
+};
+
+// byte offset of 16-byte unit u (columns 8u .. 8u+7) of row r in a
+// [128 rows][blocks of 64 columns] bf16 buffer with the 128-byte swizzle;
+// a quarter-warp's rows hit 8 distinct bank groups (conflict-free)
+__device__ __forceinline__ uint32_t small_unit(int r, int u) {
+  return (uint32_t)((u >> 3) * 16384 + r * 128 + (((u & 7) ^ (r & 7)) << 4));
+}
+
+template <int kP>
+__host__ __device__ constexpr size_t small_smem_bytes(int n_pad) {
+  return 1024 + (size_t)kP * 128 * n_pad * 2 + (size_t)kP * 128 * 128 * 2 + 64;
+}
+
+// 8 consecutive values of one row (one 16-byte unit per plane): kP = 1 the
+// bf16 value, kP = 3 (p0 + p1) + p2
+template <int kP>
+__device__ __forceinline__ void small_load8(const uint8_t* buf, size_t plane, uint32_t off, float* v) {
+  const uint4 u0 = *reinterpret_cast<const uint4*>(buf + off);
+  const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
+  if (kP == 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h0[q]);
+      v[2 * q] = f.x;
+      v[2 * q + 1] = f.y;
+    }
+  } else {
+    const uint4 u1 = *reinterpret_cast<const uint4*>(buf + plane + off);
+    const uint4 u2 = *reinterpret_cast<const uint4*>(buf + 2 * plane + off);
+    const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u2);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = __bfloat1622float2(h0[q]), b = __bfloat1622float2(h1[q]), c = __bfloat1622float2(h2[q]);
+      v[2 * q] = __fadd_rn(__fadd_rn(a.x, b.x), c.x);
+      v[2 * q + 1] = __fadd_rn(__fadd_rn(a.y, b.y), c.y);
+    }
+  }
+}
+// store 8 values (kP = 3: split into the three planes, as split3)
+template <int kP>
+__device__ __forceinline__ void small_store8(uint8_t* buf, size_t plane, uint32_t off, const float* v) {
+  uint4 u0, u1, u2;
+  __nv_bfloat162* h0 = reinterpret_cast<__nv_bfloat162*>(&u0);
+  __nv_bfloat162* h1 = reinterpret_cast<__nv_bfloat162*>(&u1);
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u2);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (kP == 1) {
+      h0[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    } else {
+      float p0[2], p1[2], p2[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        p0[e] = __bfloat162float(__float2bfloat16_rn(v[2 * q + e]));
+        const float r1 = __fsub_rn(v[2 * q + e], p0[e]);
+        p1[e] = __bfloat162float(__float2bfloat16_rn(r1));
+        p2[e] = __fsub_rn(r1, p1[e]);
+      }
+      h0[q] = __floats2bfloat162_rn(p0[0], p0[1]);
+      h1[q] = __floats2bfloat162_rn(p1[0], p1[1]);
+      h2[q] = __floats2bfloat162_rn(p2[0], p2[1]);
+    }
+  }
+  *reinterpret_cast<uint4*>(buf + off) = u0;
+  if (kP == 3) {
+    *reinterpret_cast<uint4*>(buf + plane + off) = u1;
+    *reinterpret_cast<uint4*>(buf + 2 * plane + off) = u2;
+  }
+}
+
+// fp32 accumulator: 32 columns of this thread's TMEM lane (kP = 3 and b1:
+// plus the second buffer, 128 columns further)
+template <int kP>
+__device__ __forceinline__ void small_acc32(uint32_t taddr, bool b1, float (&w)[32]) {
+  tmem_ld32(taddr, w);
+  if (kP == 3 && b1) {
+    float w2[32];
+    tmem_ld32(taddr + 128, w2);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w[j] = __fadd_rn(w[j], w2[j]);
+  }
+}
+
+// One product D = P Q (fp32 in TMEM): P is K-major at p_base (128 rows),
+// Q K-major (kQmn = false) or MN-major (kQmn = true, columns q_col0..) at
+// q_base; K = nkb blocks of 64.  kP = 3: the six plane products with the big
+// chain's second half in d + 128 (exactly the large kernel's order).
+template <int kP, bool kQmn>
+__device__ __forceinline__ void small_mma(uint32_t d, uint32_t p_base, size_t p_plane, uint32_t q_base,
+                                          size_t q_plane, int q_col0, int N, int nkb) {
+  const uint32_t idesc = idesc_bf16(128, N, 0, kQmn ? 1 : 0);
+  const int nseg = (kP == 3) ? 6 : 1;
+  const int n_first = (kP == 3) ? 5 * nkb + (nkb + 1) / 2 : nkb;
+  int step = 0;
+  for (int sg = 0; sg < nseg; ++sg) {
+    const int pa = (kP == 3) ? ((0x001012 >> (4 * sg)) & 0xF) : 0;
+    const int pb = (kP == 3) ? ((0x010210 >> (4 * sg)) & 0xF) : 0;
+    for (int kb = 0; kb < nkb; ++kb, ++step) {
+      const bool second = (kP == 3) && step >= n_first;
+      const uint32_t dd = second ? d + 128 : d;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t adesc = smem_desc_sw128(p_base + (uint32_t)(pa * p_plane) + kb * 16384 + k * 32, 16, 1024);
+        const uint64_t bdesc =
+            kQmn ? smem_desc_sw128(q_base + (uint32_t)(pb * q_plane) + (q_col0 >> 6) * 16384 + kb * 8192 + k * 2048,
+                                   16384, 1024)
+                 : smem_desc_sw128(q_base + (uint32_t)(pb * q_plane) + kb * 16384 + k * 32, 16, 1024);
+        const uint32_t acc = second ? (step > n_first || k > 0) : (step > 0 || k > 0);
+        umma_bf16(dd, adesc, bdesc, idesc, acc);
+      }
+    }
+  }
+}
+
+template <int kP>
+__global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_constant__ SmallArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const SmallMat md = args.mats ? args.mats[blockIdx.x] : args.inl[blockIdx.x];
+  const float* coef = args.coef ? args.coef : args.inl_coef;
+  const int n_pad = md.n_pad;
+  const size_t xplane = (size_t)128 * n_pad * 2;
+  const size_t aplane = (size_t)128 * 128 * 2;
+  uint8_t* X = smem;
+  uint8_t* A = smem + kP * xplane;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(A + kP * aplane);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  __shared__ double red[kSmallThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = md.m, n = md.n;
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, kSmallTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  // ---- norm (fp64 sum of exact squares, as pe_norm_kernel) and load.  The
+  // caller matrix is streamed row by row with 16-byte vectors when its rows
+  // allow (lanes along the row: coalesced); element (i, j) goes to X(r, c) with
+  // (r, c) = (i, j) (wide) or (j, i) (tall).  Folded bf16 keeps M
+  // (1/s is applied in iteration 1's epilogues), otherwise X_0 = m * inv
+  // (fp32: split into planes); rows >= m and columns >= n stay zero.
+  constexpr int V = (kP == 1) ? 8 : 4;                  // elements per 16-byte vector
+  const bool vec = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.in) & 15) == 0);
+  const bool fold = (kP == 1) && md.fold;
+  {
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int u = 0; u < n_pad / 8; ++u) small_store8<kP>(X, xplane, small_unit(tid, u), z);
+    for (int u = 0; u < 16; ++u) small_store8<kP>(A, aplane, small_unit(tid, u), z);
+  }
+  auto load_vec = [&](int64_t e, float* f) {
+    if (kP == 1) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + e));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 t2 = __bfloat1622float2(h[k]);
+        f[2 * k] = t2.x;
+        f[2 * k + 1] = t2.y;
+      }
+    } else {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.in) + e));
+      f[0] = q.x; f[1] = q.y; f[2] = q.z; f[3] = q.w;
+    }
+  };
+  auto load_one = [&](int64_t e) {
+    return (kP == 1) ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(md.in)[e])
+                     : reinterpret_cast<const float*>(md.in)[e];
+  };
+  auto put = [&](int i, int j, float f) {          // caller element (i, j) into X (after the norm)
+    const int rr = md.tall ? j : i, cc = md.tall ? i : j;
+    const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
+    if (kP == 1) {
+      *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(f);
+    } else {
+      const float p0 = __bfloat162float(__float2bfloat16_rn(f));
+      const float r1 = __fsub_rn(f, p0);
+      const float p1 = __bfloat162float(__float2bfloat16_rn(r1));
+      *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(p0);
+      *reinterpret_cast<__nv_bfloat16*>(X + xplane + off) = __float2bfloat16_rn(p1);
+      *reinterpret_cast<__nv_bfloat16*>(X + 2 * xplane + off) = __float2bfloat16_rn(__fsub_rn(r1, p1));
+    }
+  };
+  // warp w walks caller rows w, w+4, ...; its lanes walk along the row
+  // (coalesced), V elements per lane per step when vectorised
+  const int vpr = vec ? md.cols / V : md.cols;
+  __syncthreads();                                  // zeroing done before the scattered writes
+  double acc = 0.0;
+  for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+    const int64_t row = (int64_t)i * md.cols;
+    for (int jv = lane; jv < vpr; jv += 32) {
+      if (vec) {
+        float f[V];
+        load_vec(row + (int64_t)jv * V, f);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc += (kP == 1) ? (double)(f[k] * f[k]) : (double)f[k] * f[k];
+        if (fold) {                                   // (the values are already bf16)
+          if (!md.tall) {                             // 8 columns of one row: one 16-byte unit
+            *reinterpret_cast<uint4*>(X + small_unit(i, jv)) =
+                __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + row + jv * V));
+          } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) put(i, jv * V + k, f[k]);
+          }
+        }
+      } else {
+        const float v = load_one(row + jv);
+        acc += (kP == 1) ? (double)(v * v) : (double)v * v;
+        if (fold) put(i, jv, v);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  double ss = 0.0;
+  for (int w = 0; w < kSmallThreads / 32; ++w) ss += red[w];
+  const float inv = (float)(1.0 / (sqrt(ss) * 1.01 + 1e-7));    // P:494, reading R1/R2
+  if (!fold) {                                      // second (L2-hot) pass: X_0 = m * inv
+    for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+      const int64_t row = (int64_t)i * md.cols;
+      for (int jv = lane; jv < vpr; jv += 32) {
+        if (vec) {
+          float f[V];
+          load_vec(row + (int64_t)jv * V, f);
+#pragma unroll
+          for (int k = 0; k < V; ++k) put(i, jv * V + k, __fmul_rn(f[k], inv));
+        } else {
+          put(i, jv, __fmul_rn(load_one(row + jv), inv));
+        }
+      }
+    }
+  }
+  const int r = tid;
+
+  const uint32_t xs = smem_u32(X), as = smem_u32(A);
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t phase = 0;
+  auto sync_for_mma = [&]() {
+    fence_async_smem();          // generic smem writes -> the tensor core's (async proxy) reads
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto run_and_wait = [&](auto issue) {
+    if (tid == 0) {
+      issue();
+      umma_commit(bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+  };
+  const int nkx = n_pad / 64;                   // K blocks of the Gram
+  const float inv2 = __fmul_rn(inv, inv);
+  // Padded rows/columns compute to exact zeros in every phase (their
+  // operands are zero), so each thread processes its whole padded row.
+  for (int t = 0; t < args.T; ++t) {
+    const float a = coef[3 * t], b = coef[3 * t + 1], cc3 = coef[3 * t + 2];
+    const bool first = (t == 0), last = (t == args.T - 1);
+    // ---- Gram A = X X^T
+    sync_for_mma();
+    run_and_wait([&] { small_mma<kP, false>(tmem, xs, xplane, xs, xplane, 0, 128, nkx); });
+#pragma unroll 1
+    for (int g = 0; g < 4; ++g) {
+      float w[32];
+      small_acc32<kP>(trow + 32 * g, nkx >= 2, w);
+      if (fold && first) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(w[j], inv2);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) small_store8<kP>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
+    }
+    // ---- B = b A + c A A, in place over A
+    sync_for_mma();
+    run_and_wait([&] { small_mma<kP, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
+#pragma unroll 1
+    for (int g = 0; g < 4; ++g) {
+      float w[32];
+      small_acc32<kP>(trow + 32 * g, true, w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float o[8];
+        const uint32_t off = small_unit(r, 4 * g + q);
+        small_load8<kP>(A, aplane, off, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(__fmul_rn(b, o[j]), __fmul_rn(cc3, w[8 * q + j]));
+        small_store8<kP>(A, aplane, off, o);
+      }
+    }
+    // ---- X' = a X + B X, column chunks in place
+    sync_for_mma();
+    const int chunk = (kP == 1) ? 256 : 128;
+    for (int q0 = 0; q0 < n_pad; q0 += chunk) {
+      const int N = min(chunk, n_pad - q0);
+      run_and_wait([&] { small_mma<kP, true>(tmem, as, aplane, xs, xplane, q0, N, 2); });
+#pragma unroll 1
+      for (int g = 0; g < N / 32; ++g) {
+        float w[32];
+        small_acc32<kP>(trow + 32 * g, true, w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int u = (q0 + 32 * g) / 8 + q;
+          const uint32_t off = small_unit(r, u);
+          float o[8];
+          small_load8<kP>(X, xplane, off, o);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            o[j] = __fadd_rn(__fmul_rn(a, o[j]), w[8 * q + j]);
+            if (fold && first) o[j] = __fmul_rn(o[j], inv);
+          }
+          small_store8<kP>(X, xplane, off, o);
+        }
+      }
+      tc_fence_before();
+      __syncthreads();               // TMEM reads done before the next chunk's MMA
+      tc_fence_after();
+    }
+    (void)last;
+  }
+  // ---- write-back in the caller's orientation, flat and coalesced;
+  // fp32 output = (p0 + p1) + p2 of the planes (the large path's join)
+  const bool vout = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.out) & 15) == 0) && !md.tall;
+  auto get = [&](int i, int j) {                   // caller element (i, j) from X
+    const int rr = md.tall ? j : i, cc = md.tall ? i : j;
+    const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
+    float f = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + off));
+    if (kP == 3)
+      f = __fadd_rn(__fadd_rn(f, __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + xplane + off))),
+                    __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + 2 * xplane + off)));
+    return f;
+  };
+  __syncthreads();                                  // every row of X' is in smem
+  const int vpo = vout ? md.cols / V : md.cols;
+  for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+    const int64_t row = (int64_t)i * md.cols;
+    for (int jv = lane; jv < vpo; jv += 32) {
+      if (vout) {
+        if (kP == 1) {
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(md.out) + row + jv * V) =
+              *reinterpret_cast<const uint4*>(X + small_unit(i, jv));        // wide: one unit
+        } else {
+          float f[V];
+#pragma unroll
+          for (int k = 0; k < V; ++k) f[k] = get(i, jv * V + k);
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(md.out) + row + jv * V) =
+              make_float4(f[0], f[1], f[2], f[3]);
+        }
+      } else {
+        const float f = get(i, jv);
+        if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[row + jv] = __float2bfloat16_rn(f);
+        else reinterpret_cast<float*>(md.out)[row + jv] = f;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, kSmallTmemCols);
+}
+
+}  // namespace pe

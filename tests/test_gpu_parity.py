@@ -556,8 +556,9 @@ def test_cuda_graph_capture_and_replay(ctx):
         assert torch.equal(yf[0], directf[0])
         for a, b in zip(W + Mo, w0 + m0):
             assert torch.equal(a, b)
-    # not reserved -> clean error during capture
-    xo = [to_dev_bf16(syn.gaussian(100, 300, seed=160, std=0.02))]
+    # not reserved (and too large for the small-matrix path, which needs no
+    # plan) -> clean error during capture
+    xo = [to_dev_bf16(syn.gaussian(300, 700, seed=160, std=0.02))]
     g4 = torch.cuda.CUDAGraph()
     import warnings
     with warnings.catch_warnings():
@@ -606,3 +607,58 @@ def test_large_batch_of_small_random_shapes(ctx):
             assert om.rel_frobenius(X, ref) <= (2e-2 if m >= 64 else (3e-2 if m >= 16 else 1e-1))
     for i in (0, 17, 123, 299):
         assert np.array_equal(run(ctx, [mats[i]])[0], outs[i])
+
+
+_SMALL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2505_16932_b200 as pe
+data = np.load(sys.argv[2])
+ctx = pe.Context(0)
+out = {}
+for key in sorted(data.files):
+    dt, T = key.split("_")[0], int(key.split("_")[1])
+    a = data[key]
+    x = torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).cuda() if dt == "b" else torch.from_numpy(a).cuda()
+    y = ctx.polar([x], iters=T)[0]
+    torch.cuda.synchronize()
+    out[key] = (y.view(torch.int16) if dt == "b" else y.view(torch.int32)).cpu().numpy()
+    out["launches_" + key] = np.array([ctx.last_launch_count()])
+np.savez(sys.argv[3], **out)
+"""
+
+
+def test_small_path_bit_identical_to_large_path(tmp_path):
+    """The small-matrix fused path (one CTA per matrix, the whole call in one
+    launch) reproduces the large path bit for bit: bf16 folded (cols % 8 == 0)
+    and unfolded shapes, both orientations, rank one; fp32 (three planes)
+    including config 1 (128 x 128); T = 1, 3, 5.  PE_SMALL=0 forces the large
+    path; the small path is a single launch."""
+    import os
+    import subprocess
+    import sys
+    cases = {}
+    k = 0
+    for T in (1, 3, 5):
+        for (r, c) in [(128, 128), (64, 640), (640, 64), (96, 200), (200, 90), (1, 64), (37, 100), (128, 600)]:
+            bits = syn.f32_to_bf16_bits(syn.gaussian(r, c, seed=300 + k, std=0.02).astype(np.float32))
+            cases[f"b_{T}_{k:03d}"] = bits
+            k += 1
+        for (r, c) in [(128, 128), (50, 100), (100, 50), (1, 8), (127, 33)]:
+            cases[f"f_{T}_{k:03d}"] = syn.gaussian(r, c, seed=300 + k).astype(np.float32)
+            k += 1
+    src = tmp_path / "in.npz"
+    np.savez(src, **cases)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, PE_SMALL=flag)
+        dst = tmp_path / f"out{flag}.npz"
+        p = subprocess.run([sys.executable, "-c", _SMALL_SCRIPT, root, str(src), str(dst)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[flag] = np.load(dst)
+    for key in cases:
+        assert np.array_equal(res["0"][key], res["1"][key]), key
+        assert int(res["1"]["launches_" + key][0]) == 1
+        assert int(res["0"]["launches_" + key][0]) > 3
