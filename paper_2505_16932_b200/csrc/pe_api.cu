@@ -40,13 +40,11 @@
 
 using namespace pe;
 
-// smem ring depths of the two GEMM instantiations (gemm_smem_bytes must stay
-// below the 227 KB per-CTA limit: 5 x 32 KB ring + 64 KB epilogue slots)
+// smem ring depths of the GEMM instantiations (gemm_smem_bytes must stay
+// below the 227 KB per-CTA limit): poly/update 5 x 32 KB ring + 64 KB
+// epilogue slots
 #ifndef PE_LONG_STAGES
 #define PE_LONG_STAGES 5
-#endif
-#ifndef PE_SHORT_STAGES
-#define PE_SHORT_STAGES 4
 #endif
 constexpr int kLongStages = PE_LONG_STAGES;
 // the Gram (no epilogue operand, one 4 KB staging slot per warp) takes 6
@@ -54,7 +52,6 @@ constexpr int kLongStages = PE_LONG_STAGES;
 #define PE_GRAM_STAGES 6
 #endif
 constexpr int kGramStages = PE_GRAM_STAGES;
-constexpr int kShortStages = PE_SHORT_STAGES;
 // fp32 (three bf16 planes): 4 x 32 KB ring + 8 warps x 3 plane slots x 4 KB
 constexpr int kP3Stages = 4;
 
@@ -147,7 +144,6 @@ struct Plan {
   int fused_T = 0, n_fused = 0;
   Tile* fused = nullptr;
   size_t fused_cap = 0;
-  bool long_k[3] = {true, true, true};   // per GEMM mode: 5-stage (else 4-stage) instantiation
   size_t ws_needed = 0;
   uint64_t last_use = 0;
 };
@@ -305,10 +301,6 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
                                (int)gemm_smem_bytes<kLongStages, 2>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kLongStages, 2>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kShortStages, 2>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kShortStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kShortStages, 2>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kP3Stages, 3, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kP3Stages, 3>()));
   PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -639,13 +631,6 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->flags = mflags;
   P->mats = mats;
   P->count = count;
-  // kernel variant per mode (measured on B200, profiles/r1_variants.md): the
-  // 5-stage instantiation for every phase; PE_GEMM_VARIANT=short selects the
-  // 4-stage one (A/B experiments).
-  {
-    const char* ov = getenv("PE_GEMM_VARIANT");
-    for (int mode = 0; mode < 3; ++mode) P->long_k[mode] = !(ov && !strcmp(ov, "short"));
-  }
   P->n_sym = (int)sym.size();
   P->n_upd = (int)upd.size();
   for (int k = 0; k < 4; ++k) P->n_it[k] = (int)it[k].size();
@@ -840,7 +825,7 @@ static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int
 
 static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
                             int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad) {
-  static SmallArgs a;                               // ~2.6 KB: keep it off the stack
+  SmallArgs a;                                      // ~2.6 KB of kernel parameters
   const bool inl = count <= kSmallInlineMats && T <= kSmallInlineIters;
   CallSlot* cs = nullptr;
   const size_t mats_bytes = rup((size_t)count * sizeof(SmallMat), 128);
@@ -1120,14 +1105,10 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         const size_t sm = gemm_smem_bytes<kGramStages, 1>();
         if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
         else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
-      } else if (P->long_k[mode]) {
+      } else {
         const size_t sm = gemm_smem_bytes<kLongStages, 2>();
         if (edge) launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, sm, st, g);
         else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
-      } else {
-        const size_t sm = gemm_smem_bytes<kShortStages, 2>();
-        if (edge) launch(pe_gemm_sm100<kShortStages, 2, true>, grid, kGemmThreads, sm, st, g);
-        else launch(pe_gemm_sm100<kShortStages, 2, false>, grid, kGemmThreads, sm, st, g);
       }
       ++launches;
     }

@@ -30,7 +30,7 @@ a = np.array(buf[:], dtype=np.int64).reshape(3, 256, 8)
 for mode, name in enumerate(["gram", "poly", "update"]):
     lead = a[mode, 0:148:2]          # leader CTAs
     tot = lead[:, 0].astype(float)
-    print(f"{wl} {os.environ.get('PE_GEMM_VARIANT','auto')} {name}: total {tot.mean()/1e3:.1f}k cyc, "
+    print(f"{wl} {os.environ.get('PE_FUSED','0')} {name}: total {tot.mean()/1e3:.1f}k cyc, "
           f"MMA waits tempty {100*lead[:,1].mean()/tot.mean():.1f}%, waits full {100*lead[:,2].mean()/tot.mean():.1f}%, "
           f"epi waits tfull {100*lead[:,3].mean()/tot.mean():.1f}%  (min/max total {tot.min()/1e3:.0f}k/{tot.max()/1e3:.0f}k)"
           f"  issue->full latency {lead[:,4].sum()/max(lead[:,5].sum(),1):.0f} cyc/stage over {lead[:,5].sum()/74:.0f} stages/CTA")

@@ -28,5 +28,5 @@ for _ in range(calls):
     ctx.polar(xs, ys, iters=5)
 torch.cuda.synchronize()
 prof = ctx.profile_read()
-tag = os.environ.get("PE_DEBUG_GEMM", "0") + "/" + os.environ.get("PE_GEMM_VARIANT", "auto")
+tag = os.environ.get("PE_DEBUG_GEMM", "0") + "/" + os.environ.get("PE_FUSED", "0")
 print(wl, tag, " ".join(f"{k}={v[0] / max(v[1], 1) * 1e3:.1f}us" for k, v in prof.items() if v[1]))

@@ -531,22 +531,34 @@ def test_cuda_graph_capture_and_replay(ctx):
     Mo = [x.clone() for x in xs]
     G = [x.clone() * 2 for x in xs]
     torch.cuda.synchronize()
-    g1, g2, g3 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    # a batch the small-matrix path takes (one launch, descriptors as kernel parameters)
+    small_shapes = [(100, 300), (64, 64), (128, 40)]
+    xsm = [to_dev_bf16(syn.gaussian(r, c, seed=170 + i, std=0.02)) for i, (r, c) in enumerate(small_shapes)]
+    ysm = [torch.empty_like(x) for x in xsm]
+    ctx.reserve(small_shapes, pe.PE_BF16)
+    g1, g2, g3, g5 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(g1):
         ctx.polar(xs, ys, iters=5)
     with torch.cuda.graph(g2):
         ctx.polar(xf, yf, iters=5)
     with torch.cuda.graph(g3):
         ctx.muon_step(W, Mo, G, beta=0.9, lr=0.1, iters=5)
+    with torch.cuda.graph(g5):
+        ctx.polar(xsm, ysm, iters=5)
     for rep in range(2):
         for i, (r, c) in enumerate(shapes):
             xs[i].copy_(to_dev_bf16(syn.gaussian(r, c, seed=140 + 10 * rep + i, std=0.02)))
         xf[0].copy_(torch.from_numpy(syn.gaussian(256, 512, seed=150 + rep).astype(np.float32)).cuda())
         w0, m0 = [w.clone() for w in W], [m.clone() for m in Mo]
+        for i, (r, c) in enumerate(small_shapes):
+            xsm[i].copy_(to_dev_bf16(syn.gaussian(r, c, seed=180 + 10 * rep + i, std=0.02)))
         g1.replay()
         g2.replay()
         g3.replay()
+        g5.replay()
         torch.cuda.synchronize()
+        for a, b in zip(ysm, ctx.polar([x.clone() for x in xsm], iters=5)):
+            assert torch.equal(a, b)
         direct = ctx.polar([x.clone() for x in xs], iters=5)
         directf = ctx.polar([xf[0].clone()], iters=5)
         ctx.muon_step(w0, m0, G, beta=0.9, lr=0.1, iters=5)
