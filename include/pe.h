@@ -212,7 +212,7 @@ pe_status pe_last_launch_count(pe_ctx ctx, int* launches);
  *   6 fused (pe_gemm_sm100 running every phase of the call in one launch;
  *     bf16 with PE_FUSED=1 set in the environment, otherwise one launch per phase)
  *   7 small (pe_small_sm100: the whole call in one launch, one CTA per
- *     matrix, when every matrix has min side <= 128 and max side <= 640
+ *     matrix, when every matrix has min side <= 128 and max side <= 768
  *     (bf16) / 128 (fp32); PE_SMALL=0 disables it)
  */
 #define PE_PROFILE_KINDS 8

@@ -304,7 +304,7 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kP3Stages, 3, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kP3Stages, 3>()));
   PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)small_smem_bytes<1>(640)));
+                               (int)small_smem_bytes<1>(kSmallMaxNpadBf16)));
   PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)small_smem_bytes<3>(128)));
   if (!get_encode_fn()) {
@@ -807,7 +807,7 @@ static pe_status upload_slot(pe_ctx c, size_t bytes, bool capturing, int T, Call
 }
 
 // Small-matrix fused path (small_sm100.cuh): every matrix of the call has
-// min side <= 128 and max side <= 640 (bf16) / 128 (fp32): one CTA per
+// min side <= 128 and max side <= 768 (bf16) / 128 (fp32): one CTA per
 // matrix runs the whole call.
 static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int* max_npad) {
   static const bool on = !(getenv("PE_SMALL") && !strcmp(getenv("PE_SMALL"), "0"));   // A/B knob
@@ -816,7 +816,7 @@ static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int
   for (int i = 0; i < count; ++i) {
     const int64_t r = shapes[2 * i], cc = shapes[2 * i + 1];
     const int64_t m = std::min(r, cc), npad = rup(std::max(r, cc), 64);
-    if (m > kSmallMaxM || npad > (dtype == PE_BF16 ? 640 : 128)) return false;
+    if (m > kSmallMaxM || npad > (dtype == PE_BF16 ? kSmallMaxNpadBf16 : kSmallMaxNpadF32)) return false;
     mx = std::max<int>(mx, (int)npad);
   }
   *max_npad = mx;

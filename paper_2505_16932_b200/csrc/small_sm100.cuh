@@ -34,6 +34,10 @@ namespace pe {
 constexpr int kSmallThreads = 128;
 constexpr int kSmallMaxM = 128;
 constexpr int kSmallTmemCols = 256;
+// largest padded max side: bf16 X (128 x 768) + A (128 x 128) = 224 KB of smem;
+// fp32 three planes of X (128 x 128) and A = 192 KB
+constexpr int kSmallMaxNpadBf16 = 768;
+constexpr int kSmallMaxNpadF32 = 128;
 
 struct SmallMat {
   const void* in;        // caller matrix (rows x cols, row-major)
@@ -248,12 +252,36 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
       *reinterpret_cast<__nv_bfloat16*>(X + 2 * xplane + off) = __float2bfloat16_rn(__fsub_rn(r1, p1));
     }
   };
-  // warp w walks caller rows w, w+4, ...; its lanes walk along the row
-  // (coalesced), V elements per lane per step when vectorised
+  // Tall inputs: thread r gathers its X row r = caller column r, four
+  // 16-byte units (32 loads) in flight; a warp's loads of one caller row are
+  // contiguous.  Wide inputs: warp w walks caller rows w, w+4, ...; its lanes
+  // walk along the row (coalesced), V elements per lane per step.
+  const int nunits = n_pad / 8;
+  auto gather = [&](int u0, float (&f)[4][8]) {
+#pragma unroll
+    for (int uu = 0; uu < 4; ++uu)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = 8 * (u0 + uu) + k;
+        f[uu][k] = (tid < m && c < n) ? load_one((int64_t)c * md.cols + tid) : 0.f;
+      }
+  };
   const int vpr = vec ? md.cols / V : md.cols;
   __syncthreads();                                  // zeroing done before the scattered writes
   double acc = 0.0;
-  for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+  if (md.tall) {
+    for (int u0 = 0; u0 < nunits; u0 += 4) {
+      float f[4][8];
+      gather(u0, f);
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += (kP == 1) ? (double)(f[uu][k] * f[uu][k]) : (double)f[uu][k] * f[uu][k];
+        if (fold && u0 + uu < nunits) small_store8<kP>(X, xplane, small_unit(tid, u0 + uu), f[uu]);
+      }
+    }
+  }
+  for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
     const int64_t row = (int64_t)i * md.cols;
     for (int jv = lane; jv < vpr; jv += 32) {
       if (vec) {
@@ -284,7 +312,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
   double ss = 0.0;
   for (int w = 0; w < kSmallThreads / 32; ++w) ss += red[w];
   const float inv = (float)(1.0 / (sqrt(ss) * 1.01 + 1e-7));    // P:494, reading R1/R2
-  if (!fold) {                                      // second (L2-hot) pass: X_0 = m * inv
+  if (!fold && md.tall) {                           // second (L2-hot) pass: X_0 = m * inv
+    for (int u0 = 0; u0 < nunits; u0 += 4) {
+      float f[4][8];
+      gather(u0, f);
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[uu][k] = __fmul_rn(f[uu][k], inv);
+        if (u0 + uu < nunits) small_store8<kP>(X, xplane, small_unit(tid, u0 + uu), f[uu]);
+      }
+    }
+  } else if (!fold) {
     for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
       const int64_t row = (int64_t)i * md.cols;
       for (int jv = lane; jv < vpr; jv += 32) {
@@ -401,8 +440,24 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
     return f;
   };
   __syncthreads();                                  // every row of X' is in smem
+  if (md.tall && tid < m) {
+    // thread r scatters its X row r into caller column r (a warp's stores to
+    // one caller row are contiguous)
+    for (int u = 0; u < nunits; ++u) {
+      float f[8];
+      small_load8<kP>(X, xplane, small_unit(tid, u), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = 8 * u + k;
+        if (c >= n) break;
+        const size_t e = (size_t)c * md.cols + tid;
+        if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[e] = __float2bfloat16_rn(f[k]);
+        else reinterpret_cast<float*>(md.out)[e] = f[k];
+      }
+    }
+  }
   const int vpo = vout ? md.cols / V : md.cols;
-  for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+  for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
     const int64_t row = (int64_t)i * md.cols;
     for (int jv = lane; jv < vpo; jv += 32) {
       if (vout) {

@@ -20,3 +20,19 @@ for dt in (torch.float32, torch.bfloat16):
                 torch.cuda._sleep(2000000); a.record(); ctx.polar([x], [y], iters=T); b.record(); torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
             res.append(statistics.median(ms) * 1e3)
         print(dt, shape, " ".join(f"T={T}:{v:.1f}us" for T, v in zip((1, 2, 5), res)), flush=True)
+
+# per-head Muon slices: GPT-2 Small attention q, k, v, o split
+# into 12 heads each (768 x 64), 12 layers -> 576 matrices in one call
+hs = [(torch.randn((768, 64), device="cuda") * 0.02).bfloat16() for _ in range(576)]
+ho = [torch.empty_like(h) for h in hs]
+for _ in range(3):
+    ctx.polar(hs, ho, iters=5)
+torch.cuda.synchronize()
+ms = []
+for _ in range(10):
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda._sleep(2000000); a.record(); ctx.polar(hs, ho, iters=5); b.record(); torch.cuda.synchronize()
+    ms.append(a.elapsed_time(b))
+m = statistics.median(ms)
+print(f"per-head GPT-2 S attention slices (576 x 768x64 bf16), T=5: {m * 1e3:.1f} us, "
+      f"{pe.pe_flops([(768, 64)] * 576, 5) / (m * 1e-3) / 1e12:.1f} TF/s", flush=True)

@@ -652,7 +652,8 @@ def test_small_path_bit_identical_to_large_path(tmp_path):
     cases = {}
     k = 0
     for T in (1, 3, 5):
-        for (r, c) in [(128, 128), (64, 640), (640, 64), (96, 200), (200, 90), (1, 64), (37, 100), (128, 600)]:
+        for (r, c) in [(128, 128), (64, 640), (640, 64), (96, 200), (200, 90), (1, 64), (37, 100), (128, 600),
+                       (64, 768), (768, 64)]:
             bits = syn.f32_to_bf16_bits(syn.gaussian(r, c, seed=300 + k, std=0.02).astype(np.float32))
             cases[f"b_{T}_{k:03d}"] = bits
             k += 1
