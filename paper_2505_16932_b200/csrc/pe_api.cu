@@ -823,8 +823,23 @@ static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int
   return true;
 }
 
+// Per-call upload of `bytes` from the slot's pinned buffer.  `up` (pe_polar_host)
+// is the H2D copy stream: queued there, the small upload is not stuck behind
+// the next group's bulk copies in the copy engine; the kernels on `st` wait
+// for it through the slot's event.
+static pe_status upload_call(CallSlot* cs, size_t bytes, cudaStream_t st, cudaStream_t up, bool capturing) {
+  cudaStream_t us = up ? up : st;
+  PE_CUDA(cudaMemcpyAsync(cs->d, cs->h, bytes, cudaMemcpyHostToDevice, us));
+  if (!capturing) {
+    PE_CUDA(cudaEventRecord(cs->done, us));
+    cs->armed = true;
+    if (us != st) PE_CUDA(cudaStreamWaitEvent(st, cs->done, 0));
+  }
+  return PE_OK;
+}
+
 static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
-                            int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad) {
+                            int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad, cudaStream_t up) {
   SmallArgs a;                                      // ~2.6 KB of kernel parameters
   const bool inl = count <= kSmallInlineMats && T <= kSmallInlineIters;
   CallSlot* cs = nullptr;
@@ -861,11 +876,8 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     a.mats = nullptr;
     a.coef = nullptr;
   } else {
-    PE_CUDA(cudaMemcpyAsync(cs->d, cs->h, mats_bytes + (size_t)3 * T * sizeof(float), cudaMemcpyHostToDevice, st));
-    if (!capturing) {
-      PE_CUDA(cudaEventRecord(cs->done, st));
-      cs->armed = true;
-    }
+    pe_status s = upload_call(cs, mats_bytes + (size_t)3 * T * sizeof(float), st, up, capturing);
+    if (s != PE_OK) return s;
     a.mats = reinterpret_cast<const SmallMat*>(cs->d);
     a.coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + mats_bytes);
   }
@@ -884,7 +896,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
 // matrices) or the finalize pass (the others).
 static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, const void* const* grads,
                             const int64_t* shapes, int count, int iters, pe_dtype dtype, void* stream_,
-                            double beta, double lr) {
+                            double beta, double lr, cudaStream_t up = nullptr) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   if (count == 0) { c->last_launches = 0; return PE_OK; }
   if (!in || !out) return PE_ERR_INVALID_ARG;
@@ -908,7 +920,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   const bool capturing = cap_status == cudaStreamCaptureStatusActive;
   int max_npad = 0;
   if (!muon && small_eligible(shapes, count, dtype, &max_npad))
-    return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad);
+    return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad, up);
   Plan* P = nullptr;
   if (capturing) {
     // no allocation or synchronisation is allowed: the plan must be cached
@@ -978,11 +990,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     h_coef[3 * t + 1] = (float)tup[1];
     h_coef[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
   }
-  PE_CUDA(cudaMemcpyAsync(cs->d, h, call_bytes(count, T), cudaMemcpyHostToDevice, st));
-  if (!capturing) {
-    PE_CUDA(cudaEventRecord(cs->done, st));
-    cs->armed = true;
-  }
+  if ((s = upload_call(cs, call_bytes(count, T), st, up, capturing)) != PE_OK) return s;
   void** d_ptrs = reinterpret_cast<void**>(cs->d);
   const CUtensorMap* d_imaps =
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
@@ -1210,7 +1218,8 @@ extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const*
     PE_CUDA(cudaEventRecord(eh, c->s_h2d));
     PE_CUDA(cudaStreamWaitEvent(st, eh, 0));
     if (!skip_compute) {
-      s = pe_polar(c, dptr.data() + b, dptr.data() + b, shapes + 2 * b, e - b, iters, dtype, stream_);
+      s = polar_impl(c, dptr.data() + b, dptr.data() + b, nullptr, shapes + 2 * b, e - b, iters, dtype, stream_,
+                     0.0, 0.0, c->s_h2d);
       if (s != PE_OK) return s;
       launches += c->last_launches;
     }
