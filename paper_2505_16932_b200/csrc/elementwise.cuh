@@ -388,4 +388,13 @@ __global__ void __launch_bounds__(256) pe_planes_kernel(const CopyArgs a) {
   }
 }
 
+// Per-call upload of a pe_polar call (pointers, caller tensor maps,
+// coefficients) from its mapped pinned host buffer, read over PCIe by the
+// SMs: it never waits in the copy engines behind unrelated bulk transfers.
+__global__ void __launch_bounds__(256) pe_upload_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                        int n) {
+  pdl_trigger();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace pe

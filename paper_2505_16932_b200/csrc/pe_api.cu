@@ -150,7 +150,8 @@ struct Plan {
 
 // One pinned upload buffer of the per-call ring.
 struct CallSlot {
-  void* h = nullptr;            // pinned host
+  void* h = nullptr;            // pinned host (mapped)
+  const void* hd = nullptr;     // the same buffer as seen from the device (UVA), or nullptr
   void* d = nullptr;            // device
   size_t bytes = 0;
   cudaEvent_t done = nullptr;   // recorded after the upload on the call's stream
@@ -188,6 +189,7 @@ struct pe_ctx_s {
   std::vector<cudaEvent_t> host_ev;
 
   int last_launches = 0;
+  int uploads = 0;              // upload-kernel launches of the current call (counted in last_launches)
   int* done = nullptr;          // fused schedule completion counters (cleared by the norm kernel)
   float* scratch = nullptr;     // fp32 path: per-CTA running sums of the K passes (gemm_sm100.cuh)
   size_t done_cap = 0;
@@ -720,6 +722,18 @@ static pe_status ensure_fused(pe_ctx c, Plan* P, int T) {
   return PE_OK;
 }
 
+// Device buffer + mapped pinned host buffer of one upload slot.
+static bool alloc_slot(CallSlot& cs, size_t nb) {
+  void* hd = nullptr;
+  if (cudaMalloc(&cs.d, nb) != cudaSuccess || cudaHostAlloc(&cs.h, nb, cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cs.hd = (cudaHostGetDevicePointer(&hd, cs.h, 0) == cudaSuccess) ? hd : nullptr;
+  cudaGetLastError();
+  return true;
+}
+
 constexpr int kCaptureSpare = 4;
 constexpr int kCaptureMaxIters = 64;
 
@@ -743,20 +757,14 @@ extern "C" pe_status pe_reserve(pe_ctx c, const int64_t* shapes, int count, pe_d
       if (cs.d) cudaFree(cs.d);
       if (cs.h) cudaFreeHost(cs.h);
       cs = CallSlot();
-      if (cudaMalloc(&cs.d, need) != cudaSuccess || cudaMallocHost(&cs.h, need) != cudaSuccess) {
-        cudaGetLastError();
-        return PE_ERR_WORKSPACE;
-      }
+      if (!alloc_slot(cs, need)) return PE_ERR_WORKSPACE;
       cs.bytes = need;
     }
     ++spare;
   }
   while (spare < (size_t)kCaptureSpare) {
     CallSlot cs;
-    if (cudaMalloc(&cs.d, need) != cudaSuccess || cudaMallocHost(&cs.h, need) != cudaSuccess) {
-      cudaGetLastError();
-      return PE_ERR_WORKSPACE;
-    }
+    if (!alloc_slot(cs, need)) return PE_ERR_WORKSPACE;
     cs.bytes = need;
     c->cap_slots.push_back(cs);
     ++spare;
@@ -782,10 +790,7 @@ static pe_status take_call_slot(pe_ctx c, size_t bytes, CallSlot** out) {
     if (cs.h) { cudaFreeHost(cs.h); cs.h = nullptr; }
     cs.bytes = 0;
     const size_t nb = std::max<size_t>(bytes, 64 * 1024);
-    if (cudaMalloc(&cs.d, nb) != cudaSuccess || cudaMallocHost(&cs.h, nb) != cudaSuccess) {
-      cudaGetLastError();
-      return PE_ERR_WORKSPACE;
-    }
+    if (!alloc_slot(cs, nb)) return PE_ERR_WORKSPACE;
     cs.bytes = nb;
   }
   *out = &cs;
@@ -827,7 +832,20 @@ static bool small_eligible(const int64_t* shapes, int count, pe_dtype dtype, int
 // is the H2D copy stream: queued there, the small upload is not stuck behind
 // the next group's bulk copies in the copy engine; the kernels on `st` wait
 // for it through the slot's event.
-static pe_status upload_call(CallSlot* cs, size_t bytes, cudaStream_t st, cudaStream_t up, bool capturing) {
+static pe_status upload_call(pe_ctx c, CallSlot* cs, size_t bytes, cudaStream_t st, cudaStream_t up,
+                             bool capturing) {
+  if (cs->hd && !getenv("PE_UPLOAD_MEMCPY")) {
+    // the SMs read the mapped host buffer: no copy-engine queue on the way
+    const int n = (int)((bytes + 15) / 16);
+    launch(pe_upload_kernel, std::min(cdiv(n, 256), 16), 256, 0, st, reinterpret_cast<const uint4*>(cs->hd),
+           reinterpret_cast<uint4*>(cs->d), n);
+    ++c->uploads;
+    if (!capturing) {
+      PE_CUDA(cudaEventRecord(cs->done, st));
+      cs->armed = true;
+    }
+    return PE_OK;
+  }
   cudaStream_t us = up ? up : st;
   PE_CUDA(cudaMemcpyAsync(cs->d, cs->h, bytes, cudaMemcpyHostToDevice, us));
   if (!capturing) {
@@ -841,6 +859,7 @@ static pe_status upload_call(CallSlot* cs, size_t bytes, cudaStream_t st, cudaSt
 static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
                             int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad, cudaStream_t up) {
   SmallArgs a;                                      // ~2.6 KB of kernel parameters
+  c->uploads = 0;
   const bool inl = count <= kSmallInlineMats && T <= kSmallInlineIters;
   CallSlot* cs = nullptr;
   const size_t mats_bytes = rup((size_t)count * sizeof(SmallMat), 128);
@@ -876,7 +895,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     a.mats = nullptr;
     a.coef = nullptr;
   } else {
-    pe_status s = upload_call(cs, mats_bytes + (size_t)3 * T * sizeof(float), st, up, capturing);
+    pe_status s = upload_call(c, cs, mats_bytes + (size_t)3 * T * sizeof(float), st, up, capturing);
     if (s != PE_OK) return s;
     a.mats = reinterpret_cast<const SmallMat*>(cs->d);
     a.coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + mats_bytes);
@@ -885,7 +904,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     if (dtype == PE_BF16) launch(pe_small_sm100<1>, count, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
     else launch(pe_small_sm100<3>, count, kSmallThreads, small_smem_bytes<3>(max_npad), st, a); }
   PE_CUDA(cudaGetLastError());
-  c->last_launches = 1;
+  c->last_launches = 1 + c->uploads;
   return PE_OK;
 }
 
@@ -990,7 +1009,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     h_coef[3 * t + 1] = (float)tup[1];
     h_coef[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
   }
-  if ((s = upload_call(cs, call_bytes(count, T), st, up, capturing)) != PE_OK) return s;
+  c->uploads = 0;
+  if ((s = upload_call(c, cs, call_bytes(count, T), st, up, capturing)) != PE_OK) return s;
   void** d_ptrs = reinterpret_cast<void**>(cs->d);
   const CUtensorMap* d_imaps =
       reinterpret_cast<const CUtensorMap*>(reinterpret_cast<const uint8_t*>(cs->d) + omap_off);
@@ -1126,7 +1146,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   copy_pass(2, false, true);
   copy_pass(3, false, true);
   PE_CUDA(cudaGetLastError());
-  c->last_launches = launches;
+  c->last_launches = launches + c->uploads;
   return PE_OK;
 }
 
