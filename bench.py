@@ -229,16 +229,22 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
     from paper_2505_16932_b200 import dist as pdist
     idx, owner = pdist.owned(shapes, rank, world) if world > 1 else (list(range(len(shapes))), [0] * len(shapes))
     xs = make_inputs(shapes, idx, device)
-    ys = [torch.empty_like(x) for x in xs]
+    gp = None
+    if dist_on and world > 1:
+        # results land straight in the all-gather send buffer; one NCCL
+        # all_gather_into_tensor per step leaves every result on every rank
+        gp = pdist.GatherPlan(shapes, owner, world, rank, 2, torch.bfloat16, device)
+        assert gp.local_index == idx
+        ys = gp.local_views
+    else:
+        ys = [torch.empty_like(x) for x in xs]
     ctx.reserve([shapes[i] for i in idx])
     stream = torch.cuda.current_stream(device)
 
     def step():
         ctx.polar(xs, ys, iters=T, stream=stream)
-        if dist_on and world > 1:
-            local = {i: y.view(-1).view(torch.uint8) for i, y in zip(idx, ys)}
-            pdist.gather_outputs(local, shapes, owner, world, 2,
-                                 lambda nb: torch.empty(nb, dtype=torch.uint8, device=device))
+        if gp is not None:
+            gp.gather()
 
     for _ in range(warmup):
         step()

@@ -57,3 +57,40 @@ def gather_outputs(local, shapes, owner, world, elem_size, make_buffer, group=No
             out[i] = recv[r][off:off + nb]
             off += nb
     return out
+
+
+class GatherPlan:
+    """Preallocated all-gather of one layer set's results with no packing
+    copy: pe_polar writes this rank's results straight into the send buffer
+    (``local_views``), one ``all_gather_into_tensor`` fills ``recv`` (world x
+    cap bytes), and ``views`` are every matrix's result inside ``recv``.
+    Matrix slots are 256-byte aligned (the library wants 16-byte-aligned
+    buffers).  Built once per layer set; reuse it every step."""
+
+    def __init__(self, shapes, owner, world, rank, elem_size, dtype, device):
+        import torch
+        self.world, self.rank = world, rank
+        per_rank = [[i for i, o in enumerate(owner) if o == r] for r in range(world)]
+        offs, caps = {}, []
+        for r in range(world):
+            off = 0
+            for i in per_rank[r]:
+                offs[i] = (r, off)
+                off += (_nbytes(shapes[i], elem_size) + 255) // 256 * 256
+            caps.append(off)
+        self.cap = max(max(caps), 256)
+        self.recv = torch.zeros(world * self.cap, dtype=torch.uint8, device=device)
+        self.send = torch.zeros(self.cap, dtype=torch.uint8, device=device)
+
+        def view(buf, off, shape):
+            nb = _nbytes(shape, elem_size)
+            return buf[off:off + nb].view(dtype).view(int(shape[0]), int(shape[1]))
+
+        self.local_index = per_rank[rank]
+        self.local_views = [view(self.send, offs[i][1], shapes[i]) for i in self.local_index]
+        self.views = [view(self.recv, offs[i][0] * self.cap + offs[i][1], shapes[i]) for i in range(len(shapes))]
+
+    def gather(self, group=None):
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(self.recv, self.send, group=group)
+        return self.views

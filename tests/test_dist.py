@@ -40,6 +40,15 @@ def _worker(rank, world, port, q):
             exp = (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16)
             got = out[i].view(torch.int16).view(torch.bfloat16)
             ok = ok and torch.equal(got, exp)
+        # zero-copy plan: results written into the send buffer, one all-gather
+        gp = pdist.GatherPlan(shapes, owner, world, rank, 2, torch.bfloat16, "cpu")
+        for i, v in zip(gp.local_index, gp.local_views):
+            r, c = shapes[i]
+            v.copy_((torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16).view(r, c))
+        views = gp.gather()
+        for i, (r, c) in enumerate(shapes):
+            exp = (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16).view(r, c)
+            ok = ok and torch.equal(views[i], exp) and (views[i].data_ptr() - gp.recv.data_ptr()) % 256 == 0
         plans = [None] * world
         dist.all_gather_object(plans, owner)
         q.put((rank, ok, all(p == owner for p in plans), sorted(idx)))
