@@ -196,6 +196,29 @@ pe_status pe_polar_host(pe_ctx ctx, const void* const* in, void* const* out, con
 pe_status pe_muon_step(pe_ctx ctx, void* const* W, void* const* M, const void* const* G,
                        const int64_t* shapes, int count, double beta, double lr, int iters, void* stream);
 
+/*
+ * Intra-matrix sharding: one wide matrix
+ * M = [M_0 | M_1 | ... ] (m x n, column blocks on different ranks) is
+ * orthogonalised jointly; this rank passes its column block M_r (rows = m,
+ * cols = n_r, row-major bf16, cols % 8 == 0, 16-byte aligned) and receives
+ * the same columns of pe_polar(M) in `out` (m x n_r).  Per iteration
+ * A = sum_r M_r M_r^T is formed by an all-reduce of the fp32 partial Grams
+ * (rounded once to bf16 afterwards, reading R8), B = b A + c A^2 is
+ * computed redundantly on every rank and X_r <- a X_r + B X_r stays local
+ * (P:500); ||M||_F^2 is all-reduced first.  rows may exceed cols
+ * here (the Gram side is always `rows`).
+ * allreduce(buf, count, dtype, user, stream): the caller's in-place SUM
+ * all-reduce over all ranks of `count` elements (dtype 0 = fp32, 1 = fp64)
+ * of device buffer `buf`, enqueued on `stream` (e.g. ncclAllReduce); called
+ * 1 + iters times per call, from the calling thread, between kernel
+ * launches; return PE_OK or an error, which aborts the call.
+ * Errors: PE_ERR_INVALID_ARG, PE_ERR_UNSUPPORTED (cols % 8 != 0, capture),
+ * PE_ERR_WORKSPACE, PE_ERR_CUDA, or the callback's status.
+ */
+typedef pe_status (*pe_allreduce_fn)(void* buf, int64_t count, int dtype, void* user, void* stream);
+pe_status pe_polar_sharded(pe_ctx ctx, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+                           pe_allreduce_fn allreduce, void* user, void* stream);
+
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */
 pe_status pe_last_launch_count(pe_ctx ctx, int* launches);

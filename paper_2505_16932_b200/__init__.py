@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = [
     "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
-    "pe_muon_step",
+    "pe_muon_step", "pe_polar_sharded",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -78,6 +78,7 @@ def lib():
         "pe_profile_enable": (I, [P, I]),
         "pe_profile_read": (I, [P, DP, ctypes.POINTER(I), I]),
         "pe_muon_step": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, D, D, I, P]),
+        "pe_polar_sharded": (I, [P, P, P, ctypes.c_int64, ctypes.c_int64, I, ALLREDUCE_FN, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -85,6 +86,19 @@ def lib():
         f.argtypes = args
     _lib = L
     return L
+
+
+# pe_allreduce_fn (include/pe.h): (buf, count, dtype 0 fp32 / 1 fp64, user, stream) -> pe_status
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_void_p)
+
+
+class _DevBuf:
+    """A raw device buffer seen through __cuda_array_interface__ (zero copy)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
 
 
 def _check(status, where):
@@ -234,6 +248,40 @@ class Context:
         _check(lib().pe_muon_step(self._h, W, M, G, shp, n, float(beta), float(lr), int(iters),
                                   ctypes.c_void_p(stream.cuda_stream)), "pe_muon_step")
         return weights
+
+    def polar_sharded(self, shard, allreduce, out=None, iters=5, stream=None):
+        """pe_polar_sharded: `shard` is this rank's column block M_r (rows x
+        cols_r, bf16, cols_r % 8 == 0) of one wide matrix M = [M_0 | M_1 | ...];
+        returns the same columns of polar(M).  `allreduce(t)` must sum the CUDA
+        tensor `t` in place over all ranks, on the current stream (e.g.
+        torch.distributed.all_reduce)."""
+        import torch
+        if shard.dim() != 2 or not shard.is_contiguous() or not shard.is_cuda or shard.dtype != torch.bfloat16:
+            raise ValueError("polar_sharded takes a contiguous 2-D bf16 CUDA tensor")
+        if out is None:
+            out = torch.empty_like(shard)
+        if stream is None:
+            stream = torch.cuda.current_stream(shard.device)
+        errors = []
+
+        def cb(buf, count, dtype, user, st):
+            try:
+                t = torch.as_tensor(_DevBuf(buf, count, "<f4" if dtype == 0 else "<f8"), device=shard.device)
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=shard.device)):
+                    allreduce(t)
+                return 0
+            except Exception as e:          # reported after the call returns
+                errors.append(e)
+                return 5                    # PE_ERR_NCCL
+
+        fn = ALLREDUCE_FN(cb)
+        status = lib().pe_polar_sharded(self._h, ctypes.c_void_p(shard.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                        int(shard.shape[0]), int(shard.shape[1]), int(iters), fn, None,
+                                        ctypes.c_void_p(stream.cuda_stream))
+        if errors:
+            raise errors[0]
+        _check(status, "pe_polar_sharded")
+        return out
 
     def polar_host(self, inputs, outputs, iters=5, stream=None):
         """pe_polar_host on host (pinned) CPU tensors; synchronous."""

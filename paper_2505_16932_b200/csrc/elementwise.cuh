@@ -43,6 +43,7 @@ struct NormArgs {
   // the new M is taken
   const void* const* grads;    // G per matrix, or nullptr (plain pe_polar)
   float beta, omb;             // fp32(beta), fp32(1 - beta)
+  double* sums;                // sharded calls: write the local sum of squares here instead of inv
 };
 
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
@@ -155,8 +156,12 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
     const int first = blk - ci;
     double s = 0.0;
     for (int k = 0; k < a.nchunks[mat]; ++k) s += *(volatile double*)&a.partials[first + k];
-    const double denom = sqrt(s) * 1.01 + 1e-7;
-    a.inv[mat] = (float)(1.0 / denom);
+    if (a.sums != nullptr) {
+      a.sums[mat] = s;                             // all-reduced by the caller, then pe_inv_kernel
+    } else {
+      const double denom = sqrt(s) * 1.01 + 1e-7;
+      a.inv[mat] = (float)(1.0 / denom);
+    }
     a.counters[mat] = 0u;                          // ready for the next call / graph replay
   }
 }
@@ -386,6 +391,24 @@ __global__ void __launch_bounds__(256) pe_planes_kernel(const CopyArgs a) {
       __syncthreads();
     }
   }
+}
+
+// Sharded calls (pe_polar_sharded): inv from the all-reduced sum of squares
+// (P:494), and the all-reduced fp32 Gram rounded once to the bf16 A the poly
+// reads -- scaled by fp32(inv inv) in the first iteration, as the folded
+// Gram epilogue does (reading R8).
+__global__ void pe_inv_kernel(const double* sums, float* inv) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) inv[0] = (float)(1.0 / (sqrt(sums[0]) * 1.01 + 1e-7));
+}
+__global__ void __launch_bounds__(256) pe_round_gram_kernel(const float* a32, __nv_bfloat16* a, int64_t n,
+                                                            const float* inv, int first) {
+  pdl_trigger();
+  pdl_wait();
+  const float sc = first ? __fmul_rn(inv[0], inv[0]) : 1.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = __float2bfloat16_rn(first ? __fmul_rn(a32[i], sc) : a32[i]);
 }
 
 // Per-call upload of a pe_polar call (pointers, caller tensor maps,

@@ -80,6 +80,8 @@ struct GemmArgs {
   const int* mflags;           // per call, per matrix: kFlag*
   const float* inv;            // per matrix fp32(1/s)
   float* scratch;              // kP = 3: 128 x 256 fp32 per CTA (running sum of the K passes)
+  float* const* out32;         // sharded calls: the Gram writes its raw fp32 accumulator here (m x m,
+                               // leading dim ldm, blocks on/above the diagonal), not bf16 A; else nullptr
   int muon;                    // pe_muon_step: the last update's direct output is the weight W,
   float lr;                    // updated to bf16(W - lr * bf16(X'))
   // one phase per launch (nphase == 0): the phase of every tile
@@ -768,6 +770,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           phase_bits ^= 1u << k;
         }
         uint8_t* slot = slots + (kSl == 1 ? 0 : k) * kEpiSlotBytes;
+        if (cfg.mode == kModeGram && args.out32 != nullptr) {
+          // sharded call: the partial Gram leaves in fp32 (16-byte stores of
+          // this thread's row); the all-reduce and the rounding come later
+          float* dst = args.out32[tl.mat] + (size_t)r * md.ldm;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            if (c0 + 32 * h >= ncols) break;
+            float w[32];
+            tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
+            if (r < md.m) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const int col = c0 + 32 * h + 4 * v;
+                if (col + 3 < md.m) {
+                  *reinterpret_cast<float4*>(dst + col) = make_float4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    if (col + e < md.m) dst[col + e] = w[4 * v + e];
+                }
+              }
+            }
+          }
+          continue;
+        }
         if (kSl == 1 && k > 0) {
           // single staging slot (Gram: no epilogue operand): the previous
           // chunk's store must have left smem before this chunk is written

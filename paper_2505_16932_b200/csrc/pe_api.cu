@@ -192,6 +192,11 @@ struct pe_ctx_s {
   int uploads = 0;              // upload-kernel launches of the current call (counted in last_launches)
   int* done = nullptr;          // fused schedule completion counters (cleared by the norm kernel)
   float* scratch = nullptr;     // fp32 path: per-CTA running sums of the K passes (gemm_sm100.cuh)
+  // pe_polar_sharded: fp32 partial Gram (and a device pointer to it), local sum of squares
+  float* sh_a32 = nullptr;
+  size_t sh_cap = 0;
+  float** sh_ptr = nullptr;
+  double* sh_sum = nullptr;
   size_t done_cap = 0;
   int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1/3 are set)
   long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
@@ -349,6 +354,9 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   if (c->stats) cudaFree(c->stats);
   if (c->done) cudaFree(c->done);
   if (c->scratch) cudaFree(c->scratch);
+  if (c->sh_a32) cudaFree(c->sh_a32);
+  if (c->sh_ptr) cudaFree(c->sh_ptr);
+  if (c->sh_sum) cudaFree(c->sh_sum);
   delete c;
   return PE_OK;
 }
@@ -431,8 +439,12 @@ static size_t call_ptr_bytes(int count) { return rup((size_t)5 * count * sizeof(
 static size_t call_coef_off(int count) { return call_ptr_bytes(count) + (size_t)3 * count * sizeof(CUtensorMap); }
 static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size_t)3 * T * sizeof(float); }
 
-static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out) {
+// no_orient: keep rows as the Gram side even when rows > cols (a column
+// shard of a wide matrix, pe_polar_sharded).
+static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
+                            bool no_orient = false) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
+  if (no_orient) key.push_back(-1);
   for (Plan* p : c->plans)
     if (p->dtype == dtype && p->key == key) {
       p->last_use = ++c->use_clock;
@@ -451,7 +463,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     MatDev& md = mats[i];
     md.rows = (int)shapes[2 * i];
     md.cols = (int)shapes[2 * i + 1];
-    md.tall = md.rows > md.cols;                 // P:493, strict (R10)
+    md.tall = !no_orient && md.rows > md.cols;   // P:493, strict (R10)
     md.m = md.tall ? md.cols : md.rows;
     md.n = md.tall ? md.rows : md.cols;
     md.ldx = (int)rup(md.n, 8);
@@ -908,6 +920,12 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
   return PE_OK;
 }
 
+// pe_polar_sharded: the all-reduce hook of one call
+struct ShardCtx {
+  pe_allreduce_fn fn;
+  void* user;
+};
+
 // pe_polar and pe_muon_step.  Muon (grads != nullptr, bf16): `in` are the
 // momentum buffers M, updated in place by the norm kernel to
 // bf16(beta M + (1 - beta) G); `out` are the weights W, updated to
@@ -915,7 +933,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
 // matrices) or the finalize pass (the others).
 static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, const void* const* grads,
                             const int64_t* shapes, int count, int iters, pe_dtype dtype, void* stream_,
-                            double beta, double lr, cudaStream_t up = nullptr) {
+                            double beta, double lr, cudaStream_t up = nullptr, const ShardCtx* sh = nullptr) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   if (count == 0) { c->last_launches = 0; return PE_OK; }
   if (!in || !out) return PE_ERR_INVALID_ARG;
@@ -938,7 +956,11 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   PE_CUDA(cudaStreamIsCapturing(st, &cap_status));
   const bool capturing = cap_status == cudaStreamCaptureStatusActive;
   int max_npad = 0;
-  if (!muon && small_eligible(shapes, count, dtype, &max_npad))
+  if (sh && (count != 1 || dtype != PE_BF16 || muon || capturing || shapes[1] % 8 != 0)) {
+    g_last_error = "pe_polar_sharded: one bf16 shard with cols % 8 == 0, not under graph capture";
+    return PE_ERR_UNSUPPORTED;
+  }
+  if (!muon && !sh && small_eligible(shapes, count, dtype, &max_npad))
     return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad, up);
   Plan* P = nullptr;
   if (capturing) {
@@ -951,7 +973,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       return PE_ERR_WORKSPACE;
     }
     P->last_use = ++c->use_clock;
-  } else if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) {
+  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr)) != PE_OK) {
     return s;
   }
 
@@ -962,7 +984,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   // PE_FUSED=1; measured equal to one launch per phase on the GPT-2 sets and
   // within noise on Llama, profiles/r1_variants.md)
   static const bool fused_on = getenv("PE_FUSED") && strcmp(getenv("PE_FUSED"), "0") != 0;
-  const bool fused = fused_on && dtype == PE_BF16 && !capturing;   // (its setup may synchronise)
+  const bool fused = fused_on && dtype == PE_BF16 && !capturing && !sh;   // (its setup may synchronise)
   const int nq = (c->degree + 1) / 2;
   if (fused) {
     if ((s = ensure_fused(c, P, T)) != PE_OK) return s;
@@ -1038,9 +1060,36 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   na.grads = muon ? d_ptrs + 4 * count : nullptr;
   na.beta = (float)beta;
   na.omb = (float)(1.0 - beta);
+  na.sums = nullptr;
+  if (sh) {
+    // buffers of the sharded call: local sum of squares, fp32 partial Gram
+    const MatDev& md = P->mats[0];
+    const size_t need = (size_t)md.m * md.ldm;
+    if (need > c->sh_cap) {
+      PE_CUDA(cudaDeviceSynchronize());
+      if (c->sh_a32) cudaFree(c->sh_a32);
+      c->sh_a32 = nullptr;
+      c->sh_cap = 0;
+      if (cudaMalloc(&c->sh_a32, need * sizeof(float)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+      c->sh_cap = need;
+      if (!c->sh_sum && cudaMalloc(&c->sh_sum, 64) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+      if (!c->sh_ptr && cudaMalloc(&c->sh_ptr, sizeof(float*)) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }
+      PE_CUDA(cudaMemcpy(c->sh_ptr, &c->sh_a32, sizeof(float*), cudaMemcpyHostToDevice));
+    }
+    na.sums = c->sh_sum;
+  }
   { ProfScope ps(c, 0, st);
     launch(pe_norm_kernel, P->n_chunks, kNormThreads, 0, st, na); }
   ++launches;
+  if (sh) {
+    // ||M||_F^2 over every rank's columns, then inv on the device
+    if ((s = sh->fn(c->sh_sum, 1, 1, sh->user, stream_)) != PE_OK) {
+      g_last_error = "pe_polar_sharded: the all-reduce callback failed";
+      return s;
+    }
+    launch(pe_inv_kernel, 1, 32, 0, st, (const double*)c->sh_sum, at<float>(P, P->o_inv));
+    ++launches;
+  }
 
   // 2) X_0 = M / s (oriented)
   auto copy_pass = [&](int k, bool scale, bool fin) {
@@ -1083,6 +1132,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     g.inv = at<float>(P, P->o_inv);
     g.scratch = c->scratch;
     g.muon = muon ? 1 : 0;
+    g.out32 = nullptr;
     g.lr = (float)lr;
     g.nphase = 0;
     g.coef = d_coef;
@@ -1125,6 +1175,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         g.stats = c->stats + (size_t)mode * 2048;
       }
       const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
+      if (sh && mode == kModeGram) g.out32 = c->sh_ptr;         // partial Gram in fp32
+      {
       ProfScope ps(c, 2 + mode, st);
       const bool edge = (t == 0) || (t == T - 1);
       if (dtype == PE_FP32) {
@@ -1139,6 +1191,21 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
       }
       ++launches;
+      }
+      if (sh && mode == kModeGram) {
+        // A = sum over ranks of the partial Grams (P:498 on the whole
+        // matrix), then rounded once to bf16 (R8; iteration 1 also scales)
+        const MatDev& md = P->mats[0];
+        const int64_t na32 = (int64_t)md.m * md.ldm;
+        if ((s = sh->fn(c->sh_a32, na32, 0, sh->user, stream_)) != PE_OK) {
+          g_last_error = "pe_polar_sharded: the all-reduce callback failed";
+          return s;
+        }
+        launch(pe_round_gram_kernel, std::min<int64_t>(cdiv(na32, 256), c->num_sms * 4), 256, 0, st,
+               (const float*)c->sh_a32, reinterpret_cast<__nv_bfloat16*>(md.A), na32,
+               (const float*)at<float>(P, P->o_inv), t == 0 ? 1 : 0);
+        ++launches;
+      }
     }
   }
 
@@ -1153,6 +1220,16 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
 extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
                               int count, int iters, pe_dtype dtype, void* stream) {
   return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
+}
+
+extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+                                      pe_allreduce_fn allreduce, void* user, void* stream) {
+  if (!c || !in || !out || !allreduce || iters < 1) return PE_ERR_INVALID_ARG;
+  const int64_t shp[2] = {rows, cols};
+  const void* ins[1] = {in};
+  void* outs[1] = {out};
+  ShardCtx sh{allreduce, user};
+  return polar_impl(c, ins, outs, nullptr, shp, 1, iters, PE_BF16, stream, 0.0, 0.0, nullptr, &sh);
 }
 
 extern "C" pe_status pe_muon_step(pe_ctx c, void* const* W, void* const* M, const void* const* G,

@@ -94,3 +94,13 @@ class GatherPlan:
         import torch.distributed as dist
         dist.all_gather_into_tensor(self.recv, self.send, group=group)
         return self.views
+
+
+def polar_sharded(ctx, shard, iters=5, group=None, out=None):
+    """Intra-matrix sharding: this rank's column block
+    of one wide matrix, orthogonalised jointly with the other ranks' blocks;
+    the fp32 partial Grams and the squared norm are summed with
+    torch.distributed.all_reduce (NCCL on GPUs).  Returns this rank's
+    columns of polar(M)."""
+    import torch.distributed as dist
+    return ctx.polar_sharded(shard, lambda t: dist.all_reduce(t, group=group), out=out, iters=iters)

@@ -675,3 +675,66 @@ def test_small_path_bit_identical_to_large_path(tmp_path):
         assert np.array_equal(res["0"][key], res["1"][key]), key
         assert int(res["1"]["launches_" + key][0]) == 1
         assert int(res["0"]["launches_" + key][0]) > 3
+
+
+def _virtual_ranks_sharded(shards, T=5):
+    """Run pe_polar_sharded for every column block in its own host thread
+    (one context and stream each, one GPU); the all-reduce hook is a host
+    barrier plus a device sum (the kernels never wait on each other)."""
+    import threading
+    W = len(shards)
+    bar = threading.Barrier(W)
+    slots = [None] * W
+    outs = [None] * W
+    errs = []
+
+    def run(r):
+        try:
+            ctx = pe.Context(0)
+            st = torch.cuda.Stream()
+
+            def allreduce(t):
+                torch.cuda.current_stream().synchronize()     # this rank's partial is complete
+                slots[r] = t
+                bar.wait()
+                total = sum(s.clone() for s in slots)         # every rank sums the same way
+                torch.cuda.current_stream().synchronize()
+                bar.wait()
+                t.copy_(total)
+                torch.cuda.current_stream().synchronize()
+                bar.wait()
+
+            with torch.cuda.stream(st):
+                outs[r] = ctx.polar_sharded(shards[r], allreduce, iters=T)
+            st.synchronize()
+            ctx.close()
+        except Exception as e:                                # pragma: no cover
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    return outs
+
+
+@pytest.mark.parametrize("shape,W", [((768, 3072), 2), ((512, 4096), 4), ((300, 1600), 2), ((1024, 1024), 2)])
+def test_polar_sharded_virtual_ranks(ctx, shape, W):
+    """NEXT row 2 (intra-matrix sharding): the column blocks of one matrix,
+    orthogonalised jointly by pe_polar_sharded (fp32 partial Grams summed by
+    the all-reduce hook, then rounded once), equal the unsharded result to
+    bf16 accuracy and pass the G1/G3 gates against the oracle on the whole
+    matrix -- also when a block has fewer columns than rows."""
+    m, n = shape
+    M = bf16_values(syn.gaussian(m, n, seed=400 + W, std=0.02))
+    Md = to_dev_bf16(M)
+    cuts = [round(n * k / W / 8) * 8 for k in range(W + 1)]
+    shards = [Md[:, cuts[k]:cuts[k + 1]].contiguous() for k in range(W)]
+    outs = _virtual_ranks_sharded(shards)
+    X = torch.cat(outs, dim=1).float().cpu().numpy().astype(np.float64)
+    full = run(ctx, [M])[0]
+    assert om.rel_frobenius(X, full) <= 1e-2
+    check_g1_g3(X, M)
