@@ -738,3 +738,45 @@ def test_polar_sharded_virtual_ranks(ctx, shape, W):
     full = run(ctx, [M])[0]
     assert om.rel_frobenius(X, full) <= 1e-2
     check_g1_g3(X, M)
+
+
+def test_two_contexts_concurrently_in_threads():
+    """Two contexts driven from two host threads on their own streams at the
+    same time (plans, upload rings and workspaces are per context): every
+    result equals the same call made alone."""
+    import threading
+    batches = [[bf16_values(syn.gaussian(r, c, seed=500 + 10 * b + i, std=0.02))
+                for i, (r, c) in enumerate([(768, 768), (768, 3072), (300, 520), (96, 200)])] for b in range(2)]
+    alone = []
+    c0 = pe.Context(0)
+    for b in range(2):
+        alone.append(run(c0, batches[b]))
+    c0.close()
+    results = [[None] * 6, [None] * 6]
+    errs = []
+
+    def work(b):
+        try:
+            cx = pe.Context(0)
+            st = torch.cuda.Stream()
+            xs = [to_dev_bf16(M) for M in batches[b]]
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                for k in range(6):
+                    ys = cx.polar(xs, iters=5)
+                    results[b][k] = ys
+            st.synchronize()
+            cx.close()
+        except Exception as e:                                # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(b,)) for b in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    for b in range(2):
+        for ys in results[b]:
+            for y, a in zip(ys, alone[b]):
+                assert np.array_equal(y.float().cpu().numpy().astype(np.float64), a)
