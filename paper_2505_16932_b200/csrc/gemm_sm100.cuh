@@ -100,8 +100,8 @@ struct GemmArgs {
   const int* need;             // per (matrix, mode): 2 * kEpiWarps * tiles
   int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
                                // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
-                               // stores, 256 = every result store to the same box (results are
-                               // wrong with any of these)
+                               // stores, 256 = every result store to the same box, 2048 = right
+                               // operand not loaded (results are wrong with any of these)
   long long* stats;            // optional per-CTA wait-cycle counters (8 per CTA) or nullptr
 };
 
@@ -581,7 +581,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         const int kb_hi = bigseg ? (ps + 1) * o.nk / npass : o.nk;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], o.diag ? 2 * kABytes : 2 * kStageBytes);
+          const bool skip_b = o.diag || (args.dbg & 2048);    // dbg 2048: B operand not loaded (timing only)
+          if (leader) mbar_arrive_expect_tx(&full[stage], skip_b ? 2 * kABytes : 2 * kStageBytes);
           if (args.stats != nullptr && leader) st_issue[stage] = clock64();
           const uint32_t bar = full_leader0 + stage * sizeof(uint64_t);
           uint8_t* a_dst = sA + stage * kABytes;
@@ -599,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             tma_load_2d_pair(a_dst, o.A, bar, o.row_a, k0);
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, o.row_a + 64, k0);
           }
-          if (!o.diag) {          // diagonal tiles: the right operand is the left one
+          if (!skip_b) {          // diagonal tiles: the right operand is the left one
             if (o.b_wide && (kb >> 2) < o.pan_b) {
               tma_load_2d_pair(b_dst, o.Bmn, bar, o.col_b, k0 + pb);
               tma_load_2d_pair(b_dst + kBoxBytes, o.Bmn, bar, o.col_b + 64, k0 + pb);
