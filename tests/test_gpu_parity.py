@@ -52,6 +52,14 @@ def run(ctx, mats, T=5, dtype="bf16"):
     return [y.float().cpu().numpy().astype(np.float64) for y in ys]
 
 
+def g1_gate(m):
+    """G1 bound for a Gaussian input with min side m:
+    2e-2 from m = 128; below that the R8 rounding points alone spread wider
+    (CPU emulation with exact fp32 accumulation, 12-20 seeds: max 2.06e-2 at
+    71 x 547, 1.95e-2 at 300 x 64, 2.3e-2 at 37 x 100, 7.8e-2 at 8 x 8)."""
+    return 2e-2 if m >= 128 else (2.5e-2 if m >= 64 else (3e-2 if m >= 16 else 1e-1))
+
+
 def check_g1_g3(X, Mb, T=5, g1=2e-2):
     ref = oi.polar_express(Mb, TABLE, T)
     r = om.rel_frobenius(X, ref)
@@ -85,7 +93,7 @@ def test_gaussian_parity(ctx, shape):
     # 2.3e-2 at 37x100, 7.8e-2 at 8x8), so small m is gated on G3 plus a
     # size-dependent bound
     m = min(shape)
-    check_g1_g3(X, Mb, g1=2e-2 if m >= 64 else (3e-2 if m >= 16 else 1e-1))
+    check_g1_g3(X, Mb, g1=g1_gate(m))
 
 
 @pytest.mark.parametrize("T", [1, 2, 3, 4, 6, 7, 8, 10])
@@ -616,7 +624,7 @@ def test_large_batch_of_small_random_shapes(ctx):
         if m == 1:
             assert om.rel_frobenius(X, ref) <= 5e-2
         else:
-            assert om.rel_frobenius(X, ref) <= (2e-2 if m >= 64 else (3e-2 if m >= 16 else 1e-1))
+            assert om.rel_frobenius(X, ref) <= g1_gate(m)
     for i in (0, 17, 123, 299):
         assert np.array_equal(run(ctx, [mats[i]])[0], outs[i])
 
@@ -780,3 +788,24 @@ def test_two_contexts_concurrently_in_threads():
         for ys in results[b]:
             for y, a in zip(ys, alone[b]):
                 assert np.array_equal(y.float().cpu().numpy().astype(np.float64), a)
+
+
+def test_small_path_large_batch_uploaded_descriptors(ctx):
+    """More matrices than fit in the small path's kernel parameters (48): the
+    descriptors are uploaded instead; every result equals the same matrix
+    computed alone (inline parameters) and passes the size-dependent gates."""
+    rng = np.random.default_rng(9)
+    shapes = [(int(rng.integers(1, 129)), int(rng.integers(1, 700))) for _ in range(60)]
+    shapes = [(r, c) if k % 2 else (c, r) for k, (r, c) in enumerate(shapes)]
+    mats = [bf16_values(syn.gaussian(r, c, seed=600 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    outs = run(ctx, mats)
+    assert ctx.last_launch_count() == 2            # upload kernel + the small-path kernel
+    for i, (X, Mb) in enumerate(zip(outs, mats)):
+        m = min(Mb.shape)
+        ref = oi.polar_express(Mb, TABLE, 5)
+        if m == 1:
+            assert om.rel_frobenius(X, ref) <= 5e-2
+        else:
+            assert om.rel_frobenius(X, ref) <= g1_gate(m)
+        if i % 7 == 0:
+            assert np.array_equal(run(ctx, [Mb])[0], X)
