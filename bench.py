@@ -285,7 +285,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gpt2-small")
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--extra", default="llama3-8b", help="comma list of extra layer sets (N=1 only), or ''")
+    ap.add_argument("--extra", default="gpt2-large,llama3-8b", help="comma list of extra layer sets (N=1 only), or ''")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     _workload_name[0] = args.workload
