@@ -417,6 +417,11 @@ __global__ void __launch_bounds__(256) pe_round_gram_kernel(const float* a32, __
 __global__ void __launch_bounds__(256) pe_upload_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                         int n) {
   pdl_trigger();
+  // Like every kernel of the library, wait for the previous grid before
+  // touching memory: the wait is what chains consecutive calls (a later
+  // call's kernels never overlap an earlier call's, whose buffers -- this
+  // upload slot four calls back, the plan's workspace -- they reuse).
+  pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 

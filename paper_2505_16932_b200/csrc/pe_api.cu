@@ -870,14 +870,37 @@ static pe_status upload_call(pe_ctx c, CallSlot* cs, size_t bytes, cudaStream_t 
 
 static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
                             int T, pe_dtype dtype, cudaStream_t st, bool capturing, int max_npad, cudaStream_t up) {
-  SmallArgs a;                                      // ~2.6 KB of kernel parameters
+  SmallArgs a;                                      // ~3 KB of kernel parameters
   c->uploads = 0;
+  // CTA table: one matrix per CTA while that fits in one wave (one CTA per
+  // SM); beyond, just enough pairs of matrices with min side <= 64 share a
+  // CTA (packed rows 0-63 / 64-127; neighbours in padded width) to get back
+  // to one wave if possible (a pair takes longer than one matrix, but two
+  // waves take longer than a pair: 148 tall 768x64 slices 154 us unpacked /
+  // 220 us packed, 296 of them 316 / 222 us)
+  std::vector<SmallCta> ctas;
+  {
+    std::vector<int> half, whole;
+    for (int i = 0; i < count; ++i) {
+      const int64_t m = std::min(shapes[2 * i], shapes[2 * i + 1]);
+      (m <= 64 && !getenv("PE_SMALL_NOPACK") ? half : whole).push_back(i);
+    }
+    std::stable_sort(half.begin(), half.end(), [&](int x, int y) {
+      return std::max(shapes[2 * x], shapes[2 * x + 1]) < std::max(shapes[2 * y], shapes[2 * y + 1]);
+    });
+    const int npairs = (int)std::min<int64_t>(std::max(0, count - c->num_sms), (int64_t)half.size() / 2);
+    for (int k = 0; k < npairs; ++k) ctas.push_back({half[2 * k], half[2 * k + 1]});
+    for (size_t k = 2 * (size_t)npairs; k < half.size(); ++k) ctas.push_back({half[k], -1});
+    for (int i : whole) ctas.push_back({i, -1});
+  }
+  const int nctas = (int)ctas.size();
   const bool inl = count <= kSmallInlineMats && T <= kSmallInlineIters;
   CallSlot* cs = nullptr;
   const size_t mats_bytes = rup((size_t)count * sizeof(SmallMat), 128);
+  const size_t cta_bytes = rup((size_t)nctas * sizeof(SmallCta), 128);
+  const size_t up_bytes = mats_bytes + cta_bytes + (size_t)3 * T * sizeof(float);
   if (!inl) {
-    pe_status s = upload_slot(c, std::max(call_bytes(count, T), mats_bytes + (size_t)3 * T * sizeof(float)),
-                              capturing, T, &cs);
+    pe_status s = upload_slot(c, std::max(call_bytes(count, T), up_bytes), capturing, T, &cs);
     if (s != PE_OK) return s;
   }
   SmallMat* hm = inl ? a.inl : reinterpret_cast<SmallMat*>(cs->h);
@@ -894,7 +917,10 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     sm.fold = (dtype == PE_BF16) && (sm.cols % 8 == 0) && !getenv("PE_NO_FOLD");   // as build_plan
     sm.pad = 0;
   }
-  float* hc = inl ? a.inl_coef : reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(cs->h) + mats_bytes);
+  SmallCta* hct = inl ? a.inl_cta : reinterpret_cast<SmallCta*>(reinterpret_cast<uint8_t*>(cs->h) + mats_bytes);
+  std::copy(ctas.begin(), ctas.end(), hct);
+  float* hc = inl ? a.inl_coef
+                  : reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(cs->h) + mats_bytes + cta_bytes);
   const int nq = (c->degree + 1) / 2;
   for (int t = 0; t < T; ++t) {
     const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
@@ -905,16 +931,19 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
   a.T = T;
   if (inl) {
     a.mats = nullptr;
+    a.ctas = nullptr;
     a.coef = nullptr;
   } else {
-    pe_status s = upload_call(c, cs, mats_bytes + (size_t)3 * T * sizeof(float), st, up, capturing);
+    pe_status s = upload_call(c, cs, up_bytes, st, up, capturing);
     if (s != PE_OK) return s;
-    a.mats = reinterpret_cast<const SmallMat*>(cs->d);
-    a.coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + mats_bytes);
+    const uint8_t* d = reinterpret_cast<const uint8_t*>(cs->d);
+    a.mats = reinterpret_cast<const SmallMat*>(d);
+    a.ctas = reinterpret_cast<const SmallCta*>(d + mats_bytes);
+    a.coef = reinterpret_cast<const float*>(d + mats_bytes + cta_bytes);
   }
   { ProfScope ps(c, 7, st);
-    if (dtype == PE_BF16) launch(pe_small_sm100<1>, count, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
-    else launch(pe_small_sm100<3>, count, kSmallThreads, small_smem_bytes<3>(max_npad), st, a); }
+    if (dtype == PE_BF16) launch(pe_small_sm100<1>, nctas, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
+    else launch(pe_small_sm100<3>, nctas, kSmallThreads, small_smem_bytes<3>(max_npad), st, a); }
   PE_CUDA(cudaGetLastError());
   c->last_launches = 1 + c->uploads;
   return PE_OK;

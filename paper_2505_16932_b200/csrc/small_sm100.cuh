@@ -54,10 +54,19 @@ struct SmallMat {
 // the call's critical path); larger ones point to an uploaded array.
 constexpr int kSmallInlineMats = 48;
 constexpr int kSmallInlineIters = 16;
+// A CTA runs one matrix, or two with min side <= 64 packed into TMEM lanes /
+// X rows 0-63 and 64-127 (their Grams are the diagonal 64 x 64 blocks of the
+// packed Gram; the off-diagonal blocks of A are never written, so A, B and
+// the update stay block diagonal).
+struct SmallCta {
+  int mat0, mat1;        // mat1 < 0: one matrix
+};
 struct SmallArgs {
   SmallMat inl[kSmallInlineMats];
+  SmallCta inl_cta[kSmallInlineMats];
   float inl_coef[3 * kSmallInlineIters];
-  const SmallMat* mats;  // nullptr: use inl
+  const SmallMat* mats;  // nullptr: use inl / inl_cta
+  const SmallCta* ctas;
   const float* coef;     // per iteration fp32 (a, b, c); nullptr: use inl_coef
   int T;
 };
@@ -180,164 +189,179 @@ template <int kP>
 __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_constant__ SmallArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const SmallMat md = args.mats ? args.mats[blockIdx.x] : args.inl[blockIdx.x];
-  const float* coef = args.coef ? args.coef : args.inl_coef;
-  const int n_pad = md.n_pad;
-  const size_t xplane = (size_t)128 * n_pad * 2;
-  const size_t aplane = (size_t)128 * 128 * 2;
-  uint8_t* X = smem;
-  uint8_t* A = smem + kP * xplane;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(A + kP * aplane);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  __shared__ uint64_t bar_s;
+  __shared__ uint32_t tmem_slot_s;
   __shared__ double red[kSmallThreads / 32];
+  uint64_t* bar = &bar_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m = md.m, n = md.n;
-
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, kSmallTmemCols);
+  if (warp == 0) tmem_alloc(&tmem_slot_s, kSmallTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = tmem_slot_s;
   pdl_trigger();
+  // The descriptors may come from this call's upload kernel: read nothing
+  // from global memory before the previous grid has completed.
   pdl_wait();
+  const SmallCta cta = args.mats ? args.ctas[blockIdx.x] : args.inl_cta[blockIdx.x];
+  const SmallMat* mtab = args.mats ? args.mats : args.inl;
+  const bool packed = cta.mat1 >= 0;
+  SmallMat mk[2];
+  mk[0] = mtab[cta.mat0];
+  mk[1] = packed ? mtab[cta.mat1] : mk[0];
+  const float* coef = args.coef ? args.coef : args.inl_coef;
+  const int n_pad = packed ? max(mk[0].n_pad, mk[1].n_pad) : mk[0].n_pad;
+  const size_t xplane = (size_t)128 * n_pad * 2;
+  const size_t aplane = (size_t)128 * 128 * 2;
+  uint8_t* X = smem;
+  uint8_t* A = smem + kP * xplane;
 
-  // ---- norm (fp64 sum of exact squares, as pe_norm_kernel) and load.  The
-  // caller matrix is streamed row by row with 16-byte vectors when its rows
-  // allow (lanes along the row: coalesced); element (i, j) goes to X(r, c) with
-  // (r, c) = (i, j) (wide) or (j, i) (tall).  Folded bf16 keeps M
-  // (1/s is applied in iteration 1's epilogues), otherwise X_0 = m * inv
-  // (fp32: split into planes); rows >= m and columns >= n stay zero.
+  // ---- norm (fp64 sum of exact squares, as pe_norm_kernel) and load, per
+  // matrix of the CTA (slot s at X rows 64 s ..).  The caller matrix is
+  // streamed row by row with 16-byte vectors when its rows allow (lanes along
+  // the row: coalesced); element (i, j) goes to X(r, c) with (r, c) = (i, j)
+  // (wide) or (j, i) (tall).  Folded bf16 keeps M (1/s is applied in
+  // iteration 1's epilogues), otherwise X_0 = m * inv (fp32: split into
+  // planes); rows >= m and columns >= n stay zero.
   constexpr int V = (kP == 1) ? 8 : 4;                  // elements per 16-byte vector
-  const bool vec = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.in) & 15) == 0);
-  const bool fold = (kP == 1) && md.fold;
   {
     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int u = 0; u < n_pad / 8; ++u) small_store8<kP>(X, xplane, small_unit(tid, u), z);
     for (int u = 0; u < 16; ++u) small_store8<kP>(A, aplane, small_unit(tid, u), z);
   }
-  auto load_vec = [&](int64_t e, float* f) {
-    if (kP == 1) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + e));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 t2 = __bfloat1622float2(h[k]);
-        f[2 * k] = t2.x;
-        f[2 * k + 1] = t2.y;
-      }
-    } else {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.in) + e));
-      f[0] = q.x; f[1] = q.y; f[2] = q.z; f[3] = q.w;
-    }
-  };
-  auto load_one = [&](int64_t e) {
-    return (kP == 1) ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(md.in)[e])
-                     : reinterpret_cast<const float*>(md.in)[e];
-  };
-  auto put = [&](int i, int j, float f) {          // caller element (i, j) into X (after the norm)
-    const int rr = md.tall ? j : i, cc = md.tall ? i : j;
-    const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
-    if (kP == 1) {
-      *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(f);
-    } else {
-      const float p0 = __bfloat162float(__float2bfloat16_rn(f));
-      const float r1 = __fsub_rn(f, p0);
-      const float p1 = __bfloat162float(__float2bfloat16_rn(r1));
-      *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(p0);
-      *reinterpret_cast<__nv_bfloat16*>(X + xplane + off) = __float2bfloat16_rn(p1);
-      *reinterpret_cast<__nv_bfloat16*>(X + 2 * xplane + off) = __float2bfloat16_rn(__fsub_rn(r1, p1));
-    }
-  };
-  // Tall inputs: thread r gathers its X row r = caller column r, four
-  // 16-byte units (32 loads) in flight; a warp's loads of one caller row are
-  // contiguous.  Wide inputs: warp w walks caller rows w, w+4, ...; its lanes
-  // walk along the row (coalesced), V elements per lane per step.
-  const int nunits = n_pad / 8;
-  auto gather = [&](int u0, float (&f)[4][8]) {
-#pragma unroll
-    for (int uu = 0; uu < 4; ++uu)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = 8 * (u0 + uu) + k;
-        f[uu][k] = (tid < m && c < n) ? load_one((int64_t)c * md.cols + tid) : 0.f;
-      }
-  };
-  const int vpr = vec ? md.cols / V : md.cols;
+  float inv_s[2] = {1.f, 1.f};
+  bool fold_s[2] = {false, false};
   __syncthreads();                                  // zeroing done before the scattered writes
-  double acc = 0.0;
-  if (md.tall) {
-    for (int u0 = 0; u0 < nunits; u0 += 4) {
-      float f[4][8];
-      gather(u0, f);
+  for (int sl = 0; sl < (packed ? 2 : 1); ++sl) {
+    const SmallMat& md = mk[sl];
+    const int roff = 64 * sl;
+    const int m = md.m, n = md.n;
+    const bool vec = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.in) & 15) == 0);
+    const bool fold = (kP == 1) && md.fold;
+    auto load_vec = [&](int64_t e, float* f) {
+      if (kP == 1) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + e));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-      for (int uu = 0; uu < 4; ++uu) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc += (kP == 1) ? (double)(f[uu][k] * f[uu][k]) : (double)f[uu][k] * f[uu][k];
-        if (fold && u0 + uu < nunits) small_store8<kP>(X, xplane, small_unit(tid, u0 + uu), f[uu]);
-      }
-    }
-  }
-  for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
-    const int64_t row = (int64_t)i * md.cols;
-    for (int jv = lane; jv < vpr; jv += 32) {
-      if (vec) {
-        float f[V];
-        load_vec(row + (int64_t)jv * V, f);
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc += (kP == 1) ? (double)(f[k] * f[k]) : (double)f[k] * f[k];
-        if (fold) {                                   // (the values are already bf16)
-          if (!md.tall) {                             // 8 columns of one row: one 16-byte unit
-            *reinterpret_cast<uint4*>(X + small_unit(i, jv)) =
-                __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + row + jv * V));
-          } else {
-#pragma unroll
-            for (int k = 0; k < V; ++k) put(i, jv * V + k, f[k]);
-          }
+        for (int k = 0; k < 4; ++k) {
+          const float2 t2 = __bfloat1622float2(h[k]);
+          f[2 * k] = t2.x;
+          f[2 * k + 1] = t2.y;
         }
       } else {
-        const float v = load_one(row + jv);
-        acc += (kP == 1) ? (double)(v * v) : (double)v * v;
-        if (fold) put(i, jv, v);
+        const float4 q = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.in) + e));
+        f[0] = q.x; f[1] = q.y; f[2] = q.z; f[3] = q.w;
+      }
+    };
+    auto load_one = [&](int64_t e) {
+      return (kP == 1) ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(md.in)[e])
+                       : reinterpret_cast<const float*>(md.in)[e];
+    };
+    auto put = [&](int i, int j, float f) {        // caller element (i, j) into X (after the norm)
+      const int rr = roff + (md.tall ? j : i), cc = md.tall ? i : j;
+      const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
+      if (kP == 1) {
+        *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(f);
+      } else {
+        const float p0 = __bfloat162float(__float2bfloat16_rn(f));
+        const float r1 = __fsub_rn(f, p0);
+        const float p1 = __bfloat162float(__float2bfloat16_rn(r1));
+        *reinterpret_cast<__nv_bfloat16*>(X + off) = __float2bfloat16_rn(p0);
+        *reinterpret_cast<__nv_bfloat16*>(X + xplane + off) = __float2bfloat16_rn(p1);
+        *reinterpret_cast<__nv_bfloat16*>(X + 2 * xplane + off) = __float2bfloat16_rn(__fsub_rn(r1, p1));
+      }
+    };
+    // Tall inputs: thread rl gathers X row rl = caller column rl, four
+    // 16-byte units (32 loads) in flight; a warp's loads of one caller row
+    // are contiguous.  Wide inputs: warp w walks caller rows w, w+4, ...; its
+    // lanes walk along the row (coalesced), V elements per lane per step.
+    const int nu = md.n_pad / 8;
+    auto gather = [&](int u0, float (&f)[4][8]) {
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int c = 8 * (u0 + uu) + k;
+          f[uu][k] = (tid < m && c < n) ? load_one((int64_t)c * md.cols + tid) : 0.f;
+        }
+    };
+    const int vpr = vec ? md.cols / V : md.cols;
+    double acc = 0.0;
+    if (md.tall) {
+      for (int u0 = 0; u0 < nu; u0 += 4) {
+        float f[4][8];
+        gather(u0, f);
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc += (kP == 1) ? (double)(f[uu][k] * f[uu][k]) : (double)f[uu][k] * f[uu][k];
+          if (fold && u0 + uu < nu && tid < m) small_store8<kP>(X, xplane, small_unit(roff + tid, u0 + uu), f[uu]);
+        }
       }
     }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) red[warp] = acc;
-  __syncthreads();
-  double ss = 0.0;
-  for (int w = 0; w < kSmallThreads / 32; ++w) ss += red[w];
-  const float inv = (float)(1.0 / (sqrt(ss) * 1.01 + 1e-7));    // P:494, reading R1/R2
-  if (!fold && md.tall) {                           // second (L2-hot) pass: X_0 = m * inv
-    for (int u0 = 0; u0 < nunits; u0 += 4) {
-      float f[4][8];
-      gather(u0, f);
-#pragma unroll
-      for (int uu = 0; uu < 4; ++uu) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) f[uu][k] = __fmul_rn(f[uu][k], inv);
-        if (u0 + uu < nunits) small_store8<kP>(X, xplane, small_unit(tid, u0 + uu), f[uu]);
-      }
-    }
-  } else if (!fold) {
-    for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+    for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
       const int64_t row = (int64_t)i * md.cols;
       for (int jv = lane; jv < vpr; jv += 32) {
         if (vec) {
           float f[V];
           load_vec(row + (int64_t)jv * V, f);
 #pragma unroll
-          for (int k = 0; k < V; ++k) put(i, jv * V + k, __fmul_rn(f[k], inv));
+          for (int k = 0; k < V; ++k) acc += (kP == 1) ? (double)(f[k] * f[k]) : (double)f[k] * f[k];
+          if (fold)                                   // 8 columns of one row: one 16-byte unit
+            *reinterpret_cast<uint4*>(X + small_unit(roff + i, jv)) =
+                __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + row + jv * V));
         } else {
-          put(i, jv, __fmul_rn(load_one(row + jv), inv));
+          const float v = load_one(row + jv);
+          acc += (kP == 1) ? (double)(v * v) : (double)v * v;
+          if (fold) put(i, jv, v);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    double ss = 0.0;
+    for (int w = 0; w < kSmallThreads / 32; ++w) ss += red[w];
+    const float inv = (float)(1.0 / (sqrt(ss) * 1.01 + 1e-7));    // P:494, reading R1/R2
+    __syncthreads();                                // red is reused by the next slot
+    inv_s[sl] = inv;
+    fold_s[sl] = fold;
+    if (!fold && md.tall) {                         // second (L2-hot) pass: X_0 = m * inv
+      for (int u0 = 0; u0 < nu; u0 += 4) {
+        float f[4][8];
+        gather(u0, f);
+#pragma unroll
+        for (int uu = 0; uu < 4; ++uu) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[uu][k] = __fmul_rn(f[uu][k], inv);
+          if (u0 + uu < nu && tid < m) small_store8<kP>(X, xplane, small_unit(roff + tid, u0 + uu), f[uu]);
+        }
+      }
+    } else if (!fold) {
+      for (int i = warp; i < md.rows; i += kSmallThreads / 32) {
+        const int64_t row = (int64_t)i * md.cols;
+        for (int jv = lane; jv < vpr; jv += 32) {
+          if (vec) {
+            float f[V];
+            load_vec(row + (int64_t)jv * V, f);
+#pragma unroll
+            for (int k = 0; k < V; ++k) put(i, jv * V + k, __fmul_rn(f[k], inv));
+          } else {
+            put(i, jv, __fmul_rn(load_one(row + jv), inv));
+          }
         }
       }
     }
   }
+  // this thread's row: its matrix (slot), 1/s and folding
+  const int my = packed ? (tid >> 6) : 0;
+  const float inv = inv_s[my];
+  const bool fold = fold_s[my];
   const int r = tid;
 
   const uint32_t xs = smem_u32(X), as = smem_u32(A);
@@ -377,8 +401,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(w[j], inv2);
       }
+      // packed: only the own diagonal block (columns 64 my ..) is written
+      if (!packed || (g >> 1) == my) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) small_store8<kP>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
+        for (int q = 0; q < 4; ++q) small_store8<kP>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
+      }
     }
     // ---- B = b A + c A A, in place over A
     sync_for_mma();
@@ -427,54 +454,59 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
     }
     (void)last;
   }
-  // ---- write-back in the caller's orientation, flat and coalesced;
-  // fp32 output = (p0 + p1) + p2 of the planes (the large path's join)
-  const bool vout = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.out) & 15) == 0) && !md.tall;
-  auto get = [&](int i, int j) {                   // caller element (i, j) from X
-    const int rr = md.tall ? j : i, cc = md.tall ? i : j;
-    const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
-    float f = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + off));
-    if (kP == 3)
-      f = __fadd_rn(__fadd_rn(f, __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + xplane + off))),
-                    __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + 2 * xplane + off)));
-    return f;
-  };
+  // ---- write-back in the caller's orientation, coalesced; fp32
+  // output = (p0 + p1) + p2 of the planes (the large path's join)
   __syncthreads();                                  // every row of X' is in smem
-  if (md.tall && tid < m) {
-    // thread r scatters its X row r into caller column r (a warp's stores to
-    // one caller row are contiguous)
-    for (int u = 0; u < nunits; ++u) {
-      float f[8];
-      small_load8<kP>(X, xplane, small_unit(tid, u), f);
+  for (int sl = 0; sl < (packed ? 2 : 1); ++sl) {
+    const SmallMat& md = mk[sl];
+    const int roff = 64 * sl;
+    const int m = md.m, n = md.n;
+    const bool vout = (md.cols % V == 0) && ((reinterpret_cast<uintptr_t>(md.out) & 15) == 0) && !md.tall;
+    auto get = [&](int i, int j) {                  // caller element (i, j) from X
+      const int rr = roff + (md.tall ? j : i), cc = md.tall ? i : j;
+      const uint32_t off = small_unit(rr, cc >> 3) + ((cc & 7) << 1);
+      float f = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + off));
+      if (kP == 3)
+        f = __fadd_rn(__fadd_rn(f, __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + xplane + off))),
+                      __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + 2 * xplane + off)));
+      return f;
+    };
+    if (md.tall && tid < m) {
+      // thread r scatters its X row into caller column r (a warp's stores to
+      // one caller row are contiguous)
+      for (int u = 0; u < md.n_pad / 8; ++u) {
+        float f[8];
+        small_load8<kP>(X, xplane, small_unit(roff + tid, u), f);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = 8 * u + k;
-        if (c >= n) break;
-        const size_t e = (size_t)c * md.cols + tid;
-        if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[e] = __float2bfloat16_rn(f[k]);
-        else reinterpret_cast<float*>(md.out)[e] = f[k];
+        for (int k = 0; k < 8; ++k) {
+          const int c = 8 * u + k;
+          if (c >= n) break;
+          const size_t e = (size_t)c * md.cols + tid;
+          if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[e] = __float2bfloat16_rn(f[k]);
+          else reinterpret_cast<float*>(md.out)[e] = f[k];
+        }
       }
     }
-  }
-  const int vpo = vout ? md.cols / V : md.cols;
-  for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
-    const int64_t row = (int64_t)i * md.cols;
-    for (int jv = lane; jv < vpo; jv += 32) {
-      if (vout) {
-        if (kP == 1) {
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(md.out) + row + jv * V) =
-              *reinterpret_cast<const uint4*>(X + small_unit(i, jv));        // wide: one unit
-        } else {
-          float f[V];
+    const int vpo = vout ? md.cols / V : md.cols;
+    for (int i = warp; i < md.rows && !md.tall; i += kSmallThreads / 32) {
+      const int64_t row = (int64_t)i * md.cols;
+      for (int jv = lane; jv < vpo; jv += 32) {
+        if (vout) {
+          if (kP == 1) {
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(md.out) + row + jv * V) =
+                *reinterpret_cast<const uint4*>(X + small_unit(roff + i, jv));      // wide: one unit
+          } else {
+            float f[V];
 #pragma unroll
-          for (int k = 0; k < V; ++k) f[k] = get(i, jv * V + k);
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(md.out) + row + jv * V) =
-              make_float4(f[0], f[1], f[2], f[3]);
+            for (int k = 0; k < V; ++k) f[k] = get(i, jv * V + k);
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(md.out) + row + jv * V) =
+                make_float4(f[0], f[1], f[2], f[3]);
+          }
+        } else {
+          const float f = get(i, jv);
+          if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[row + jv] = __float2bfloat16_rn(f);
+          else reinterpret_cast<float*>(md.out)[row + jv] = f;
         }
-      } else {
-        const float f = get(i, jv);
-        if (kP == 1) reinterpret_cast<__nv_bfloat16*>(md.out)[row + jv] = __float2bfloat16_rn(f);
-        else reinterpret_cast<float*>(md.out)[row + jv] = f;
       }
     }
   }

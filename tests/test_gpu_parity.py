@@ -809,3 +809,29 @@ def test_small_path_large_batch_uploaded_descriptors(ctx):
             assert om.rel_frobenius(X, ref) <= g1_gate(m)
         if i % 7 == 0:
             assert np.array_equal(run(ctx, [Mb])[0], X)
+
+
+def test_back_to_back_async_calls_stress(ctx):
+    """Twelve calls issued back to back with no host synchronisation, cycling
+    through the 4-slot upload ring three times, alternating a small-path
+    batch large enough to upload its descriptors (60 matrices) with a
+    large-path batch: every output equals the synchronous result (each
+    kernel waits for the previous grid before touching memory, so a call
+    never overlaps the previous call's use of a reused slot or workspace)."""
+    rng = np.random.default_rng(21)
+    small = [bf16_values(syn.gaussian(int(rng.integers(8, 129)), int(rng.integers(8, 500)), seed=700 + i, std=0.02))
+             for i in range(60)]
+    big = [bf16_values(syn.gaussian(r, c, seed=800 + i, std=0.02))
+           for i, (r, c) in enumerate([(768, 768), (768, 3072), (3072, 768), (300, 520)])]
+    ref_s, ref_b = run(ctx, small), run(ctx, big)
+    xs_s = [to_dev_bf16(M) for M in small]
+    xs_b = [to_dev_bf16(M) for M in big]
+    torch.cuda.synchronize()
+    outs = []
+    for k in range(12):
+        torch.cuda._sleep(200000)          # keep the GPU busy so the calls really queue up
+        outs.append(ctx.polar(xs_s if k % 2 == 0 else xs_b, iters=5))
+    torch.cuda.synchronize()
+    for k, ys in enumerate(outs):
+        for y, r in zip(ys, ref_s if k % 2 == 0 else ref_b):
+            assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
