@@ -419,6 +419,18 @@ for T in (1, 2, 5):
     torch.cuda.synchronize()
     for i, y in enumerate(ys):
         out[f"T{T}_{i}"] = y.view(torch.int16).cpu().numpy()
+# a Muon step through the same schedule
+ws = [torch.zeros_like(torch.from_numpy(m.view(np.int16).copy()).view(torch.bfloat16)).cuda() for m in mats]
+ms = [torch.from_numpy(m.view(np.int16).copy()).view(torch.bfloat16).cuda() for m in mats]
+gs = [x.clone() * 3 for x in ms]
+ctx.muon_step(ws, ms, gs, beta=0.9, lr=0.1, iters=5)
+torch.cuda.synchronize()
+for i, (w, m_) in enumerate(zip(ws, ms)):
+    out[f"muonW_{i}"] = w.view(torch.int16).cpu().numpy()
+    out[f"muonM_{i}"] = m_.view(torch.int16).cpu().numpy()
+xs = [torch.from_numpy(m.view(np.int16).copy()).view(torch.bfloat16).cuda() for m in mats]
+ctx.polar(xs, iters=5)
+torch.cuda.synchronize()
 np.savez(sys.argv[3], **out)
 print("launches", ctx.last_launch_count())
 """
@@ -429,7 +441,7 @@ def test_fused_schedule_bit_identical(tmp_path):
     cross-CTA dataflow through completion counters) computes exactly the same
     arithmetic as one launch per phase: outputs are bit-identical on a mixed
     batch (folded and unfolded, wide, tall, ragged, several tiles) for T = 1,
-    2, 5, and the fused call is a single GEMM launch."""
+    2, 5 and for a Muon step, and the fused call is a single GEMM launch."""
     import os
     import subprocess
     import sys
