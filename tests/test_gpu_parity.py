@@ -847,3 +847,74 @@ def test_back_to_back_async_calls_stress(ctx):
     for k, ys in enumerate(outs):
         for y, r in zip(ys, ref_s if k % 2 == 0 else ref_b):
             assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
+
+
+def _r8_emulated(M, T):
+    """CPU emulation of the bf16 rounding points (reading R8: bf16 operands,
+    exact products accumulated in fp64 then rounded to fp32, A rounded once,
+    B and X' rounded once from fp32 epilogues, first iteration folded when the
+    library folds it (cols % 8 == 0), else an explicit bf16 X_0) -- the
+    error this reading itself makes, used to scale the fuzz gate."""
+    bf = lambda x: syn.to_bf16_values(np.asarray(x, np.float32)).astype(np.float32)    # noqa: E731
+    mm = lambda a, b: (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)  # noqa: E731
+    fold = M.shape[1] % 8 == 0          # the library folds 1/s into iteration 1 exactly then
+    X = bf(M)
+    tall = X.shape[0] > X.shape[1]
+    if tall:
+        X = X.T.copy()
+    s = np.sqrt(np.sum(X.astype(np.float64) ** 2)) * 1.01 + 1e-7
+    inv = np.float32(1 / s)
+    if not fold:
+        X = bf(X * inv)                  # explicit X_0 = bf16(m inv)
+    for t, (a, b, c) in enumerate(oi.schedule(TABLE, T)):
+        a, b, c = np.float32(a), np.float32(b), np.float32(c)
+        sc = fold and t == 0
+        acc = mm(X, X.T)
+        A = bf(acc * np.float32(inv * inv)) if sc else bf(acc)
+        B = bf(b * A + c * mm(A, A))
+        X = bf((a * X + mm(B, X)) * inv) if sc else bf(a * X + mm(B, X))
+    return (X.T if tall else X).astype(np.float64)
+
+
+@pytest.mark.slow
+def test_random_calls_fuzz(ctx):
+    """Fuzz: 150 random calls (1-6 matrices each, sides drawn around the tile,
+    packing and small-path boundaries 1, 63-65, 127-129, 255-257, 511-513 and
+    uniform up to 1200, both orientations; bf16 or fp32; T = 1..8) against the
+    oracle with the size-dependent gates (fp32: 1e-5)."""
+    rng = np.random.default_rng(2024)
+    edges = [1, 2, 8, 63, 64, 65, 127, 128, 129, 255, 256, 257, 511, 512, 513]
+
+    def side():
+        return int(rng.choice(edges)) if rng.random() < 0.5 else int(rng.integers(1, 1201))
+
+    for call in range(150):
+        f32 = rng.random() < 0.25
+        T = int(rng.integers(1, 9))
+        k = int(rng.integers(1, 7))
+        shapes = []
+        for _ in range(k):
+            r, c = side(), side()
+            if f32 and max(r, c) > 640:           # keep the fp64 oracle quick
+                r, c = min(r, 640), min(c, 640)
+            shapes.append((r, c))
+        mats = [syn.gaussian(r, c, seed=10000 + 100 * call + i, std=0.02) for i, (r, c) in enumerate(shapes)]
+        mats = [M.astype(np.float32).astype(np.float64) if f32 else bf16_values(M) for M in mats]
+        outs = run(ctx, mats, T=T, dtype="f32" if f32 else "bf16")
+        for X, M in zip(outs, mats):
+            assert X.shape == M.shape and np.all(np.isfinite(X)), (call, M.shape)
+            ref = oi.polar_express(M, TABLE, T)
+            err = om.rel_frobenius(X, ref)
+            m = min(M.shape)
+            if f32:
+                # rank one: all of sigma_hat at 1/1.01, where the composite's
+                # slope (up to ~40 for T = 2..4) amplifies the fp32 rounding
+                # of the 1 x 1 Gram: 1e-4 (measured 4.1e-5 at 1 x 513, T = 4)
+                assert err <= (1e-4 if m == 1 else 1e-5), (call, M.shape, T, err)
+            else:
+                # the fixed gates, or 1.5x the reading's own error on this
+                # input (small m, rank one and early iterates sit on steep
+                # parts of the composite)
+                emu = om.rel_frobenius(_r8_emulated(M, T), ref)
+                gate = max(5e-2 if m == 1 else g1_gate(m), 1.5 * emu + 2e-3)
+                assert err <= gate, (call, M.shape, T, err, emu)
