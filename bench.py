@@ -162,7 +162,6 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
 
 def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
     """The fp64 oracle (as it stands) on host cores over a bounded sample."""
-    import numpy as np
     import pe_synth as syn
     from oracle import coeffs as oc, iteration as oi
     table, _ = oc.pe_coeffs(ELL, DEGREE, 8, 1.01)

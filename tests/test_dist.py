@@ -4,7 +4,6 @@ all-gather leaves every rank with every matrix's bytes."""
 import os
 import socket
 
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
