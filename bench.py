@@ -7,7 +7,7 @@ Frobenius norm, scale/orient, T x {Gram, b A + c A^2, a X + B X}, transpose
 back), inputs resident in HBM.  Default workload: BASELINE.json configs[1]
 (GPT-2 Small layer set, 72 matrices, bf16, T=5, degree 5).  With N ranks each
 rank computes its pe_shard_plan share and the results are all-gathered
-(strong scaling of one layer set).
+over NCCL inside libpe (pe_polar_sharded; strong scaling of one layer set).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
                        [--impl ours|reference] [--extra llama3-8b,...]
@@ -228,22 +228,25 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
     from paper_2505_16932_b200 import dist as pdist
     idx, owner = pdist.owned(shapes, rank, world) if world > 1 else (list(range(len(shapes))), [0] * len(shapes))
     xs = make_inputs(shapes, idx, device)
-    gp = None
     if dist_on and world > 1:
-        # results land straight in the all-gather send buffer; one NCCL
-        # all_gather_into_tensor per step leaves every result on every rank
-        gp = pdist.GatherPlan(shapes, owner, world, rank, 2, torch.bfloat16, device)
-        assert gp.local_index == idx
-        ys = gp.local_views
+        # pe_polar_sharded: this rank computes its pe_shard_plan share; libpe
+        # broadcasts every result from its owner into every rank's output
+        # over its own NCCL communicator, bucket by bucket, overlapping compute
+        pdist.attach(ctx)
+        xin = [None] * len(shapes)
+        for i, x in zip(idx, xs):
+            xin[i] = x
+        ys = [torch.empty(s_, dtype=torch.bfloat16, device=device) for s_ in shapes]
     else:
         ys = [torch.empty_like(x) for x in xs]
     ctx.reserve([shapes[i] for i in idx])
     stream = torch.cuda.current_stream(device)
 
     def step():
-        ctx.polar(xs, ys, iters=T, stream=stream)
-        if gp is not None:
-            gp.gather()
+        if dist_on and world > 1:
+            ctx.polar_sharded(xin, ys, iters=T, stream=stream)
+        else:
+            ctx.polar(xs, ys, iters=T, stream=stream)
 
     for _ in range(warmup):
         step()
@@ -349,7 +352,7 @@ def main():
         "config": {"workload": args.workload, "matrices": len(shapes), "T": T, "degree": DEGREE, "ell": ELL,
                    "coeffs": "pe_coeffs(1e-3,5,8,1.01) (Listing 2 table)",
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "parallelism": f"dp{world} (LPT shard + all-gather)" if world > 1 else "single GPU"},
+                   "parallelism": f"dp{world} (pe_polar_sharded: LPT shard + bucketed NCCL broadcasts)" if world > 1 else "single GPU"},
         "tflops": round(tflops, 2), "tflops_unit": "TFLOP/s (algorithmic, symmetric-aware)",
         "frac_of_bf16_peak": round(tflops / peaks[peak_key], 4),
         "peak_used": f"{peaks[peak_key]} TFLOP/s ({src} {'sustained' if peak_key.endswith('sustained') else 'burst'})",

@@ -216,7 +216,7 @@ pe_status pe_muon_step(pe_ctx ctx, void* const* W, void* const* M, const void* c
  * PE_ERR_WORKSPACE, PE_ERR_CUDA, or the callback's status.
  */
 typedef pe_status (*pe_allreduce_fn)(void* buf, int64_t count, int dtype, void* user, void* stream);
-pe_status pe_polar_sharded(pe_ctx ctx, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+pe_status pe_polar_split(pe_ctx ctx, const void* in, void* out, int64_t rows, int64_t cols, int iters,
                            pe_allreduce_fn allreduce, void* user, void* stream);
 
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
@@ -250,6 +250,49 @@ pe_status pe_profile_read(pe_ctx ctx, double* ms, int* counts, int nkinds);
  * Errors: PE_ERR_INVALID_ARG (world < 1, count < 0, NULL).
  */
 pe_status pe_shard_plan(const int64_t* shapes, int count, int world, int* owner);
+
+/*
+ * Bucket boundaries pe_polar_sharded uses: consecutive index ranges of about
+ * equal total cost 3 m^2 n + m^3, identical on every rank.  begin[0..nbuckets]
+ * (caller-owned, nbuckets + 1 ints) receives the first index of each bucket
+ * and `count` at the end (trailing empty buckets repeat `count`).
+ * Errors: PE_ERR_INVALID_ARG.
+ */
+pe_status pe_shard_buckets(const int64_t* shapes, int count, int nbuckets, int* begin);
+
+/*
+ * Data-parallel Muon across GPUs.  Every rank holds
+ * every momentum matrix and needs every polar factor for its weight update
+ * W <- W - lr * polar(M); the matrices are independent (the
+ * iteration runs per parameter).  NCCL is loaded at run time (the copy
+ * already in the process, else $PE_NCCL_LIB, else libnccl.so.2); without it
+ * these calls return PE_ERR_NCCL and everything else still works.
+ *
+ * pe_nccl_unique_id: a fresh ncclUniqueId (128 bytes, caller-owned `id`),
+ *   made on one rank and handed to the others out of band.
+ * pe_attach_comm: collective over the `world` ranks (ncclCommInitRank inside);
+ *   binds a communicator to the context's device and creates a side stream
+ *   for the exchange.  Calling it again replaces the communicator.
+ * pe_comm_info: the attached rank / world (world = 0 when none is attached).
+ * pe_polar_sharded: same arguments and semantics as pe_polar, called by every
+ *   rank with the same shape list.  Rank r computes the matrices
+ *   pe_shard_plan(shapes, count, world) assigns to it, in buckets of
+ *   consecutive matrices (pe_shard_buckets, 4 by default or $PE_SHARD_BUCKETS);
+ *   as soon as bucket b is computed its matrices are broadcast from their
+ *   owners into every rank's out[i] on the side stream (ncclBroadcast, one
+ *   NCCL group per bucket) while bucket b+1 is computed.  When the work
+ *   enqueued on `stream` completes, out[i] holds polar(M_i) on every rank.
+ *   in[i] is read only on the owner of matrix i (it may be NULL elsewhere);
+ *   out[i] must be valid on every rank; in[i] == out[i] is allowed.
+ *   Errors: PE_ERR_INVALID_ARG (no communicator, bad arguments),
+ *   PE_ERR_NCCL (NCCL missing or failed; an earlier asynchronous NCCL error),
+ *   and pe_polar's.
+ */
+pe_status pe_nccl_unique_id(char id[128]);
+pe_status pe_attach_comm(pe_ctx ctx, const char id[128], int rank, int world);
+pe_status pe_comm_info(pe_ctx ctx, int* rank, int* world);
+pe_status pe_polar_sharded(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
+                           int count, int iters, pe_dtype dtype, void* stream);
 
 /* Algorithmic flops of one pe_polar call (symmetric Gram and A^2 counted
  * once): sum_i T [ m(m+1) n + m^2 (m+1) + 2 m^2 n ]; degree-3

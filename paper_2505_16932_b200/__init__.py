@@ -15,7 +15,8 @@ import os
 
 __all__ = [
     "PE_BF16", "PE_FP32", "PE_SAFETY_ALL", "PE_SAFETY_NOT_FINAL", "PE_NO_RECENTER",
-    "PeError", "lib", "pe_coeffs", "pe_coeffs_ex", "pe_shard_plan", "pe_flops",
+    "PeError", "lib", "pe_coeffs", "pe_coeffs_ex", "pe_shard_plan", "pe_shard_buckets", "pe_flops",
+    "pe_nccl_unique_id",
     "Context", "pe_polar", "pe_polar_host", "EXPORTED_SYMBOLS",
 ]
 
@@ -32,7 +33,8 @@ EXPORTED_SYMBOLS = [
     "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
-    "pe_muon_step", "pe_polar_sharded",
+    "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
+    "pe_comm_info", "pe_polar_sharded",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -78,7 +80,12 @@ def lib():
         "pe_profile_enable": (I, [P, I]),
         "pe_profile_read": (I, [P, DP, ctypes.POINTER(I), I]),
         "pe_muon_step": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, D, D, I, P]),
-        "pe_polar_sharded": (I, [P, P, P, ctypes.c_int64, ctypes.c_int64, I, ALLREDUCE_FN, P, P]),
+        "pe_polar_split": (I, [P, P, P, ctypes.c_int64, ctypes.c_int64, I, ALLREDUCE_FN, P, P]),
+        "pe_shard_buckets": (I, [I64P, I, I, ctypes.POINTER(I)]),
+        "pe_nccl_unique_id": (I, [ctypes.c_char_p]),
+        "pe_attach_comm": (I, [P, ctypes.c_char_p, I, I]),
+        "pe_comm_info": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "pe_polar_sharded": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -138,6 +145,22 @@ def pe_shard_plan(shapes, world):
     own = (ctypes.c_int * max(n, 1))()
     _check(lib().pe_shard_plan(_shapes_arr(shapes), n, int(world), own), "pe_shard_plan")
     return list(own[:n])
+
+
+def pe_shard_buckets(shapes, nbuckets):
+    """First matrix index of each of `nbuckets` cost-balanced consecutive
+    buckets, plus len(shapes) at the end (pe_polar_sharded's exchange order)."""
+    n = len(shapes)
+    beg = (ctypes.c_int * (nbuckets + 1))()
+    _check(lib().pe_shard_buckets(_shapes_arr(shapes), n, int(nbuckets), beg), "pe_shard_buckets")
+    return list(beg)
+
+
+def pe_nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (make it on one rank, share it out of band)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().pe_nccl_unique_id(buf), "pe_nccl_unique_id")
+    return buf.raw
 
 
 def pe_flops(shapes, iters, degree=5):
@@ -249,15 +272,15 @@ class Context:
                                   ctypes.c_void_p(stream.cuda_stream)), "pe_muon_step")
         return weights
 
-    def polar_sharded(self, shard, allreduce, out=None, iters=5, stream=None):
-        """pe_polar_sharded: `shard` is this rank's column block M_r (rows x
+    def polar_split(self, shard, allreduce, out=None, iters=5, stream=None):
+        """pe_polar_split: `shard` is this rank's column block M_r (rows x
         cols_r, bf16, cols_r % 8 == 0) of one wide matrix M = [M_0 | M_1 | ...];
         returns the same columns of polar(M).  `allreduce(t)` must sum the CUDA
         tensor `t` in place over all ranks, on the current stream (e.g.
         torch.distributed.all_reduce)."""
         import torch
         if shard.dim() != 2 or not shard.is_contiguous() or not shard.is_cuda or shard.dtype != torch.bfloat16:
-            raise ValueError("polar_sharded takes a contiguous 2-D bf16 CUDA tensor")
+            raise ValueError("polar_split takes a contiguous 2-D bf16 CUDA tensor")
         if out is None:
             out = torch.empty_like(shard)
         if stream is None:
@@ -275,13 +298,53 @@ class Context:
                 return 5                    # PE_ERR_NCCL
 
         fn = ALLREDUCE_FN(cb)
-        status = lib().pe_polar_sharded(self._h, ctypes.c_void_p(shard.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+        status = lib().pe_polar_split(self._h, ctypes.c_void_p(shard.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                         int(shard.shape[0]), int(shard.shape[1]), int(iters), fn, None,
                                         ctypes.c_void_p(stream.cuda_stream))
         if errors:
             raise errors[0]
-        _check(status, "pe_polar_sharded")
+        _check(status, "pe_polar_split")
         return out
+
+    def attach_comm(self, unique_id, rank, world):
+        """pe_attach_comm: collective over `world` ranks (ncclCommInitRank)."""
+        if len(unique_id) != 128:
+            raise ValueError("unique_id must be the 128 bytes pe_nccl_unique_id returned")
+        _check(lib().pe_attach_comm(self._h, ctypes.create_string_buffer(bytes(unique_id), 128), int(rank),
+                                    int(world)), "pe_attach_comm")
+
+    def comm_info(self):
+        r, w = ctypes.c_int(), ctypes.c_int()
+        _check(lib().pe_comm_info(self._h, ctypes.byref(r), ctypes.byref(w)), "pe_comm_info")
+        return r.value, w.value
+
+    def polar_sharded(self, inputs, outputs, iters=5, stream=None):
+        """pe_polar_sharded: every rank passes the whole layer set (same shapes
+        on every rank); this rank computes its pe_shard_plan share and the
+        results are broadcast from their owners into every rank's `outputs`.
+        ``inputs[i]`` may be None on ranks that do not own matrix i."""
+        import torch
+        n = len(outputs)
+        if len(inputs) != n:
+            raise ValueError("polar_sharded takes equally long input / output lists")
+        if n == 0:
+            _check(lib().pe_polar_sharded(self._h, None, None, None, 0, int(iters), PE_BF16, None),
+                   "pe_polar_sharded")
+            return outputs
+        dt = _dtype_code(outputs[0])
+        for x, y in zip(inputs, outputs):
+            if y.dim() != 2 or not y.is_contiguous() or not y.is_cuda or _dtype_code(y) != dt:
+                raise ValueError("polar_sharded takes contiguous 2-D CUDA tensors of one dtype")
+            if x is not None and (x.shape != y.shape or not x.is_contiguous() or _dtype_code(x) != dt):
+                raise ValueError("polar_sharded: input / output shapes or dtypes differ")
+        ins = (ctypes.c_void_p * n)(*[x.data_ptr() if x is not None else 0 for x in inputs])
+        outs = (ctypes.c_void_p * n)(*[y.data_ptr() for y in outputs])
+        shp = _shapes_arr([tuple(y.shape) for y in outputs])
+        if stream is None:
+            stream = torch.cuda.current_stream(outputs[0].device)
+        _check(lib().pe_polar_sharded(self._h, ins, outs, shp, n, int(iters), dt,
+                                      ctypes.c_void_p(stream.cuda_stream)), "pe_polar_sharded")
+        return outputs
 
     def polar_host(self, inputs, outputs, iters=5, stream=None):
         """pe_polar_host on host (pinned) CPU tensors; synchronous."""

@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpe.so")
-SOURCES = ["pe_api.cu", "pe_coeffs.cpp"]
-HEADERS = ["ptx.cuh", "pe_types.h", "gemm_sm100.cuh", "small_sm100.cuh", "elementwise.cuh"]
+SOURCES = ["pe_api.cu", "pe_coeffs.cpp", "pe_dist.cpp"]
+HEADERS = ["ptx.cuh", "pe_types.h", "gemm_sm100.cuh", "small_sm100.cuh", "elementwise.cuh", "pe_internal.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -37,7 +37,7 @@ def build(force=False, verbose=False):
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl", "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) pe_planes_kernel(const CopyArgs a) {
   }
 }
 
-// Sharded calls (pe_polar_sharded): inv from the all-reduced sum of squares
+// Sharded calls (pe_polar_split): inv from the all-reduced sum of squares
 // (P:494), and the all-reduced fp32 Gram rounded once to the bf16 A the poly
 // reads -- scaled by fp32(inv inv) in the first iteration, as the folded
 // Gram epilogue does (reading R8).

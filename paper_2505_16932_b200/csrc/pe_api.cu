@@ -36,6 +36,7 @@
 #include "gemm_sm100.cuh"
 #include "small_sm100.cuh"
 #include "pe.h"
+#include "pe_internal.h"
 #include "pe_types.h"
 
 using namespace pe;
@@ -192,7 +193,7 @@ struct pe_ctx_s {
   int uploads = 0;              // upload-kernel launches of the current call (counted in last_launches)
   int* done = nullptr;          // fused schedule completion counters (cleared by the norm kernel)
   float* scratch = nullptr;     // fp32 path: per-CTA running sums of the K passes (gemm_sm100.cuh)
-  // pe_polar_sharded: fp32 partial Gram (and a device pointer to it), local sum of squares
+  // pe_polar_split: fp32 partial Gram (and a device pointer to it), local sum of squares
   float* sh_a32 = nullptr;
   size_t sh_cap = 0;
   float** sh_ptr = nullptr;
@@ -207,7 +208,14 @@ struct pe_ctx_s {
   size_t ev_used = 0;
   struct Pending { int kind; cudaEvent_t a, b; };
   std::vector<Pending> pending;
+
+  PeDist* dist = nullptr;       // pe_attach_comm (pe_dist.cpp)
 };
+
+PeDist*& pe_ctx_dist(pe_ctx c) { return c->dist; }
+int pe_ctx_device(pe_ctx c) { return c->device; }
+void pe_ctx_set_launches(pe_ctx c, int n) { c->last_launches = n; }
+void pe_set_error(const char* msg) { g_last_error = msg; }
 
 static void free_plan(Plan* p) {
   if (p->meta) cudaFree(p->meta);
@@ -357,6 +365,7 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   if (c->sh_a32) cudaFree(c->sh_a32);
   if (c->sh_ptr) cudaFree(c->sh_ptr);
   if (c->sh_sum) cudaFree(c->sh_sum);
+  if (c->dist) pe_dist_free(c->dist);
   delete c;
   return PE_OK;
 }
@@ -440,7 +449,7 @@ static size_t call_coef_off(int count) { return call_ptr_bytes(count) + (size_t)
 static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size_t)3 * T * sizeof(float); }
 
 // no_orient: keep rows as the Gram side even when rows > cols (a column
-// shard of a wide matrix, pe_polar_sharded).
+// shard of a wide matrix, pe_polar_split).
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
                             bool no_orient = false) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
@@ -949,8 +958,8 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
   return PE_OK;
 }
 
-// pe_polar_sharded: the all-reduce hook of one call
-struct ShardCtx {
+// pe_polar_split: the all-reduce hook of one call
+struct SplitCtx {
   pe_allreduce_fn fn;
   void* user;
 };
@@ -962,7 +971,7 @@ struct ShardCtx {
 // matrices) or the finalize pass (the others).
 static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, const void* const* grads,
                             const int64_t* shapes, int count, int iters, pe_dtype dtype, void* stream_,
-                            double beta, double lr, cudaStream_t up = nullptr, const ShardCtx* sh = nullptr) {
+                            double beta, double lr, cudaStream_t up = nullptr, const SplitCtx* sh = nullptr) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   if (count == 0) { c->last_launches = 0; return PE_OK; }
   if (!in || !out) return PE_ERR_INVALID_ARG;
@@ -986,7 +995,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   const bool capturing = cap_status == cudaStreamCaptureStatusActive;
   int max_npad = 0;
   if (sh && (count != 1 || dtype != PE_BF16 || muon || capturing || shapes[1] % 8 != 0)) {
-    g_last_error = "pe_polar_sharded: one bf16 shard with cols % 8 == 0, not under graph capture";
+    g_last_error = "pe_polar_split: one bf16 shard with cols % 8 == 0, not under graph capture";
     return PE_ERR_UNSUPPORTED;
   }
   if (!muon && !sh && small_eligible(shapes, count, dtype, &max_npad))
@@ -1113,7 +1122,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   if (sh) {
     // ||M||_F^2 over every rank's columns, then inv on the device
     if ((s = sh->fn(c->sh_sum, 1, 1, sh->user, stream_)) != PE_OK) {
-      g_last_error = "pe_polar_sharded: the all-reduce callback failed";
+      g_last_error = "pe_polar_split: the all-reduce callback failed";
       return s;
     }
     launch(pe_inv_kernel, 1, 32, 0, st, (const double*)c->sh_sum, at<float>(P, P->o_inv));
@@ -1227,7 +1236,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         const MatDev& md = P->mats[0];
         const int64_t na32 = (int64_t)md.m * md.ldm;
         if ((s = sh->fn(c->sh_a32, na32, 0, sh->user, stream_)) != PE_OK) {
-          g_last_error = "pe_polar_sharded: the all-reduce callback failed";
+          g_last_error = "pe_polar_split: the all-reduce callback failed";
           return s;
         }
         launch(pe_round_gram_kernel, std::min<int64_t>(cdiv(na32, 256), c->num_sms * 4), 256, 0, st,
@@ -1251,13 +1260,13 @@ extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out,
   return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
 }
 
-extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+extern "C" pe_status pe_polar_split(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,
                                       pe_allreduce_fn allreduce, void* user, void* stream) {
   if (!c || !in || !out || !allreduce || iters < 1) return PE_ERR_INVALID_ARG;
   const int64_t shp[2] = {rows, cols};
   const void* ins[1] = {in};
   void* outs[1] = {out};
-  ShardCtx sh{allreduce, user};
+  SplitCtx sh{allreduce, user};
   return polar_impl(c, ins, outs, nullptr, shp, 1, iters, PE_BF16, stream, 0.0, 0.0, nullptr, &sh);
 }
 

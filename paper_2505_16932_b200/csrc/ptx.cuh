@@ -163,8 +163,15 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Arrive on a barrier of another CTA of the cluster with the default (.cta)
+// scope.  Used only to hand an accumulator back to the MMA issuer: the
+// TMEM reads it orders are covered by tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync, no generic-proxy data is published.
+// (.release.cluster lowers to MEMBAR.ALL.GPU + ERRBAR, which waits for the
+// warp's outstanding memory traffic: ~13 % of the epilogue warps' stall
+// samples in the GPT-2 S update, profiles/r1_ncu_membar.md.)
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-CTA TMA load: data lands in this CTA's smem, bytes are counted on the
 // barrier at `bar_cluster_addr` (the leader CTA's barrier).

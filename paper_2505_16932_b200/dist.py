@@ -12,7 +12,7 @@ tests).
 """
 from __future__ import annotations
 
-from . import pe_shard_plan
+from . import pe_nccl_unique_id, pe_shard_plan
 
 
 def owned(shapes, rank, world):
@@ -96,11 +96,32 @@ class GatherPlan:
         return self.views
 
 
-def polar_sharded(ctx, shard, iters=5, group=None, out=None):
+def attach(ctx, group=None):
+    """pe_attach_comm over the ranks of a torch.distributed group: rank 0 makes
+    the ncclUniqueId (pe_nccl_unique_id), torch.distributed hands it to the
+    others (plumbing only), and every rank binds a libpe NCCL communicator to
+    its context.  Returns (rank, world)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [pe_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ctx.attach_comm(box[0], rank, world)
+    return rank, world
+
+
+def polar_sharded(ctx, inputs, outputs, iters=5, stream=None):
+    """pe_polar_sharded: the layer set is split over the
+    ranks by pe_shard_plan, each rank computes its share and libpe broadcasts
+    every result from its owner into every rank's ``outputs`` over NCCL,
+    bucket by bucket, overlapping the remaining compute.  Needs ``attach``."""
+    return ctx.polar_sharded(inputs, outputs, iters=iters, stream=stream)
+
+
+def polar_split(ctx, shard, iters=5, group=None, out=None):
     """Intra-matrix sharding: this rank's column block
     of one wide matrix, orthogonalised jointly with the other ranks' blocks;
     the fp32 partial Grams and the squared norm are summed with
     torch.distributed.all_reduce (NCCL on GPUs).  Returns this rank's
     columns of polar(M)."""
     import torch.distributed as dist
-    return ctx.polar_sharded(shard, lambda t: dist.all_reduce(t, group=group), out=out, iters=iters)
+    return ctx.polar_split(shard, lambda t: dist.all_reduce(t, group=group), out=out, iters=iters)

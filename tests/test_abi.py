@@ -142,3 +142,39 @@ def test_create_without_gpu_fails_cleanly():
     assert st in (1, 2, 4)
     with pytest.raises(pe.PeError):
         pe.Context(0)
+
+
+def test_shard_buckets_cover_the_set_in_order_with_balanced_cost():
+    """pe_shard_buckets (pe_polar_sharded's exchange order): consecutive,
+    non-decreasing boundaries from 0 to count; for many equal matrices every
+    bucket holds about 1/B of the cost."""
+    import pe_synth as syn
+    for name in ["gpt2-small", "gpt2-large", "llama3-8b"]:
+        shapes = syn.layer_set_shapes(name)
+        cost = [3 * min(s) ** 2 * max(s) + min(s) ** 3 for s in shapes]
+        for B in (1, 2, 4, 8):
+            beg = pe.pe_shard_buckets(shapes, B)
+            assert beg[0] == 0 and beg[-1] == len(shapes) and len(beg) == B + 1
+            assert all(a <= b for a, b in zip(beg, beg[1:]))
+            share = [sum(cost[beg[b]:beg[b + 1]]) / sum(cost) for b in range(B)]
+            assert max(share) <= 1.0 / B + max(cost) / sum(cost) + 1e-12, (name, B, share)
+    assert pe.pe_shard_buckets([(3, 4)], 4) == [0, 1, 1, 1, 1]
+    assert pe.pe_shard_buckets([], 2) == [0, 0, 0]
+    with pytest.raises(pe.PeError):
+        pe.pe_shard_buckets([(0, 4)], 2)
+
+
+def test_nccl_entry_points_validate_without_a_gpu():
+    """pe_nccl_unique_id needs no device (NCCL bootstrap only); the collective
+    calls reject a NULL context synchronously."""
+    L = pe.lib()
+    try:
+        uid = pe.pe_nccl_unique_id()
+        assert len(uid) == 128 and any(uid)
+        assert pe.pe_nccl_unique_id() != uid
+    except pe.PeError as e:                      # no libnccl on this host
+        assert e.status == 5
+    assert L.pe_attach_comm(None, b"\0" * 128, 0, 1) == 1
+    assert L.pe_polar_sharded(None, None, None, None, 0, 5, 0, None) == 1
+    r, w = ctypes.c_int(), ctypes.c_int()
+    assert L.pe_comm_info(None, ctypes.byref(r), ctypes.byref(w)) == 1

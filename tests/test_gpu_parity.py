@@ -698,7 +698,7 @@ def test_small_path_bit_identical_to_large_path(tmp_path):
 
 
 def _virtual_ranks_sharded(shards, T=5):
-    """Run pe_polar_sharded for every column block in its own host thread
+    """Run pe_polar_split for every column block in its own host thread
     (one context and stream each, one GPU); the all-reduce hook is a host
     barrier plus a device sum (the kernels never wait on each other)."""
     import threading
@@ -725,7 +725,7 @@ def _virtual_ranks_sharded(shards, T=5):
                 bar.wait()
 
             with torch.cuda.stream(st):
-                outs[r] = ctx.polar_sharded(shards[r], allreduce, iters=T)
+                outs[r] = ctx.polar_split(shards[r], allreduce, iters=T)
             st.synchronize()
             ctx.close()
         except Exception as e:                                # pragma: no cover
@@ -742,9 +742,9 @@ def _virtual_ranks_sharded(shards, T=5):
 
 
 @pytest.mark.parametrize("shape,W", [((768, 3072), 2), ((512, 4096), 4), ((300, 1600), 2), ((1024, 1024), 2)])
-def test_polar_sharded_virtual_ranks(ctx, shape, W):
+def test_polar_split_virtual_ranks(ctx, shape, W):
     """NEXT row 2 (intra-matrix sharding): the column blocks of one matrix,
-    orthogonalised jointly by pe_polar_sharded (fp32 partial Grams summed by
+    orthogonalised jointly by pe_polar_split (fp32 partial Grams summed by
     the all-reduce hook, then rounded once), equal the unsharded result to
     bf16 accuracy and pass the G1/G3 gates against the oracle on the whole
     matrix -- also when a block has fewer columns than rows."""
@@ -918,3 +918,33 @@ def test_random_calls_fuzz(ctx):
                 emu = om.rel_frobenius(_r8_emulated(M, T), ref)
                 gate = max(5e-2 if m == 1 else g1_gate(m), 1.5 * emu + 2e-3)
                 assert err <= gate, (call, M.shape, T, err, emu)
+
+
+def test_polar_sharded_single_rank_communicator():
+    """pe_polar_sharded over a 1-rank libpe NCCL communicator (the only
+    world size one GPU allows): the owned subset is the whole set, so the
+    result equals pe_polar bit for bit, with several buckets (one pe_polar per
+    bucket) and in place; without a communicator the call is refused."""
+    import os
+    shapes = [(768, 768), (768, 3072), (3072, 768), (300, 520), (96, 200), (1024, 256)]
+    mats = [bf16_values(syn.gaussian(r, c, seed=700 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    c = pe.Context(0)
+    xs = [to_dev_bf16(M) for M in mats]
+    with pytest.raises(pe.PeError):
+        c.polar_sharded(xs, [torch.empty_like(x) for x in xs])
+    ref = c.polar(xs, iters=5)
+    c.attach_comm(pe.pe_nccl_unique_id(), 0, 1)
+    assert c.comm_info() == (0, 1)
+    for nb in ("1", "3"):
+        os.environ["PE_SHARD_BUCKETS"] = nb
+        try:
+            ys = c.polar_sharded(xs, [torch.empty_like(x) for x in xs], iters=5)
+            inplace = [x.clone() for x in xs]
+            c.polar_sharded(inplace, inplace, iters=5)
+        finally:
+            del os.environ["PE_SHARD_BUCKETS"]
+        torch.cuda.synchronize()
+        for y, z, r in zip(ys, inplace, ref):
+            assert torch.equal(y.view(torch.int16), r.view(torch.int16))
+            assert torch.equal(z.view(torch.int16), r.view(torch.int16))
+    c.close()
