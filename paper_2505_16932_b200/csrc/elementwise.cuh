@@ -21,10 +21,17 @@
 namespace pe {
 
 #ifndef PE_NORM_CHUNK
-#define PE_NORM_CHUNK 65536
+#define PE_NORM_CHUNK 98304
+#endif
+#ifndef PE_NORM_PERSIST
+#define PE_NORM_PERSIST 0
 #endif
 constexpr int kNormChunk = PE_NORM_CHUNK;   // elements per norm block
 constexpr int kNormThreads = 256;
+#ifndef PE_NORM_UNROLL
+#define PE_NORM_UNROLL 8
+#endif
+constexpr int kNormUnroll = PE_NORM_UNROLL;
 
 struct NormArgs {
   const void* const* srcs;     // per matrix, caller layout (rows x cols contiguous)
@@ -44,6 +51,7 @@ struct NormArgs {
   const void* const* grads;    // G per matrix, or nullptr (plain pe_polar)
   float beta, omb;             // fp32(beta), fp32(1 - beta)
   double* sums;                // sharded calls: write the local sum of squares here instead of inv
+  int nblk;                    // chunks in total (the grid is persistent: block b takes chunks b, b + grid, ...)
 };
 
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
@@ -57,11 +65,9 @@ __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
   return acc;
 }
 
-__global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  for (int i = blockIdx.x * kNormThreads + threadIdx.x; i < a.nzero; i += gridDim.x * kNormThreads) a.zero[i] = 0;
-  const int blk = blockIdx.x;
+// One chunk of one matrix: partial sum of squares, and the matrix's s when
+// this is its last chunk to finish.
+__device__ __forceinline__ void norm_chunk(const NormArgs& a, const int blk) {
   const int mat = a.chunk_mat[blk];
   const int ci = a.chunk_idx[blk];
   const int64_t total = a.elems[mat];
@@ -118,13 +124,13 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
     int64_t i = begin + (int64_t)threadIdx.x * 8;
     constexpr int64_t kStride = (int64_t)kNormThreads * 8;
     if (al) {
-      // four independent 16-byte loads in flight per thread
-      for (; i + 3 * kStride + 8 <= end; i += 4 * kStride) {
-        uint4 u0 = __ldg(reinterpret_cast<const uint4*>(p + i));
-        uint4 u1 = __ldg(reinterpret_cast<const uint4*>(p + i + kStride));
-        uint4 u2 = __ldg(reinterpret_cast<const uint4*>(p + i + 2 * kStride));
-        uint4 u3 = __ldg(reinterpret_cast<const uint4*>(p + i + 3 * kStride));
-        acc += sumsq8_bf16(u0) + sumsq8_bf16(u1) + sumsq8_bf16(u2) + sumsq8_bf16(u3);
+      // kNormUnroll independent 16-byte loads in flight per thread
+      for (; i + (kNormUnroll - 1) * kStride + 8 <= end; i += kNormUnroll * kStride) {
+        uint4 u[kNormUnroll];
+#pragma unroll
+        for (int q = 0; q < kNormUnroll; ++q) u[q] = __ldg(reinterpret_cast<const uint4*>(p + i + q * kStride));
+#pragma unroll
+        for (int q = 0; q < kNormUnroll; ++q) acc += sumsq8_bf16(u[q]);
       }
       for (; i + 8 <= end; i += kStride) acc += sumsq8_bf16(__ldg(reinterpret_cast<const uint4*>(p + i)));
     }
@@ -164,6 +170,20 @@ __global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a)
     }
     a.counters[mat] = 0u;                          // ready for the next call / graph replay
   }
+  __syncthreads();                                 // red / last are reused by the next chunk
+}
+
+// One block per chunk (PE_NORM_PERSIST=1: one wave of blocks walking the
+// chunks round-robin -- measured slower, 66 vs 49 us on GPT-2 S, because a
+// block's loads stop at every chunk's reduction).  Chunks of 96 Ki elements
+// with 8 loads in flight per thread: 42.9 us for the GPT-2 S set (65536 / 4
+// loads: 53 us; ncu of that one: SMs active 67 % of the elapsed cycles, a
+// 1.46-wave tail); profiles/r1_norm.md.
+__global__ void __launch_bounds__(kNormThreads) pe_norm_kernel(const NormArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * kNormThreads + threadIdx.x; i < a.nzero; i += gridDim.x * kNormThreads) a.zero[i] = 0;
+  for (int blk = blockIdx.x; blk < a.nblk; blk += gridDim.x) norm_chunk(a, blk);
 }
 
 // Per-matrix parameters of a copy pass (row copy or tile transpose).

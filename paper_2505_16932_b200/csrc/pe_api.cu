@@ -165,6 +165,7 @@ constexpr int kCallSlots = 4;
 struct pe_ctx_s {
   int device = 0;
   int num_sms = 148;
+  int norm_blocks = 148;         // resident blocks of the persistent norm kernel (one wave)
   std::vector<double> table;   // ntab * nq
   int degree = 5;
   int ntab = 0;
@@ -329,6 +330,12 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
   pe_ctx c = new pe_ctx_s();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  {
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pe_norm_kernel, kNormThreads, 0) != cudaSuccess)
+      per_sm = 1;
+    c->norm_blocks = c->num_sms * std::max(1, per_sm);
+  }
   if (const char* d = getenv("PE_DEBUG_GEMM")) c->dbg = atoi(d);
   c->table.resize(8 * 3);
   pe_status s = pe_coeffs(1e-3, 5, 8, 1.01, c->table.data());   // Listing 2 table
@@ -1099,6 +1106,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   na.beta = (float)beta;
   na.omb = (float)(1.0 - beta);
   na.sums = nullptr;
+  na.nblk = P->n_chunks;
   if (sh) {
     // buffers of the sharded call: local sum of squares, fp32 partial Gram
     const MatDev& md = P->mats[0];
@@ -1117,7 +1125,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     na.sums = c->sh_sum;
   }
   { ProfScope ps(c, 0, st);
-    launch(pe_norm_kernel, P->n_chunks, kNormThreads, 0, st, na); }
+    launch(pe_norm_kernel, PE_NORM_PERSIST ? std::min(P->n_chunks, c->norm_blocks) : P->n_chunks, kNormThreads, 0,
+           st, na); }
   ++launches;
   if (sh) {
     // ||M||_F^2 over every rank's columns, then inv on the device
