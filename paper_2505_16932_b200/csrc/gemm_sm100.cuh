@@ -35,9 +35,9 @@
 //               = two 256-column fp32 accumulators -> the epilogue of tile i
 //               overlaps the main loop of tile i+1)
 //   warps 2..9  epilogue: lane quadrant (warp % 4) x column half
-//               ((warp-2) / 4), 32-row x 64-column chunks staged in smem
-//               (128B swizzle): operand chunks arrive by TMA, bf16 results
-//               leave by TMA store.
+//               ((warp-2) / 4), 32-row x 64-column chunks staged in a 4 KB
+//               smem slot (128B swizzle): operand chunks arrive by TMA, bf16
+//               results leave by TMA store.
 // Grouped scheduling: one launch covers every tile of every matrix of the
 // batch; cluster c walks tiles c, c + #clusters, ... of a host-built list.
 //
@@ -501,9 +501,10 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
 }
 
 // kSt: smem pipeline stages; kSl: 4 KB epilogue slots per warp (2 = one per
-// chunk, whole-tile operand prefetch; 1 = a single staging slot, for the Gram
-// which has no epilogue operand and takes a deeper ring; 3 = the three plane
-// slots of the fp32 instantiation); kEdge: first/last-iteration
+// chunk, whole-tile operand prefetch; 1 = a single staging slot: the Gram has
+// no epilogue operand, poly/update load chunk 1's operand once chunk 0's
+// result has left the slot -- the freed 32 KB buy a sixth ring stage; 3 = the
+// three plane slots of the fp32 instantiation); kEdge: first/last-iteration
 // specialisation; kP: planes per buffer (1 = bf16, 3 = fp32, see top).
 template <int kSt, int kSl, bool kEdge, int kP = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_gemm_sm100(const GemmArgs args) {
@@ -722,7 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     auto issue_tile = [&](const Tile& tl2, const TileCfg& c2, int nc) {
       if (c2.dep != nullptr) acquire_counter(c2.dep, c2.dep_need);   // fused: the operand is complete
       const int r0 = tl2.tm * kBM + row_off;
-      for (int kk = 0; kk < kEpiChunks && col0(tl2, kk) < nc; ++kk) {
+      for (int kk = 0; kk < (kSl == 1 ? 1 : kEpiChunks) && col0(tl2, kk) < nc; ++kk) {
         const int c0 = col0(tl2, kk);
         mbar_arrive_expect_tx(&xbar[kk], kEpiSlotBytes);
         if (!(kEdge && c2.ein_tr)) tma_load_2d(slots + kk * kEpiSlotBytes, c2.ein, &xbar[kk], c0, r0);
@@ -766,11 +767,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       for (int k = 0; k < kEpiChunks; ++k) {
         const int c0 = col0(tl, k);
         if (c0 >= ncols || !do_work) break;                  // warp-uniform
-        if (need_load) {
-          mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
-          phase_bits ^= 1u << k;
-        }
+        const int xb = (kSl == 1) ? 0 : k;                   // operand barrier / phase bit of this chunk
         uint8_t* slot = slots + (kSl == 1 ? 0 : k) * kEpiSlotBytes;
+        if (kSl == 1 && need_load && k > 0) {
+          // one slot: this chunk's operand is loaded once the previous chunk's
+          // result has left the slot
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            mbar_arrive_expect_tx(&xbar[0], kEpiSlotBytes);
+            if (!(kEdge && cfg.ein_tr)) tma_load_2d(slot, cfg.ein, &xbar[0], c0, r0);
+            else tma_load_2d(slot, cfg.ein, &xbar[0], r0, c0);
+          }
+          __syncwarp();
+        }
+        if (need_load) {
+          mbar_wait(&xbar[xb], (phase_bits >> xb) & 1u);
+          phase_bits ^= 1u << xb;
+        }
         if (cfg.mode == kModeGram && args.out32 != nullptr) {
           // sharded call: the partial Gram leaves in fp32 (16-byte stores of
           // this thread's row); the all-reduce and the rounding come later
@@ -796,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           }
           continue;
         }
-        if (kSl == 1 && k > 0) {
+        if (kSl == 1 && k > 0 && !need_load) {
           // single staging slot (Gram: no epilogue operand): the previous
           // chunk's store must have left smem before this chunk is written
           if (lane == 0) bulk_wait_read<0>();
@@ -814,13 +827,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             // bring the weight chunk into the slot (same map and box as the store)
             if (lane == 0) {
               fence_async_smem();
-              mbar_arrive_expect_tx(&xbar[k], kEpiSlotBytes);
-              if (!cfg.eout_tr) tma_load_2d(slot, cfg.eout, &xbar[k], c0, r0);
-              else tma_load_2d(slot, cfg.eout, &xbar[k], r0, c0);
+              mbar_arrive_expect_tx(&xbar[xb], kEpiSlotBytes);
+              if (!cfg.eout_tr) tma_load_2d(slot, cfg.eout, &xbar[xb], c0, r0);
+              else tma_load_2d(slot, cfg.eout, &xbar[xb], r0, c0);
             }
             __syncwarp();
-            mbar_wait(&xbar[k], (phase_bits >> k) & 1u);
-            phase_bits ^= 1u << k;
+            mbar_wait(&xbar[xb], (phase_bits >> xb) & 1u);
+            phase_bits ^= 1u << xb;
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {

@@ -42,10 +42,10 @@
 using namespace pe;
 
 // smem ring depths of the GEMM instantiations (gemm_smem_bytes must stay
-// below the 227 KB per-CTA limit): poly/update 5 x 32 KB ring + 64 KB
-// epilogue slots
+// below the 227 KB per-CTA limit): poly/update 6 x 32 KB ring + 32 KB
+// epilogue slots (one per warp)
 #ifndef PE_LONG_STAGES
-#define PE_LONG_STAGES 5
+#define PE_LONG_STAGES 6
 #endif
 constexpr int kLongStages = PE_LONG_STAGES;
 // the Gram (no epilogue operand, one 4 KB staging slot per warp) takes 6
@@ -53,6 +53,15 @@ constexpr int kLongStages = PE_LONG_STAGES;
 #define PE_GRAM_STAGES 6
 #endif
 constexpr int kGramStages = PE_GRAM_STAGES;
+// 4 KB epilogue slots per warp of poly/update: 1 = one slot (operand chunk 1
+// is loaded after chunk 0's result left it), which pays for the sixth ring
+// stage; 2 = the whole tile's operand prefetched during its main loop (with a
+// 5-stage ring).  GPT-2 S update 119.1 -> 114.8 us per launch with 6 / 1,
+// poly unchanged (profiles/r1_variants.md)
+#ifndef PE_OP_SLOTS
+#define PE_OP_SLOTS 1
+#endif
+constexpr int kOpSlots = PE_OP_SLOTS;
 // fp32 (three bf16 planes): 4 x 32 KB ring + 8 warps x 3 plane slots x 4 KB
 constexpr int kP3Stages = 4;
 
@@ -313,10 +322,10 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
                                (int)gemm_smem_bytes<kGramStages, 1>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kGramStages, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kGramStages, 1>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kLongStages, 2>()));
-  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gemm_smem_bytes<kLongStages, 2>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, kOpSlots, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages, kOpSlots>()));
+  PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kLongStages, kOpSlots, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)gemm_smem_bytes<kLongStages, kOpSlots>()));
   PE_CUDA(cudaFuncSetAttribute(pe_gemm_sm100<kP3Stages, 3, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)gemm_smem_bytes<kP3Stages, 3>()));
   PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1199,7 +1208,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     g.a = g.b = g.c = 0.f;
     const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);
     ProfScope ps(c, 6, st);
-    launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, gemm_smem_bytes<kLongStages, 2>(), st, g);
+    launch(pe_gemm_sm100<kLongStages, kOpSlots, true>, grid, kGemmThreads, gemm_smem_bytes<kLongStages, kOpSlots>(), st, g);
     ++launches;
   }
   for (int t = 0; t < T && !fused; ++t) {
@@ -1233,9 +1242,9 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
         else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
       } else {
-        const size_t sm = gemm_smem_bytes<kLongStages, 2>();
-        if (edge) launch(pe_gemm_sm100<kLongStages, 2, true>, grid, kGemmThreads, sm, st, g);
-        else launch(pe_gemm_sm100<kLongStages, 2, false>, grid, kGemmThreads, sm, st, g);
+        const size_t sm = gemm_smem_bytes<kLongStages, kOpSlots>();
+        if (edge) launch(pe_gemm_sm100<kLongStages, kOpSlots, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kLongStages, kOpSlots, false>, grid, kGemmThreads, sm, st, g);
       }
       ++launches;
       }
