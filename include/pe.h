@@ -165,6 +165,27 @@ pe_status pe_polar(pe_ctx ctx, const void* const* in, void* const* out, const in
                    int count, int iters, pe_dtype dtype, void* stream);
 
 /*
+ * pe_polar with separate element types for the caller's input, the caller's
+ * output and the arithmetic: Listing 2 casts the (usually
+ * fp32) Muon momentum to bf16 and iterates in bf16, and returns bf16.
+ *   compute = PE_BF16: in_dtype and out_dtype each PE_BF16 or PE_FP32.  An
+ *     fp32 input is normalised in fp32 (s from the fp64 sum of its squares,
+ *     P:494) and rounded once to bf16 as X_0 = bf16(fp32(x) * inv) (reading
+ *     R16: the fp32 values, not a bf16 copy of them, are normalised); an fp32
+ *     output receives the bf16 result exactly (no further rounding).  These
+ *     matrices go through the copy passes instead of being folded into the
+ *     first / last GEMM, so in == out requires in_dtype == out_dtype.
+ *   compute = PE_FP32: in_dtype = out_dtype = PE_FP32 only (= pe_polar).
+ * Same pointers, shapes, streams and errors as pe_polar, plus
+ * PE_ERR_UNSUPPORTED for other type combinations.  Under CUDA-graph capture a
+ * mixed-type call needs its plan built by an earlier uncaptured call with the
+ * same shapes and types (pe_reserve covers in = out = compute only).
+ */
+pe_status pe_polar_ex(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
+                      int count, int iters, pe_dtype in_dtype, pe_dtype out_dtype, pe_dtype compute,
+                      void* stream);
+
+/*
  * End-to-end variant on HOST buffers: copies in[i] (host) to device staging
  * owned by the context, runs pe_polar, copies the results back to out[i]
  * (host) and synchronises `stream` before returning.  The batch is cut into

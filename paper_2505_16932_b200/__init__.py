@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = [
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
-    "pe_comm_info", "pe_polar_sharded",
+    "pe_comm_info", "pe_polar_sharded", "pe_polar_ex",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -74,6 +74,7 @@ def lib():
         "pe_reserve": (I, [P, I64P, I, I]),
         "pe_polar": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
         "pe_polar_host": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
+        "pe_polar_ex": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, I, I, P]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -247,6 +248,32 @@ class Context:
             stream = torch.cuda.current_stream(inputs[0].device)
         _check(lib().pe_polar(self._h, ins, outs, shp, n, int(iters), dt, ctypes.c_void_p(stream.cuda_stream)),
                "pe_polar")
+        return outputs
+
+    def polar_ex(self, inputs, outputs, iters=5, compute=PE_BF16, stream=None):
+        """pe_polar_ex: the element types of ``inputs`` and ``outputs`` (bf16 or
+        fp32 CUDA tensors, each list of one type) may differ from the
+        arithmetic ``compute`` (PE_BF16: fp32 momentum in, bf16 iteration,
+        bf16 or fp32 out -- Listing 2's X = G.bfloat16())."""
+        import torch
+        n = len(inputs)
+        if len(outputs) != n:
+            raise ValueError("polar_ex takes equally long input / output lists")
+        if n == 0:
+            return outputs
+        di, do = _dtype_code(inputs[0]), _dtype_code(outputs[0])
+        for x, y in zip(inputs, outputs):
+            if x.dim() != 2 or not x.is_contiguous() or not y.is_contiguous() or x.shape != y.shape:
+                raise ValueError("pe_polar_ex takes contiguous 2-D tensors of matching shapes")
+            if _dtype_code(x) != di or _dtype_code(y) != do or not x.is_cuda or not y.is_cuda:
+                raise ValueError("pe_polar_ex takes CUDA tensors, one dtype per list")
+        ins = (ctypes.c_void_p * n)(*[x.data_ptr() for x in inputs])
+        outs = (ctypes.c_void_p * n)(*[y.data_ptr() for y in outputs])
+        shp = _shapes_arr([tuple(x.shape) for x in inputs])
+        if stream is None:
+            stream = torch.cuda.current_stream(inputs[0].device)
+        _check(lib().pe_polar_ex(self._h, ins, outs, shp, n, int(iters), di, do, int(compute),
+                                 ctypes.c_void_p(stream.cuda_stream)), "pe_polar_ex")
         return outputs
 
     def muon_step(self, weights, momenta, grads, beta=0.9, lr=0.02, iters=5, stream=None):

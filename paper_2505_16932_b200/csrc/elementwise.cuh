@@ -243,17 +243,34 @@ template <typename T> __device__ __forceinline__ T from_f(float v);
 template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
-// dst[r][c] = scale * src[r][c] for the rows of each item.
-template <typename T>
+// 8 elements of a row <-> fp32 registers (bf16: one 16-byte vector, fp32: two)
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
+  unpack(*reinterpret_cast<const uint4*>(p), f, (__nv_bfloat16*)nullptr);
+}
+__device__ __forceinline__ void load8(const float* p, float* f) {
+  unpack(*reinterpret_cast<const uint4*>(p), f, (float*)nullptr);
+  unpack(*reinterpret_cast<const uint4*>(p + 4), f + 4, (float*)nullptr);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
+  *reinterpret_cast<uint4*>(p) = pack(f, (__nv_bfloat16*)nullptr);
+}
+__device__ __forceinline__ void store8(float* p, const float* f) {
+  *reinterpret_cast<uint4*>(p) = pack(f, (float*)nullptr);
+  *reinterpret_cast<uint4*>(p + 4) = pack(f + 4, (float*)nullptr);
+}
+
+// dst[r][c] = scale * src[r][c] for the rows of each item (S, D: element
+// types of source and destination; bf16 <-> fp32 conversions for pe_polar_ex).
+template <typename S, typename D = S>
 __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
   pdl_trigger();
   pdl_wait();
-  constexpr int V = VecT<T>::N;
+  constexpr int V = 8;
   for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
     const CopyItem ci = a.items[it];
     const CopyMat cm = a.mats[ci.mat];
-    const T* src = reinterpret_cast<const T*>(a.srcs[ci.mat]);
-    T* dst = reinterpret_cast<T*>(a.dsts[ci.mat]);
+    const S* src = reinterpret_cast<const S*>(a.srcs[ci.mat]);
+    D* dst = reinterpret_cast<D*>(a.dsts[ci.mat]);
     const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
     const bool vec = (cm.cols % V == 0) && (cm.sld % V == 0) && (cm.dld % V == 0) &&
                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
@@ -263,20 +280,19 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
       for (int64_t e = threadIdx.x; e < nv; e += blockDim.x) {
         const int rr = ci.a + (int)(e / vpr);
         const int cc = (int)(e % vpr) * V;
-        const uint4 u = *reinterpret_cast<const uint4*>(src + (size_t)rr * cm.sld + cc);
         float f[V];
-        unpack(u, f, (T*)nullptr);
+        load8(src + (size_t)rr * cm.sld + cc, f);
         if (a.scale) {
 #pragma unroll
           for (int j = 0; j < V; ++j) f[j] = __fmul_rn(f[j], sc);
         }
         if (a.muon) {
           float w[V];
-          unpack(*reinterpret_cast<const uint4*>(dst + (size_t)rr * cm.dld + cc), w, (T*)nullptr);
+          load8(dst + (size_t)rr * cm.dld + cc, w);
 #pragma unroll
           for (int j = 0; j < V; ++j) f[j] = __fsub_rn(w[j], __fmul_rn(a.lr, f[j]));
         }
-        *reinterpret_cast<uint4*>(dst + (size_t)rr * cm.dld + cc) = pack(f, (T*)nullptr);
+        store8(dst + (size_t)rr * cm.dld + cc, f);
       }
     } else {
       const int64_t ne = (int64_t)cm.cols * ci.b;
@@ -286,36 +302,38 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
         float f = to_f(src[(size_t)rr * cm.sld + cc]);
         if (a.scale) f = __fmul_rn(f, sc);
         if (a.muon) f = __fsub_rn(to_f(dst[(size_t)rr * cm.dld + cc]), __fmul_rn(a.lr, f));
-        dst[(size_t)rr * cm.dld + cc] = from_f<T>(f);
+        dst[(size_t)rr * cm.dld + cc] = from_f<D>(f);
       }
     }
   }
 }
 
 // dst (cols x rows) = (scale * src)^T, 64x64 tiles, 256 threads.
-template <typename T>
+template <typename S, typename D = S>
 __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
   pdl_trigger();
   pdl_wait();
-  constexpr int V = VecT<T>::N;                 // elements per 16-byte vector
-  constexpr int VPR = 64 / V;                   // vectors per 64-element tile row
+  constexpr int V = VecT<S>::N;                 // source elements per 16-byte vector
+  constexpr int VPR = 64 / V;                   // source vectors per 64-element tile row
+  constexpr int W = VecT<D>::N;                 // destination elements per 16-byte vector
+  constexpr int WPR = 64 / W;
   __shared__ float tile[64][65];
   for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
     const CopyItem ci = a.items[it];
     const CopyMat cm = a.mats[ci.mat];
-    const T* src = reinterpret_cast<const T*>(a.srcs[ci.mat]);
-    T* dst = reinterpret_cast<T*>(a.dsts[ci.mat]);
+    const S* src = reinterpret_cast<const S*>(a.srcs[ci.mat]);
+    D* dst = reinterpret_cast<D*>(a.dsts[ci.mat]);
     const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
     const int r0 = ci.a * 64, c0 = ci.b * 64;
     const bool vin = (cm.sld % V == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-    const bool vout = (cm.dld % V == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    const bool vout = (cm.dld % W == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
     // load 64 x 64 (rows r0.., cols c0..)
     for (int e = threadIdx.x; e < 64 * VPR; e += 256) {
       const int i = e / VPR, jv = (e % VPR) * V;
       const int r = r0 + i, c = c0 + jv;
       float f[V];
       if (vin && r < cm.rows && c + V <= cm.cols) {
-        unpack(*reinterpret_cast<const uint4*>(src + (size_t)r * cm.sld + c), f, (T*)nullptr);
+        unpack(*reinterpret_cast<const uint4*>(src + (size_t)r * cm.sld + c), f, (S*)nullptr);
       } else {
 #pragma unroll
         for (int j = 0; j < V; ++j) f[j] = (r < cm.rows && c + j < cm.cols) ? to_f(src[(size_t)r * cm.sld + c + j]) : 0.f;
@@ -325,28 +343,28 @@ __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
     }
     __syncthreads();
     // store transposed: dst row = c0 + i (source column), dst cols = r0.. (source rows)
-    for (int e = threadIdx.x; e < 64 * VPR; e += 256) {
-      const int i = e / VPR, jv = (e % VPR) * V;
+    for (int e = threadIdx.x; e < 64 * WPR; e += 256) {
+      const int i = e / WPR, jv = (e % WPR) * W;
       const int dr = c0 + i, dc = r0 + jv;
       if (dr >= cm.cols) continue;
-      float f[V];
+      float f[W];
 #pragma unroll
-      for (int j = 0; j < V; ++j) f[j] = tile[jv + j][i];
-      if (vout && dc + V <= cm.rows) {
+      for (int j = 0; j < W; ++j) f[j] = tile[jv + j][i];
+      if (vout && dc + W <= cm.rows) {
         if (a.muon) {
-          float w[V];
-          unpack(*reinterpret_cast<const uint4*>(dst + (size_t)dr * cm.dld + dc), w, (T*)nullptr);
+          float w[W];
+          unpack(*reinterpret_cast<const uint4*>(dst + (size_t)dr * cm.dld + dc), w, (D*)nullptr);
 #pragma unroll
-          for (int j = 0; j < V; ++j) f[j] = __fsub_rn(w[j], __fmul_rn(a.lr, f[j]));
+          for (int j = 0; j < W; ++j) f[j] = __fsub_rn(w[j], __fmul_rn(a.lr, f[j]));
         }
-        *reinterpret_cast<uint4*>(dst + (size_t)dr * cm.dld + dc) = pack(f, (T*)nullptr);
+        *reinterpret_cast<uint4*>(dst + (size_t)dr * cm.dld + dc) = pack(f, (D*)nullptr);
       } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j)
+        for (int j = 0; j < W; ++j)
           if (dc + j < cm.rows) {
             float v = f[j];
             if (a.muon) v = __fsub_rn(to_f(dst[(size_t)dr * cm.dld + dc + j]), __fmul_rn(a.lr, v));
-            dst[(size_t)dr * cm.dld + dc + j] = from_f<T>(v);
+            dst[(size_t)dr * cm.dld + dc + j] = from_f<D>(v);
           }
       }
     }

@@ -466,10 +466,14 @@ static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size
 
 // no_orient: keep rows as the Gram side even when rows > cols (a column
 // shard of a wide matrix, pe_polar_split).
+// io (bf16 compute only, pe_polar_ex): bit 0 = the caller's input is fp32,
+// bit 1 = the caller's output is fp32; such matrices go through the copy
+// passes (conversion) instead of being folded into the first / last GEMM.
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
-                            bool no_orient = false) {
+                            bool no_orient = false, int io = 0) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
   if (no_orient) key.push_back(-1);
+  if (io) key.push_back(-2 - io);
   for (Plan* p : c->plans)
     if (p->dtype == dtype && p->key == key) {
       p->last_use = ++c->use_clock;
@@ -588,8 +592,9 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   std::vector<void*> x0(count);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
-    const bool folded = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
-    const bool direct = folded;
+    const bool foldable = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
+    const bool folded = foldable && !(io & 1);
+    const bool direct = foldable && !(io & 2);
     mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0);
     x0[i] = md.X[0];
     const int64_t pst = (int64_t)md.m * md.ldx;
@@ -987,7 +992,8 @@ struct SplitCtx {
 // matrices) or the finalize pass (the others).
 static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, const void* const* grads,
                             const int64_t* shapes, int count, int iters, pe_dtype dtype, void* stream_,
-                            double beta, double lr, cudaStream_t up = nullptr, const SplitCtx* sh = nullptr) {
+                            double beta, double lr, cudaStream_t up = nullptr, const SplitCtx* sh = nullptr,
+                            int io = 0) {
   if (!c || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
   if (count == 0) { c->last_launches = 0; return PE_OK; }
   if (!in || !out) return PE_ERR_INVALID_ARG;
@@ -1014,12 +1020,14 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     g_last_error = "pe_polar_split: one bf16 shard with cols % 8 == 0, not under graph capture";
     return PE_ERR_UNSUPPORTED;
   }
-  if (!muon && !sh && small_eligible(shapes, count, dtype, &max_npad))
+  if (io && (dtype != PE_BF16 || muon || sh)) return PE_ERR_UNSUPPORTED;
+  if (!muon && !sh && !io && small_eligible(shapes, count, dtype, &max_npad))
     return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad, up);
   Plan* P = nullptr;
   if (capturing) {
     // no allocation or synchronisation is allowed: the plan must be cached
     std::vector<int64_t> key(shapes, shapes + 2 * count);
+    if (io) key.push_back(-2 - io);
     for (Plan* q : c->plans)
       if (q->dtype == dtype && q->key == key) P = q;
     if (!P || (dtype == PE_FP32 && !c->scratch)) {
@@ -1027,7 +1035,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       return PE_ERR_WORKSPACE;
     }
     P->last_use = ++c->use_clock;
-  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr)) != PE_OK) {
+  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr, io)) != PE_OK) {
     return s;
   }
 
@@ -1095,7 +1103,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   const float* d_coef = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(cs->d) + call_coef_off(count));
   void** d_fin_src = d_ptrs + 2 * count;
   void** d_out = d_ptrs + 3 * count;
-  const int src_f32 = (dtype == PE_FP32);
+  const int src_f32 = (dtype == PE_FP32) || (io & 1);
   int launches = 0;
 
   // 1) norm
@@ -1162,9 +1170,19 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     const int grid = std::min(P->n_it[k], c->num_sms * 8);
     ProfScope ps(c, fin ? 5 : 1, st);
     const bool tr = (k == 1 || k == 2);
-    if (dtype == PE_BF16) {
-      if (tr) launch(pe_transpose_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
-      else launch(pe_rows_kernel<__nv_bfloat16>, grid, 256, 0, st, ca);
+    using bf = __nv_bfloat16;
+    if (dtype == PE_BF16 && ((!fin && (io & 1)) || (fin && (io & 2)))) {
+      // pe_polar_ex: fp32 caller input -> bf16 X_0, or bf16 result -> fp32 caller output
+      if (!fin) {
+        if (tr) launch(pe_transpose_kernel<float, bf>, grid, 256, 0, st, ca);
+        else launch(pe_rows_kernel<float, bf>, grid, 256, 0, st, ca);
+      } else {
+        if (tr) launch(pe_transpose_kernel<bf, float>, grid, 256, 0, st, ca);
+        else launch(pe_rows_kernel<bf, float>, grid, 256, 0, st, ca);
+      }
+    } else if (dtype == PE_BF16) {
+      if (tr) launch(pe_transpose_kernel<bf>, grid, 256, 0, st, ca);
+      else launch(pe_rows_kernel<bf>, grid, 256, 0, st, ca);
     } else if (scale) {
       if (tr) launch(pe_planes_kernel<true, true>, grid, 256, 0, st, ca);
       else launch(pe_planes_kernel<true, false>, grid, 256, 0, st, ca);
@@ -1276,6 +1294,22 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
 extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
                               int count, int iters, pe_dtype dtype, void* stream) {
   return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
+}
+
+extern "C" pe_status pe_polar_ex(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
+                                 int count, int iters, pe_dtype in_dtype, pe_dtype out_dtype, pe_dtype compute,
+                                 void* stream) {
+  auto ok = [](pe_dtype d) { return d == PE_BF16 || d == PE_FP32; };
+  if (!ok(in_dtype) || !ok(out_dtype) || !ok(compute)) return PE_ERR_INVALID_ARG;
+  if (compute == PE_FP32) {
+    if (in_dtype != PE_FP32 || out_dtype != PE_FP32) {
+      g_last_error = "pe_polar_ex: fp32 compute takes fp32 input and output";
+      return PE_ERR_UNSUPPORTED;
+    }
+    return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_FP32, stream, 0.0, 0.0);
+  }
+  const int io = (in_dtype == PE_FP32 ? 1 : 0) | (out_dtype == PE_FP32 ? 2 : 0);
+  return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_BF16, stream, 0.0, 0.0, nullptr, nullptr, io);
 }
 
 extern "C" pe_status pe_polar_split(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,

@@ -948,3 +948,48 @@ def test_polar_sharded_single_rank_communicator():
             assert torch.equal(y.view(torch.int16), r.view(torch.int16))
             assert torch.equal(z.view(torch.int16), r.view(torch.int16))
     c.close()
+
+
+@pytest.mark.parametrize("shape", [(768, 3072), (3072, 768), (520, 200), (200, 520), (300, 1100), (96, 100)])
+def test_polar_ex_fp32_momentum_bf16_compute(ctx, shape):
+    """pe_polar_ex (compute bf16): fp32 input normalised in fp32 and rounded
+    once to bf16 (R16) against the oracle on the fp32 values (G1/G3); the
+    fp32 output is exactly the bf16 output; a bf16 input with an fp32 output
+    is exactly pe_polar's bf16 result (same arithmetic, only the last store
+    differs).  Tall and unaligned (cols % 8 != 0) shapes included."""
+    M32 = syn.gaussian(*shape, seed=900 + shape[0] + shape[1], std=0.02).astype(np.float32)
+    x32 = torch.from_numpy(M32).cuda()
+    yb = ctx.polar_ex([x32], [torch.empty(shape, dtype=torch.bfloat16, device="cuda")])[0]
+    yf = ctx.polar_ex([x32], [torch.empty(shape, dtype=torch.float32, device="cuda")])[0]
+    torch.cuda.synchronize()
+    X = yb.float().cpu().numpy().astype(np.float64)
+    assert torch.equal(yf, yb.float())
+    check_g1_g3(X, M32.astype(np.float64), g1=g1_gate(min(shape)))
+    # bf16 in, fp32 out == pe_polar (bf16) upcast
+    Mb = bf16_values(M32)
+    xb = to_dev_bf16(Mb)
+    ref = ctx.polar([xb])[0]
+    yf2 = ctx.polar_ex([xb], [torch.empty(shape, dtype=torch.float32, device="cuda")])[0]
+    torch.cuda.synchronize()
+    assert torch.equal(yf2, ref.float())
+
+
+def test_polar_ex_type_combinations(ctx):
+    """Same-type calls equal pe_polar; fp32 compute needs fp32 in and out."""
+    M = syn.gaussian(256, 640, seed=31, std=0.02).astype(np.float32)
+    x32 = torch.from_numpy(M).cuda()
+    xb = to_dev_bf16(bf16_values(M))
+    assert torch.equal(ctx.polar_ex([x32], [torch.empty_like(x32)], compute=pe.PE_FP32)[0], ctx.polar([x32])[0])
+    assert torch.equal(ctx.polar_ex([xb], [torch.empty_like(xb)])[0].view(torch.int16),
+                       ctx.polar([xb])[0].view(torch.int16))
+    with pytest.raises(pe.PeError):
+        ctx.polar_ex([xb], [torch.empty_like(x32)], compute=pe.PE_FP32)
+    # mixed batch in one call: fp32 inputs of several shapes -> bf16 outputs
+    shapes = [(128, 384), (384, 128), (64, 72)]
+    xs = [torch.from_numpy(syn.gaussian(r, c, seed=40 + i, std=0.02).astype(np.float32)).cuda()
+          for i, (r, c) in enumerate(shapes)]
+    ys = ctx.polar_ex(xs, [torch.empty(s, dtype=torch.bfloat16, device="cuda") for s in shapes])
+    one = [ctx.polar_ex([x], [torch.empty(s, dtype=torch.bfloat16, device="cuda")])[0] for x, s in zip(xs, shapes)]
+    torch.cuda.synchronize()
+    for y, o in zip(ys, one):
+        assert torch.equal(y.view(torch.int16), o.view(torch.int16))
