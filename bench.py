@@ -160,6 +160,25 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
     return out
 
 
+def pctl(ms):
+    """median / p10 / p90 of per-step device times."""
+    v = sorted(ms)
+    q = lambda f: v[min(len(v) - 1, max(0, int(round(f * (len(v) - 1)))))]
+    return {"median_ms": round(q(0.5), 4), "p10_ms": round(q(0.1), 4), "p90_ms": round(q(0.9), 4),
+            "mean_ms": round(sum(v) / len(v), 4), "n": len(v)}
+
+
+def norm_gbs(prof, shapes, steps, peaks):
+    """Achieved HBM bandwidth of the norm pass (row a3: m*n elements read)."""
+    tot, cnt = prof.get("norm", (0.0, 0))
+    if cnt == 0 or tot <= 0:
+        return None
+    nbytes = sum(2.0 * r * c for r, c in shapes)
+    gbs = nbytes / (tot / cnt * 1e-3) / 1e9
+    return {"bytes_per_launch": nbytes, "launch_ms": round(tot / cnt, 4), "achieved_gbs": round(gbs, 1),
+            "peak_gbs": peaks["hbm_gbs"], "frac": round(gbs / peaks["hbm_gbs"], 4)}
+
+
 def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
     """The fp64 oracle (as it stands) on host cores over a bounded sample."""
     import pe_synth as syn
@@ -276,7 +295,28 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
     # with per-launch events gives the per-kernel split and the roofline
     ms, _ = timed(False)
     _, prof = timed(True)
-    return ms, prof, launches, idx, xs, ys
+    graph_ms = None
+    if not (dist_on and world > 1):
+        # the whole layer set replayed from one CUDA graph (the
+        # reserved plan: no allocation or synchronisation while capturing)
+        try:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=torch.cuda.Stream(device)):
+                ctx.polar(xs, ys, iters=T, stream=torch.cuda.current_stream(device))
+            gr.replay()
+            torch.cuda.synchronize(device)
+            gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for k in range(steps):
+                flush.zero_()
+                gevs[k][0].record()
+                gr.replay()
+                gevs[k][1].record()
+            torch.cuda.synchronize(device)
+            graph_ms = [a.elapsed_time(b) for a, b in gevs]
+            del gr
+        except Exception as e:                       # reported, not fatal
+            graph_ms = str(e)[:200]
+    return ms, prof, launches, idx, xs, ys, graph_ms
 
 
 def main():
@@ -315,8 +355,8 @@ def main():
 
     clocks = ClockSampler(local_rank)
     clocks.start()
-    ms, prof, launches, idx, xs, ys = time_workload(ctx, shapes, T, args.steps, args.warmup, world, rank,
-                                                    device, flush, dist_on)
+    ms, prof, launches, idx, xs, ys, graph_ms = time_workload(ctx, shapes, T, args.steps, args.warmup, world,
+                                                              rank, device, flush, dist_on)
     clk = clocks.stop()
     mean_ms = sum(ms) / len(ms)
     if dist_on:
@@ -363,6 +403,9 @@ def main():
         "clocks": clk,
         "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+        "ms_per_step_stats": pctl(ms),
+        "graph_replay": (pctl(graph_ms) if isinstance(graph_ms, list) else graph_ms),
+        "norm_pass": norm_gbs(prof, [shapes[i] for i in idx], args.steps, peaks),
     }
 
     # extra layer sets (north-star Llama-3-8B) at N=1
@@ -374,7 +417,7 @@ def main():
             ctx2 = pe.Context(local_rank)
             c2 = ClockSampler(local_rank)
             c2.start()
-            ms2, prof2, l2, idx2, xs2, ys2 = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False)
+            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False)
             ck2 = c2.stop()
             m2 = sum(ms2) / len(ms2)
             f2 = pe.pe_flops(sh, T, DEGREE)
