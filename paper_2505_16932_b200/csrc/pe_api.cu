@@ -522,15 +522,31 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   // Update tiles are generated row-block fastest so concurrently running
   // tiles share a column panel of X (L2 reuse); lists are then stably sorted
   // longest K first.
+  // Matrices with more than 16 row blocks (m > 4096) are walked in bands of
+  // kBand = 8 row blocks (grouped rasterisation): a wave of ~74 concurrent
+  // tiles then touches about 8 + 74 / 8 operand panels instead of 1 + 74, so
+  // the panels it streams are shared through L2 (16384^2: 8 MB per panel;
+  // call 77.6 -> 70.7 ms, 8192^2 7.63 -> 7.48 ms).  At m = 4096 the plain
+  // orders measured 2-4 % faster (the whole iterate is about L2-sized), so
+  // smaller matrices keep them.
   std::vector<Tile> sym, upd;
   const int tile = kBN;
+  static const int kBand = getenv("PE_BAND") ? std::max(1, atoi(getenv("PE_BAND"))) : 8;   // A/B knob
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
     const int nm = cdiv(md.m, tile), nn = cdiv(md.n, tile);
-    for (int tm = 0; tm < nm; ++tm)
-      for (int tn = tm; tn < nm; ++tn) sym.push_back({i, tm, tn, 0});
-    for (int tn = 0; tn < nn; ++tn)
-      for (int tm = 0; tm < nm; ++tm) upd.push_back({i, tm, tn, 0});
+    const int band = (nm > 16) ? kBand : nm;
+    if (band == nm) {
+      for (int tm = 0; tm < nm; ++tm)
+        for (int tn = tm; tn < nm; ++tn) sym.push_back({i, tm, tn, 0});
+    } else {
+      for (int b0 = 0; b0 < nm; b0 += band)
+        for (int tn = b0; tn < nm; ++tn)
+          for (int tm = b0; tm < std::min(b0 + band, nm) && tm <= tn; ++tm) sym.push_back({i, tm, tn, 0});
+    }
+    for (int b0 = 0; b0 < nm; b0 += band)
+      for (int tn = 0; tn < nn; ++tn)
+        for (int tm = b0; tm < std::min(b0 + band, nm); ++tm) upd.push_back({i, tm, tn, 0});
   }
   auto by_k = [&](bool gram) {
     return [&, gram](const Tile& x, const Tile& y) {
