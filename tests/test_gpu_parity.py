@@ -849,7 +849,7 @@ def test_back_to_back_async_calls_stress(ctx):
             assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
 
 
-def _r8_emulated(M, T):
+def _r8_emulated(M, T, f32_input=False):
     """CPU emulation of the bf16 rounding points (reading R8: bf16 operands,
     exact products accumulated in fp64 then rounded to fp32, A rounded once,
     B and X' rounded once from fp32 epilogues, first iteration folded when the
@@ -857,8 +857,8 @@ def _r8_emulated(M, T):
     error this reading itself makes, used to scale the fuzz gate."""
     bf = lambda x: syn.to_bf16_values(np.asarray(x, np.float32)).astype(np.float32)    # noqa: E731
     mm = lambda a, b: (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)  # noqa: E731
-    fold = M.shape[1] % 8 == 0          # the library folds 1/s into iteration 1 exactly then
-    X = bf(M)
+    fold = M.shape[1] % 8 == 0 and not f32_input   # the library folds 1/s into iteration 1 exactly then
+    X = np.asarray(M, np.float32) if f32_input else bf(M)    # pe_polar_ex: fp32 input scaled in fp32 (R16)
     tall = X.shape[0] > X.shape[1]
     if tall:
         X = X.T.copy()
@@ -993,3 +993,39 @@ def test_polar_ex_type_combinations(ctx):
     torch.cuda.synchronize()
     for y, o in zip(ys, one):
         assert torch.equal(y.view(torch.int16), o.view(torch.int16))
+
+
+@pytest.mark.slow
+def test_polar_ex_random_calls_fuzz(ctx):
+    """Fuzz pe_polar_ex: 40 random batches of fp32 momentum (sides around the
+    tile and packing boundaries, both orientations, T = 1..8), bf16
+    arithmetic, bf16 or fp32 output, against the oracle on the fp32 values
+    with the same gates as the bf16 fuzz (the emulation takes R16's explicit
+    X_0 = bf16(fp32(x) * inv)); an fp32 output is the bf16 result exactly."""
+    rng = np.random.default_rng(77)
+    edges = [1, 7, 8, 63, 64, 65, 127, 128, 129, 255, 256, 257, 300, 513]
+
+    def side():
+        return int(rng.choice(edges)) if rng.random() < 0.5 else int(rng.integers(1, 900))
+
+    for call in range(40):
+        T = int(rng.integers(1, 9))
+        shapes = [(side(), side()) for _ in range(int(rng.integers(1, 5)))]
+        mats = [syn.gaussian(r, c, seed=20000 + 100 * call + i, std=0.02).astype(np.float32)
+                for i, (r, c) in enumerate(shapes)]
+        xs = [torch.from_numpy(M).cuda() for M in mats]
+        out_f32 = rng.random() < 0.5
+        ys = ctx.polar_ex(xs, [torch.empty(M.shape, dtype=torch.float32 if out_f32 else torch.bfloat16,
+                                           device="cuda") for M in mats], iters=T)
+        torch.cuda.synchronize()
+        for y, M in zip(ys, mats):
+            X = y.float().cpu().numpy().astype(np.float64)
+            if out_f32:
+                assert np.array_equal(X.astype(np.float32), syn.to_bf16_values(X.astype(np.float32)))
+            M64 = M.astype(np.float64)
+            ref = oi.polar_express(M64, TABLE, T)
+            err = om.rel_frobenius(X, ref)
+            m = min(M.shape)
+            emu = om.rel_frobenius(_r8_emulated(M64, T, f32_input=True), ref)
+            gate = max(5e-2 if m == 1 else g1_gate(m), 1.5 * emu + 2e-3)
+            assert np.all(np.isfinite(X)) and err <= gate, (call, M.shape, T, err, emu)
