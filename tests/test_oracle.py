@@ -444,3 +444,58 @@ def test_muon_step_pins():
     g = rng.standard_normal((1, 50))
     W3, _ = oi.muon_step(np.zeros((1, 50)), np.zeros((1, 50)), g, 0.0, 1.0, table, 12)
     assert np.allclose(-W3, g / np.linalg.norm(g), rtol=0, atol=1e-6)
+
+
+def _mp_quintic(l, u, mp):
+    """Listing 1's optimal_quintic in 60-digit arithmetic, with
+    the Remez loop run to the high-precision fixed point (|dE| < 1e-50)."""
+    if l / u >= mp.mpf(1) - mp.mpf("5e-6"):
+        return (mp.mpf(15) / 8 / u, mp.mpf(-10) / 8 / u ** 3, mp.mpf(3) / 8 / u ** 5)
+    q, r = (3 * l + u) / 4, (l + 3 * u) / 4
+    E, old = mp.inf, None
+    for _ in range(200):
+        if old is not None and abs(old - E) < mp.mpf("1e-50"):
+            break
+        old = E
+        M = mp.matrix([[l, l ** 3, l ** 5, 1], [q, q ** 3, q ** 5, -1],
+                       [r, r ** 3, r ** 5, 1], [u, u ** 3, u ** 5, -1]])
+        a, b, c, E = mp.lu_solve(M, mp.matrix([1, 1, 1, 1]))
+        d = mp.sqrt(9 * b ** 2 - 20 * a * c)
+        q, r = mp.sqrt((-3 * b - d) / (10 * c)), mp.sqrt((-3 * b + d) / (10 * c))
+    return (a, b, c)
+
+
+def test_coefficients_against_60_digit_replay():
+    """SURVEY §8(c)1 cross-check: Listing 1's greedy composition (cushion,
+    recentring) replayed in 60-digit mpmath arithmetic agrees with
+    the fp64 oracle tuple by tuple (tuples 1-6 to 1e-12 relative, tuple 7 to
+    1e-9 where the tiny interval makes the fp64 solve ill-conditioned, the
+    Pade tail exactly, reading R4) -- i.e. the oracle's fp64 evaluation loses
+    no accuracy that matters -- and the pre-safety table P:476-483 matches
+    the high-precision values as well."""
+    mpmath = pytest.importorskip("mpmath")
+    mp = mpmath.mp
+    mp.dps = 60
+    l, u = mp.mpf("1e-3"), mp.mpf(1)
+    cushion = mp.mpf("0.02407327424182761")
+    hp = []
+    for _ in range(8):
+        a, b, c = _mp_quintic(max(l, cushion * u), u, mp)
+        if max(l, cushion * u) / u < mp.mpf(1) - mp.mpf("5e-6"):
+            p = lambda x: a * x + b * x ** 3 + c * x ** 5      # noqa: E731
+            s = 2 / (p(l) + p(u))                               # P:545
+            a, b, c = a * s, b * s, c * s
+        else:
+            a, b, c = mp.mpf(15) / 8, mp.mpf(-10) / 8, mp.mpf(3) / 8
+        hp.append((a, b, c))
+        l = a * l + b * l ** 3 + c * l ** 5
+        u = 2 - l
+    raw, pade, _ = oc.greedy_composition(1e-3, 8)
+    printed = [tuple(float(v) for v in line.split()) for line in
+               open(os.path.join(GOLD, "listing2_coeffs_pre_safety.txt")) if line.strip() and not line.startswith("#")]
+    for t, (h, o, pr) in enumerate(zip(hp, raw, printed)):
+        tol = 1e-12 if t < 6 else (1e-9 if t == 6 else 0.0)
+        for hv, ov, pv in zip(h, o, pr):
+            assert abs(float(hv) - ov) <= tol * abs(float(hv)), (t, float(hv), ov)
+            if t < 7:
+                assert abs(float(hv) - pv) <= max(tol, 1e-13) * abs(float(hv)) + 1e-14, (t, float(hv), pv)
