@@ -1029,3 +1029,31 @@ def test_polar_ex_random_calls_fuzz(ctx):
             emu = om.rel_frobenius(_r8_emulated(M64, T, f32_input=True), ref)
             gate = max(5e-2 if m == 1 else g1_gate(m), 1.5 * emu + 2e-3)
             assert np.all(np.isfinite(X)) and err <= gate, (call, M.shape, T, err, emu)
+
+
+def test_dist_attach_and_polar_sharded_world_one():
+    """dist.attach over a 1-rank torch.distributed NCCL group hands libpe its
+    communicator (unique id broadcast through torch.distributed); then
+    dist.polar_sharded equals pe_polar bit for bit on a mixed batch."""
+    import socket
+    import torch.distributed as tdist
+    from paper_2505_16932_b200 import dist as pdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                             device_id=torch.device("cuda", 0))
+    try:
+        c = pe.Context(0)
+        assert pdist.attach(c) == (0, 1)
+        shapes = [(768, 768), (3072, 768), (130, 1000)]
+        xs = [to_dev_bf16(bf16_values(syn.gaussian(r, cc, seed=800 + i, std=0.02))) for i, (r, cc) in enumerate(shapes)]
+        ref = c.polar(xs, iters=5)
+        ys = pdist.polar_sharded(c, xs, [torch.empty_like(x) for x in xs], iters=5)
+        torch.cuda.synchronize()
+        for y, r in zip(ys, ref):
+            assert torch.equal(y.view(torch.int16), r.view(torch.int16))
+        c.close()
+    finally:
+        tdist.destroy_process_group()
