@@ -291,7 +291,38 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
     };
     const int vpr = vec ? md.cols / V : md.cols;
     double acc = 0.0;
-    if (md.tall) {
+    if (md.tall && kP == 1 && vec && fold) {
+      // Tall bf16, 16-byte rows: coalesced 16-byte loads of the caller's rows
+      // (unit e = caller row i, columns 8v .. 8v+7 = X rows 8v .. 8v+7 at
+      // X column i), eight in flight per thread, scattered into X as bf16.
+      // (The per-element column gather above kept ~32 two-byte loads in
+      // flight and took half of the call on 768 x 64 head slices.)
+      const int upr = md.cols / 8;
+      const int nunits = md.rows * upr;
+      const uint4* src = reinterpret_cast<const uint4*>(md.in);
+      for (int base = tid; base < nunits; base += kSmallThreads * 8) {
+        uint4 q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int e = base + j * kSmallThreads;
+          q[j] = (e < nunits) ? __ldg(src + e) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int e = base + j * kSmallThreads;
+          if (e >= nunits) break;
+          const int i = e / upr, v = e - i * upr;
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q[j]);
+          const uint32_t col = ((uint32_t)(i & 7) << 1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float f = __bfloat162float(h[k]);
+            acc += (double)(f * f);
+            *reinterpret_cast<__nv_bfloat16*>(X + small_unit(roff + 8 * v + k, i >> 3) + col) = h[k];
+          }
+        }
+      }
+    } else if (md.tall) {
       for (int u0 = 0; u0 < nu; u0 += 4) {
         float f[4][8];
         gather(u0, f);
@@ -471,7 +502,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
                       __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(X + 2 * xplane + off)));
       return f;
     };
-    if (md.tall && tid < m) {
+    if (md.tall && kP == 1 && (md.cols % 8 == 0) && ((reinterpret_cast<uintptr_t>(md.out) & 15) == 0)) {
+      // tall bf16, 16-byte rows: unit e = caller row i, columns 8v .. 8v+7,
+      // gathered from X rows 8v .. 8v+7 at X column i, one 16-byte store
+      const int upr = md.cols / 8;
+      const int nunits = md.rows * upr;
+      uint4* dst = reinterpret_cast<uint4*>(md.out);
+      for (int e = tid; e < nunits; e += kSmallThreads) {
+        const int i = e / upr, v = e - i * upr;
+        const uint32_t col = ((uint32_t)(i & 7) << 1);
+        uint4 u;
+        __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          h[k] = *reinterpret_cast<const __nv_bfloat16*>(X + small_unit(roff + 8 * v + k, i >> 3) + col);
+        dst[e] = u;
+      }
+    } else if (md.tall && tid < m) {
       // thread r scatters its X row into caller column r (a warp's stores to
       // one caller row are contiguous)
       for (int u = 0; u < md.n_pad / 8; ++u) {
