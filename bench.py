@@ -47,14 +47,43 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """Clocks and throttle reasons DURING the timed region (B200_PROFILING.md
+    clocks line): NVML polled every ~2 ms from a thread while `active` (the
+    timed steps, host enqueue to device completion); nvidia-smi at 200 ms if
+    NVML is unavailable."""
 
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self.active = False
+        self._stop = False
 
     def start(self):
+        if os.environ.get("PE_BENCH_SAMPLER") == "smi":     # A/B knob: skip NVML
+            self.nvml = None
+            return self._start_smi()
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            try:
+                pr = torch.cuda.get_device_properties(self.device)
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.nvml, self.h = pynvml, h
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
+        self._start_smi()
+
+    def _start_smi(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device),
@@ -66,36 +95,58 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self._stop:
+            if self.active:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((float(sm), float(mx), int(rs)))
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            if self.active:
+                self.lines.append(line.strip())
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self._stop = True
+        if self.nvml is None and not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no NVML / nvidia-smi"]}
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         self.t.join(timeout=2)
         sm, smax, reasons = [], [], set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 4:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-                bits = int(parts[3], 16) if parts[3].startswith("0x") else int(parts[3])
-                for b, name in REASON_BITS.items():
-                    if bits & b and name != "gpu_idle":
-                        reasons.add(name)
-            except ValueError:
-                continue
+        if self.nvml is not None:
+            rows = self.samples
+            src = "nvml 2 ms, timed steps only"
+        else:
+            rows = []
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                try:
+                    bits = int(parts[3], 16) if parts[3].startswith("0x") else int(parts[3])
+                    rows.append((float(parts[0]), float(parts[1]), bits))
+                except (ValueError, IndexError):
+                    continue
+            src = "nvidia-smi 200 ms, timed steps only"
+        for a, b, bits in rows:
+            sm.append(a)
+            smax.append(b)
+            for bit, name in REASON_BITS.items():
+                if bits & bit and name != "gpu_idle":
+                    reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": src}
 
 
 def layer_set(name):
@@ -165,7 +216,7 @@ def pctl(ms):
     v = sorted(ms)
     q = lambda f: v[min(len(v) - 1, max(0, int(round(f * (len(v) - 1)))))]
     return {"median_ms": round(q(0.5), 4), "p10_ms": round(q(0.1), 4), "p90_ms": round(q(0.9), 4),
-            "mean_ms": round(sum(v) / len(v), 4), "n": len(v)}
+            "mean_ms": round(sum(v) / len(v), 4), "n": len(v), "all_ms": [round(x, 4) for x in ms]}
 
 
 def norm_gbs(prof, shapes, steps, peaks):
@@ -240,7 +291,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dist_on):
+def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dist_on, clocks=None):
     """Device-timed steps of one layer set; returns per-step ms list, profile, extras."""
     import torch
     import paper_2505_16932_b200 as pe
@@ -267,7 +318,8 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         else:
             ctx.polar(xs, ys, iters=T, stream=stream)
 
-    for _ in range(warmup):
+    for _ in range(max(0, warmup - 1)):        # + 1 inside timed(), right before the timed steps
+        flush.zero_()                          # warm-up steps see the same flushed L2 as timed ones
         step()
     torch.cuda.synchronize(device)
     launches = ctx.last_launch_count()
@@ -276,14 +328,25 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         if dist_on:
             torch.distributed.barrier()
         torch.cuda.synchronize(device)
+        if clocks is not None and not profile:
+            clocks.active = True
         ctx.profile_enable(profile)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        # the last warm-up step is enqueued right before the timed ones (no
+        # idle gap before the first timed step).  Warm-up steps flush L2 like
+        # the timed ones: the first write to the 256 MiB flush buffer made the
+        # following step ~0.2 ms slower (profiles/first_step.py), which used to
+        # land on timed step 1.
+        flush.zero_()
+        step()
         for k in range(steps):
             flush.zero_()                    # evict L2 (buffer > 126 MB) between timed steps
             evs[k][0].record(stream)
             step()
             evs[k][1].record(stream)
         torch.cuda.synchronize(device)
+        if clocks is not None:
+            clocks.active = False
         if dist_on:
             torch.distributed.barrier()
         prof = ctx.profile_read() if profile else None
@@ -356,7 +419,7 @@ def main():
     clocks = ClockSampler(local_rank)
     clocks.start()
     ms, prof, launches, idx, xs, ys, graph_ms = time_workload(ctx, shapes, T, args.steps, args.warmup, world,
-                                                              rank, device, flush, dist_on)
+                                                              rank, device, flush, dist_on, clocks)
     clk = clocks.stop()
     mean_ms = sum(ms) / len(ms)
     if dist_on:
@@ -417,7 +480,7 @@ def main():
             ctx2 = pe.Context(local_rank)
             c2 = ClockSampler(local_rank)
             c2.start()
-            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False)
+            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False, c2)
             ck2 = c2.stop()
             m2 = sum(ms2) / len(ms2)
             f2 = pe.pe_flops(sh, T, DEGREE)
