@@ -42,7 +42,7 @@ typedef enum {
   PE_ERR_UNSUPPORTED = 2,     /* e.g. degree not in {3,5}, no sm_100 device   */
   PE_ERR_NO_CONVERGENCE = 3,  /* Remez exceeded 50 iterations (reading R6)    */
   PE_ERR_CUDA = 4,            /* CUDA runtime/driver error (sticky errors too) */
-  PE_ERR_NCCL = 5,            /* reserved for the multi-GPU all-gather        */
+  PE_ERR_NCCL = 5,            /* NCCL missing or failed (multi-GPU calls)     */
   PE_ERR_WORKSPACE = 6        /* device allocation failed                     */
 } pe_status;
 
@@ -239,6 +239,24 @@ pe_status pe_muon_step(pe_ctx ctx, void* const* W, void* const* M, const void* c
 typedef pe_status (*pe_allreduce_fn)(void* buf, int64_t count, int dtype, void* user, void* stream);
 pe_status pe_polar_split(pe_ctx ctx, const void* in, void* out, int64_t rows, int64_t cols, int iters,
                            pe_allreduce_fn allreduce, void* user, void* stream);
+
+/*
+ * Spectrum-aware first step (App. G, k = 1; reading R17), for
+ * inputs with one large outlying singular value.  power_iters > 0 turns it
+ * on for the context's later bf16 pe_polar / pe_polar_ex / pe_polar_host
+ * calls (0 = off, the default): after Listing 2's normalisation X_0 = M / s,
+ * power_iters steps of the power method on A_0 = X_0 X_0^T (deterministic
+ * start vector v0_i = frac((i+1)/phi) + 0.5) give the Rayleigh quotient
+ * lambda <= sigma_1(X_0)^2 and z = sqrt(lambda) / ||X_0||_F; when
+ * 1/sqrt(2) <= z <= 1 - 1e-6 the odd cubic p(x) = a x + b x^3 of
+ * eq. (init_poly) (p(sqrt(1-z^2)) = p(z) = 1 on the unit-norm
+ * scale) is applied before the T iterations, else the step is the identity.
+ * Costs one extra Gram + update (+ power_iters passes over A_0); matrices run
+ * on the large path (the small-matrix path is bypassed).  fp32 calls and
+ * pe_muon_step ignore it.  Errors: PE_ERR_INVALID_ARG (NULL, power_iters < 0
+ * or > 1000).
+ */
+pe_status pe_set_spectrum_init(pe_ctx ctx, int power_iters);
 
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */

@@ -101,3 +101,69 @@ def muon_step(W, M, G, beta, lr, table, T):
     W = np.asarray(W, dtype=np.float64)
     Mt = beta * np.asarray(M, dtype=np.float64) + (1.0 - beta) * np.asarray(G, dtype=np.float64)
     return W - lr * polar_express(Mt, table, T), Mt
+
+
+# ---------------------------------------------------------------- App. G
+INIT_Z_MIN = 1.0 / np.sqrt(2.0)     # P:1252 "the intervals do not overlap ... z >= 1/sqrt(2)"
+INIT_Z_MAX = 1.0 - 1e-6             # reading R17: numerically rank one -> no init
+INIT_SAFETY = 2.0 ** -7             # reading R17: p_G = p / (1 + |b| 2^-7), see spectrum_init
+
+
+def power_start(m):
+    """The deterministic power-method start vector both sides generate
+    (counter based, reading R17): v0_i = frac((i + 1) * phi^-1) + 0.5."""
+    i = np.arange(m, dtype=np.float64)
+    return np.mod((i + 1) * 0.6180339887498949, 1.0) + 0.5
+
+
+def init_cubic(z):
+    """eq. (init_poly): the odd cubic p(x) = a x + b x^3 with
+    p(sqrt(1 - z^2)) = p(z) = 1, for ||M||_F = 1 and sigma_1 in [z, 1]."""
+    t = np.sqrt(1.0 - z * z)
+    den = z * t * (2.0 * z * z - 1.0)
+    return (z * z * (z + t) - t) / den, (t - z) / den
+
+
+def spectrum_init(X, power_iters):
+    """App. G, k = 1: for the normalised iterate X (Listing 2's
+    X_0, ||X||_F = F), estimate z = sigma~_1 / F from below by the power
+    method on A = X X^T (the k = 1 case of the footnote's subspace iteration,
+    P:1237-1239: Rayleigh quotient of the last vector, sigma~_1 <= sigma_1),
+    and if 1/sqrt(2) <= z apply p(x) = a (x/F) + b (x/F)^3 with
+    (a, b) = init_cubic(z) (eq. init_poly), i.e. X <- (a/F) X + (b/F^3) A X,
+    divided by 1 + |b| 2^-7 (reading R17: as z -> 1, |a| ~ |b| ~ 1/sqrt(1-z^2)
+    and p(sigma_1) = a sigma_1 + b sigma_1^3 is a cancellation whose bf16
+    error ~ |b| 2^-8 would push sigma_1 past the 1.01 margin the Polar Express
+    table allows; the scale keeps p <= 1 under that error, and the GPU path
+    computes the same step).  Returns (X', z, applied)."""
+    X = np.asarray(X, dtype=np.float64)
+    F = np.sqrt(np.sum(X * X))
+    A = X @ X.T
+    v = power_start(A.shape[0])
+    lam = 0.0
+    for _ in range(power_iters):
+        w = A @ v
+        lam = float(v @ w) / float(v @ v)          # Rayleigh quotient <= lambda_max(A)
+        v = w / np.sqrt(float(w @ w))
+    z = np.sqrt(max(lam, 0.0)) / F if F > 0 else 0.0
+    if not (INIT_Z_MIN <= z <= INIT_Z_MAX):
+        return X, z, False
+    a, b = init_cubic(z)
+    sc = 1.0 / (1.0 + abs(b) * INIT_SAFETY)
+    return (a * sc / F) * X + (b * sc / F ** 3) * (A @ X), z, True
+
+
+def polar_express_init(M, table, T, power_iters=8, norm="listing2"):
+    """Polar Express with App. G's spectrum-aware first step: normalise and
+    orient as Listing 2, apply ``spectrum_init``,
+    then the T Listing 2 iterations, transpose back."""
+    M = np.asarray(M, dtype=np.float64)
+    tall = M.shape[0] > M.shape[1]
+    X = M.T if tall else M
+    X = normalize(X, norm)
+    X, z, applied = spectrum_init(X, power_iters)
+    for tup in schedule(table, T):
+        A = X @ X.T
+        a, b, c = tup
+        X = a * X + (b * A + c * (A @ A)) @ X
+    return (X.T if tall else X), z, applied

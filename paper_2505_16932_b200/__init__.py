@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = [
     "pe_create", "pe_destroy", "pe_set_coeffs", "pe_reserve", "pe_polar", "pe_polar_host",
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
-    "pe_comm_info", "pe_polar_sharded", "pe_polar_ex",
+    "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -75,6 +75,7 @@ def lib():
         "pe_polar": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
         "pe_polar_host": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
         "pe_polar_ex": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, I, I, P]),
+        "pe_set_spectrum_init": (I, [P, I]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -205,6 +206,11 @@ class Context:
         flat = [float(v) for t in tuples for v in t]
         arr = (ctypes.c_double * len(flat))(*flat)
         _check(lib().pe_set_coeffs(self._h, arr, len(tuples), deg), "pe_set_coeffs")
+
+    def set_spectrum_init(self, power_iters):
+        """pe_set_spectrum_init: App. G's spectrum-aware first step with
+        `power_iters` power-method steps (0 = off)."""
+        _check(lib().pe_set_spectrum_init(self._h, int(power_iters)), "pe_set_spectrum_init")
 
     def reserve(self, shapes, dtype=PE_BF16):
         _check(lib().pe_reserve(self._h, _shapes_arr(shapes), len(shapes), int(dtype)), "pe_reserve")

@@ -52,6 +52,7 @@ struct NormArgs {
   float beta, omb;             // fp32(beta), fp32(1 - beta)
   double* sums;                // sharded calls: write the local sum of squares here instead of inv
   int nblk;                    // chunks in total (the grid is persistent: block b takes chunks b, b + grid, ...)
+  double* ssq;                 // spectrum-aware init: per matrix sum of squares, or nullptr
 };
 
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
@@ -162,6 +163,7 @@ __device__ __forceinline__ void norm_chunk(const NormArgs& a, const int blk) {
     const int first = blk - ci;
     double s = 0.0;
     for (int k = 0; k < a.nchunks[mat]; ++k) s += *(volatile double*)&a.partials[first + k];
+    if (a.ssq != nullptr) a.ssq[mat] = s;
     if (a.sums != nullptr) {
       a.sums[mat] = s;                             // all-reduced by the caller, then pe_inv_kernel
     } else {
@@ -461,6 +463,200 @@ __global__ void __launch_bounds__(256) pe_upload_kernel(const uint4* __restrict_
   // upload slot four calls back, the plan's workspace -- they reuse).
   pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------- App. G
+// Spectrum-aware first step (k = 1; reading R17): the power
+// method on A_0 = X_0 X_0^T (the iteration-1 Gram, bf16, upper 256-block
+// triangle stored) gives the Rayleigh quotient lambda <= sigma_1(X_0)^2, hence
+// z = sqrt(lambda) / F with F = ||X_0||_F; if 1/sqrt(2) <= z <= 1 - 1e-6 the
+// first step applies p(x) = [a (x/F) + b (x/F)^3] / (1 + |b| 2^-7), (a, b)
+// from eq. (init_poly), as B = (b'/F^3) A_0 and
+// X_1 = (a'/F) X_0 + B X_0 through the poly and update GEMMs; otherwise
+// (a, b) = (1, 0).
+constexpr int kSymvRows = 32;        // rows of A per work item (one per lane)
+constexpr int kSymvThreads = 256;
+
+struct SymvArgs {
+  const MatDev* mats;
+  const int* item_mat;       // per item: matrix
+  const int* item_r0;        // per item: first row
+  int nitems;
+  const int* item0;          // per matrix: first item
+  const int* nitem;          // per matrix: items
+  const int64_t* voff;       // per matrix: offset of its vector (floats)
+  const float* vin;          // previous w (nullptr: first iteration, v = v0)
+  const double* nrm2_in;     // ||previous w||^2 per matrix (normalises vin)
+  float* wout;               // A v
+  double* part;              // per item: v.w, w.w, v.v over its rows
+  unsigned* counters;        // per matrix, zero at rest (self-resetting)
+  double* lam;               // per matrix: v.w / v.v
+  double* nrm2_out;          // per matrix: w.w
+};
+
+// v0_i = frac((i + 1) / phi) + 0.5 (the oracle's power_start, same counter)
+__device__ __forceinline__ float power_v0(int i) {
+  const double x = (double)(i + 1) * 0.6180339887498949;
+  return (float)(x - floor(x) + 0.5);
+}
+
+// w = A v for every matrix (one launch per power iteration).  A(r, c) with
+// c's 256-block left of r's is read from the stored transposed block as
+// A[c][r0 .. r0+31] (4 lanes x 16 bytes per column, 8 columns per warp
+// instruction), the rest row-wise as A[r][c .. c+7] (16 bytes per lane).
+__device__ __forceinline__ void symv_v8(const float* vin, float vs, int c, int m, float* v) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = (c + k < m) ? (vin ? vin[c + k] * vs : power_v0(c + k)) : 0.f;
+}
+
+__global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int kW = kSymvThreads / 32;
+  __shared__ float lpart[kW][kSymvRows];
+  __shared__ float upart[kSymvRows];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+    const int mat = a.item_mat[it], r0 = a.item_r0[it];
+    const MatDev md = a.mats[mat];
+    const int m = md.m, ld = md.ldm;
+    const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(md.A);
+    const float* vin = a.vin ? a.vin + a.voff[mat] : nullptr;
+    const float vs = vin ? (float)(1.0 / sqrt(a.nrm2_in[mat])) : 1.0f;
+    auto v_at = [&](int c) { return vin ? vin[c] * vs : power_v0(c); };
+    const int cl = (r0 / 256) * 256;                 // columns [0, cl): transposed stored blocks
+    // part L: lane = (column offset lane / 4, row segment lane % 4 of 8 rows)
+    {
+      const int seg = lane & 3, rs = r0 + seg * 8;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const bool full = rs + 8 <= m;
+      for (int c = warp * 8 + (lane >> 2); c < cl; c += kW * 8) {
+        const float vc = v_at(c);
+        const __nv_bfloat16* p = A + (size_t)c * ld + rs;
+        if (full) {
+          const uint4 u = *reinterpret_cast<const uint4*>(p);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(h[q]);
+            acc[2 * q] += f.x * vc;
+            acc[2 * q + 1] += f.y * vc;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (rs + k < m) acc[k] += __bfloat162float(p[k]) * vc;
+        }
+      }
+      // lanes with the same segment hold the same rows: reduce over lane / 4
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+      }
+      if (lane < 4) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lpart[warp][lane * 8 + k] = acc[k];
+      }
+    }
+    // part U: warp w takes rows r0 + 4w .. r0 + 4w + 3, 16 bytes of a row per lane
+#pragma unroll 1
+    for (int q = 0; q < kSymvRows / kW; ++q) {
+      const int rr = r0 + warp * (kSymvRows / kW) + q;
+      float acc = 0.f;
+      if (rr < m) {
+        const __nv_bfloat16* row = A + (size_t)rr * ld;
+        for (int c = cl + 8 * lane; c < m; c += 256) {
+          float v[8];
+          symv_v8(vin, vs, c, m, v);
+          if (c + 8 <= m) {
+            const uint4 u = *reinterpret_cast<const uint4*>(row + c);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __bfloat1622float2(h[k]);
+              acc += f.x * v[2 * k] + f.y * v[2 * k + 1];
+            }
+          } else {
+            for (int k = 0; k < 8 && c + k < m; ++k) acc += __bfloat162float(row[c + k]) * v[k];
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) upart[rr - r0] = acc;
+    }
+    __syncthreads();
+    double vw = 0.0, ww = 0.0, vv = 0.0;
+    if (warp == 0) {
+      const int r = r0 + lane;
+      float w = upart[lane];
+      for (int k = 0; k < kW; ++k) w += lpart[k][lane];
+      if (r < m) {
+        a.wout[a.voff[mat] + r] = w;
+        const float vr = v_at(r);
+        vw = (double)vr * w;
+        ww = (double)w * w;
+        vv = (double)vr * vr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        vw += __shfl_xor_sync(0xffffffffu, vw, o);
+        ww += __shfl_xor_sync(0xffffffffu, ww, o);
+        vv += __shfl_xor_sync(0xffffffffu, vv, o);
+      }
+      if (lane == 0) {
+        a.part[3 * it] = vw;
+        a.part[3 * it + 1] = ww;
+        a.part[3 * it + 2] = vv;
+        __threadfence();
+        const unsigned prev = atomicAdd(&a.counters[mat], 1u);
+        last = (prev + 1 == (unsigned)a.nitem[mat]);
+      }
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      double svw = 0.0, sww = 0.0, svv = 0.0;        // items of the matrix in order (deterministic)
+      for (int k = a.item0[mat]; k < a.item0[mat] + a.nitem[mat]; ++k) {
+        svw += *(volatile double*)&a.part[3 * k];
+        sww += *(volatile double*)&a.part[3 * k + 1];
+        svv += *(volatile double*)&a.part[3 * k + 2];
+      }
+      a.lam[mat] = svv > 0.0 ? svw / svv : 0.0;
+      a.nrm2_out[mat] = sww;
+      a.counters[mat] = 0u;
+    }
+    __syncthreads();
+  }
+}
+
+// Per matrix: z = sqrt(lambda / F^2), F^2 = ssq * inv^2 (= ||X_0||_F^2), and
+// the first step's (a/F, b/F^3) from eq. (init_poly), or (1, 0).
+__global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const float* inv, float* mcoef,
+                                    int count) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double f2 = ssq[i] * (double)inv[i] * (double)inv[i];
+  const double z = (f2 > 0.0 && lam[i] > 0.0) ? sqrt(lam[i] / f2) : 0.0;
+  float ca = 1.f, cb = 0.f;
+  if (z >= 0.70710678118654752 && z <= 1.0 - 1e-6) {
+    const double t = sqrt(1.0 - z * z);
+    const double den = z * t * (2.0 * z * z - 1.0);
+    const double F = sqrt(f2);
+    const double a = (z * z * (z + t) - t) / den, b = (t - z) / den;
+    // reading R17: divide by 1 + |b| 2^-7 -- p(sigma_1) = a s + b s^3 cancels
+    // (|a| ~ |b| ~ 1/t as z -> 1), and its bf16 error ~ |b| 2^-8 must not push
+    // sigma_1 past the table's 1.01 margin (unscaled: NaN at z = 0.9995)
+    const double sc = 1.0 / (1.0 + fabs(b) * 0.0078125);
+    ca = (float)(a * sc / F);
+    cb = (float)(b * sc / (F * F * F));
+  }
+  mcoef[2 * i] = ca;
+  mcoef[2 * i + 1] = cb;
 }
 
 }  // namespace pe

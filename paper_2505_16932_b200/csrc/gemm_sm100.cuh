@@ -98,6 +98,7 @@ struct GemmArgs {
   const float* coef;           // per iteration fp32 (a, b, c)
   int* done;                   // per (matrix, phase) completion counters, zero at launch
   const int* need;             // per (matrix, mode): 2 * kEpiWarps * tiles
+  const float* mcoef;          // spectrum-aware first step (App. G): per matrix (a, b), c = 0; else nullptr
   int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
                                // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
                                // stores, 256 = every result store to the same box, 2048 = right
@@ -169,6 +170,11 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.a = g.a;
     c.b = g.b;
     c.c = g.c;
+    if (g.mcoef != nullptr) {              // App. G first step: p(x) = a x + b x^3 per matrix
+      c.a = g.mcoef[2 * tl.mat];
+      c.b = g.mcoef[2 * tl.mat + 1];
+      c.c = 0.f;
+    }
   }
   const int fl = kEdge ? g.mflags[tl.mat] : 0;
   const bool fold = kEdge && c.first && (fl & kFlagFolded);

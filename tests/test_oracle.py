@@ -501,3 +501,69 @@ def test_coefficients_against_60_digit_replay():
             assert abs(float(hv) - ov) <= tol * abs(float(hv)), (t, float(hv), ov)
             if t < 7:
                 assert abs(float(hv) - pv) <= max(tol, 1e-13) * abs(float(hv)) + 1e-14, (t, float(hv), pv)
+
+
+# ---------------------------------------------------------------- App. G
+def test_init_cubic_interpolates_and_bounds():
+    """eq. (init_poly) (P:1256-1259): p(sqrt(1-z^2)) = p(z) = 1; p(1) > 1/sqrt(2)
+    (P:1262); p <= 1 on [0, sqrt(1-z^2)] and p([z, 1]) within [p(1), 1]
+    (P:1260-1261), for z over [1/sqrt(2), 1)."""
+    for z in np.linspace(0.7072, 0.99995, 60):
+        a, b = oi.init_cubic(z)
+        t = np.sqrt(1 - z * z)
+        p = lambda x: a * x + b * x ** 3          # noqa: E731
+        assert abs(p(t) - 1) < 1e-9 and abs(p(z) - 1) < 1e-9, z
+        assert p(1.0) > 1 / np.sqrt(2)
+        lo = np.linspace(0, t, 200)
+        assert np.all(p(lo) <= 1 + 1e-9) and np.all(np.diff(p(lo)) >= -1e-12)      # concave-increasing
+        hi = np.linspace(z, 1, 200)
+        assert np.all(p(hi) <= 1 + 1e-9) and np.all(p(hi) >= p(1.0) - 1e-12)
+
+
+def test_spectrum_init_is_the_scalar_map_and_a_lower_bound():
+    """spectrum_init(X) = U p(Sigma/F) V^T / (1 + |b| 2^-7) with p from the z it
+    found (matrix function, via an independent SVD route; R17's
+    scale); z <= sigma_1 / F (Rayleigh
+    quotient bound) and -> sigma_1 / F as the power method
+    converges; no gap (Gaussian, z < 1/sqrt(2)) leaves X unchanged."""
+    rng = np.random.default_rng(5)
+    U, _ = np.linalg.qr(rng.standard_normal((40, 40)))
+    V, _ = np.linalg.qr(rng.standard_normal((90, 40)))
+    s = np.concatenate([[1.0], np.geomspace(0.2, 1e-3, 39)])
+    X = (U * s) @ V.T * 0.37
+    F = np.sqrt(np.sum(X * X))
+    zs = []
+    for q in (1, 2, 4, 8, 30):
+        Y, z, applied = oi.spectrum_init(X, q)
+        zs.append(z)
+        assert z <= s[0] * 0.37 / F + 1e-12
+        assert applied == (z >= 1 / np.sqrt(2)) and (applied or q < 8)
+        if not applied:
+            assert np.array_equal(Y, X)
+            continue
+        a, b = oi.init_cubic(z)
+        sc = 1.0 / (1.0 + abs(b) * 2.0 ** -7)        # reading R17's margin for the bf16 cancellation
+        sh = s * 0.37 / F
+        ref = (U * (sc * (a * sh + b * sh ** 3))) @ V.T
+        assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
+        assert np.linalg.svd(Y, compute_uv=False)[0] <= 1 + 1e-9
+    assert zs == sorted(zs) and abs(zs[-1] - s[0] * 0.37 / F) < 1e-12
+    G = rng.standard_normal((64, 128))
+    Y, z, applied = oi.spectrum_init(G, 8)
+    assert not applied and z < 1 / np.sqrt(2) and np.array_equal(Y, G)
+
+
+def test_spectrum_init_speeds_up_power_law_spectrum():
+    """App. G's figure claim: on a 32 x 32 matrix with
+    sigma_j = j^-5, the spectrum-aware step followed by T-1 Polar Express
+    iterations beats T Polar Express iterations (the step counted as one)."""
+    rng = np.random.default_rng(0)
+    U, _ = np.linalg.qr(rng.standard_normal((32, 32)))
+    V, _ = np.linalg.qr(rng.standard_normal((32, 32)))
+    M = (U * np.arange(1, 33) ** -5.0) @ V.T
+    P = oi.exact_polar(M)
+    table, _ = oc.pe_coeffs(1e-3, 5, 8, 1.01)
+    for T in range(3, 8):
+        plain = om.rel_frobenius(oi.polar_express(M, table, T), P)
+        X, z, applied = oi.polar_express_init(M, table, T - 1)
+        assert applied and om.rel_frobenius(X, P) < plain - 1e-3, (T, plain)
