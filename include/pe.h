@@ -232,8 +232,11 @@ pe_status pe_muon_step(pe_ctx ctx, void* const* W, void* const* M, const void* c
  * all-reduce over all ranks of `count` elements (dtype 0 = fp32, 1 = fp64)
  * of device buffer `buf`, enqueued on `stream` (e.g. ncclAllReduce); called
  * 1 + iters times per call, from the calling thread, between kernel
- * launches; return PE_OK or an error, which aborts the call.
- * Errors: PE_ERR_INVALID_ARG, PE_ERR_UNSUPPORTED (cols % 8 != 0, capture),
+ * launches; return PE_OK or an error, which aborts the call.  allreduce =
+ * NULL uses the context's own communicator (pe_attach_comm): an in-place
+ * ncclAllReduce (SUM) on `stream`; `user` is then ignored.
+ * Errors: PE_ERR_INVALID_ARG (also: NULL allreduce without a communicator),
+ * PE_ERR_UNSUPPORTED (cols % 8 != 0, capture),
  * PE_ERR_WORKSPACE, PE_ERR_CUDA, or the callback's status.
  */
 typedef pe_status (*pe_allreduce_fn)(void* buf, int64_t count, int dtype, void* user, void* stream);

@@ -305,12 +305,13 @@ class Context:
                                   ctypes.c_void_p(stream.cuda_stream)), "pe_muon_step")
         return weights
 
-    def polar_split(self, shard, allreduce, out=None, iters=5, stream=None):
+    def polar_split(self, shard, allreduce=None, out=None, iters=5, stream=None):
         """pe_polar_split: `shard` is this rank's column block M_r (rows x
         cols_r, bf16, cols_r % 8 == 0) of one wide matrix M = [M_0 | M_1 | ...];
         returns the same columns of polar(M).  `allreduce(t)` must sum the CUDA
         tensor `t` in place over all ranks, on the current stream (e.g.
-        torch.distributed.all_reduce)."""
+        torch.distributed.all_reduce); None uses the context's own NCCL
+        communicator (attach_comm)."""
         import torch
         if shard.dim() != 2 or not shard.is_contiguous() or not shard.is_cuda or shard.dtype != torch.bfloat16:
             raise ValueError("polar_split takes a contiguous 2-D bf16 CUDA tensor")
@@ -323,14 +324,14 @@ class Context:
         def cb(buf, count, dtype, user, st):
             try:
                 t = torch.as_tensor(_DevBuf(buf, count, "<f4" if dtype == 0 else "<f8"), device=shard.device)
-                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=shard.device)):
+                with torch.cuda.stream(torch.cuda.ExternalStream(st or 0, device=shard.device)):
                     allreduce(t)
                 return 0
             except Exception as e:          # reported after the call returns
                 errors.append(e)
                 return 5                    # PE_ERR_NCCL
 
-        fn = ALLREDUCE_FN(cb)
+        fn = ALLREDUCE_FN(cb) if allreduce is not None else ALLREDUCE_FN()
         status = lib().pe_polar_split(self._h, ctypes.c_void_p(shard.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                         int(shard.shape[0]), int(shard.shape[1]), int(iters), fn, None,
                                         ctypes.c_void_p(stream.cuda_stream))

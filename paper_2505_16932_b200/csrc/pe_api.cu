@@ -1408,7 +1408,15 @@ extern "C" pe_status pe_polar_ex(pe_ctx c, const void* const* in, void* const* o
 
 extern "C" pe_status pe_polar_split(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,
                                       pe_allreduce_fn allreduce, void* user, void* stream) {
-  if (!c || !in || !out || !allreduce || iters < 1) return PE_ERR_INVALID_ARG;
+  if (!c || !in || !out || iters < 1) return PE_ERR_INVALID_ARG;
+  if (!allreduce) {                      // the context's own communicator (pe_attach_comm)
+    if (!pe_ctx_dist(c)) {
+      g_last_error = "pe_polar_split: no allreduce callback and no communicator (pe_attach_comm)";
+      return PE_ERR_INVALID_ARG;
+    }
+    allreduce = pe_comm_allreduce;
+    user = c;
+  }
   const int64_t shp[2] = {rows, cols};
   const void* ins[1] = {in};
   void* outs[1] = {out};

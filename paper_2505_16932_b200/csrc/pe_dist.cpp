@@ -39,6 +39,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclCommGetAsyncError) commGetAsyncError = nullptr;
   decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) getErrorString = nullptr;
@@ -70,6 +71,7 @@ NcclApi* nccl() {
   api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
   api.commGetAsyncError = reinterpret_cast<decltype(api.commGetAsyncError)>(sym("ncclCommGetAsyncError"));
   api.broadcast = reinterpret_cast<decltype(api.broadcast)>(sym("ncclBroadcast"));
+  api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
   api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
   api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
   api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(sym("ncclGetErrorString"));
@@ -286,4 +288,20 @@ extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* con
   }
   pe_ctx_set_launches(c, launches);
   return PE_OK;
+}
+
+// pe_polar_split's all-reduce when the caller passes none: an in-place
+// ncclAllReduce (SUM) over the context's communicator, on the call's stream.
+extern "C" __attribute__((visibility("hidden"))) pe_status pe_comm_allreduce(void* buf, int64_t count, int dtype,
+                                                                              void* user, void* stream) {
+  pe_ctx c = reinterpret_cast<pe_ctx>(user);
+  PeDist* d = c ? pe_ctx_dist(c) : nullptr;
+  NcclApi* api = nccl();
+  if (!d || !api) {
+    pe_set_error("pe_polar_split: no allreduce callback and no communicator (pe_attach_comm)");
+    return PE_ERR_INVALID_ARG;
+  }
+  const ncclResult_t r = api->allReduce(buf, buf, (size_t)count, dtype == 0 ? ncclFloat32 : ncclFloat64, ncclSum,
+                                        d->comm, reinterpret_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? PE_OK : nccl_fail(api, r, "ncclAllReduce");
 }

@@ -13,3 +13,7 @@ int pe_ctx_device(pe_ctx c);
 void pe_ctx_set_launches(pe_ctx c, int n);   // what pe_last_launch_count reports
 void pe_set_error(const char* msg);          // pe_last_error_message of this thread
 void pe_dist_free(PeDist* d);                // called by pe_destroy
+// pe_polar_split's default all-reduce (user = the context): ncclAllReduce SUM
+// over the context's communicator, on `stream`
+extern "C" __attribute__((visibility("hidden"))) pe_status pe_comm_allreduce(void* buf, int64_t count, int dtype,
+                                                                              void* user, void* stream);

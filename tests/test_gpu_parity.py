@@ -1126,3 +1126,26 @@ def test_spectrum_init_helps_on_power_law(shape, law):
         assert applied and e_fast < e_plain - 0.05, (T, e_fast, e_plain)
         assert e_fast <= e_ref + 2e-2, (T, e_fast, e_ref)
     c.close()
+
+
+def test_polar_split_with_library_communicator():
+    """pe_polar_split with allreduce = NULL uses the context's own NCCL
+    communicator (a 1-rank one here, where the all-reduce is the identity):
+    the whole matrix as one column block equals the callback path (a no-op
+    callback) bit for bit and matches pe_polar within 1e-2; without a
+    communicator the NULL callback is refused."""
+    c = pe.Context(0)
+    M = bf16_values(syn.gaussian(384, 1536, seed=612, std=0.02))
+    x = to_dev_bf16(M)
+    with pytest.raises(pe.PeError):
+        c.polar_split(x)
+    via_cb = c.polar_split(x, lambda t: None, iters=5)
+    c.attach_comm(pe.pe_nccl_unique_id(), 0, 1)
+    via_nccl = c.polar_split(x, iters=5)
+    full = c.polar([x], iters=5)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(via_cb.view(torch.int16), via_nccl.view(torch.int16))
+    X = via_nccl.float().cpu().numpy().astype(np.float64)
+    assert om.rel_frobenius(X, full.float().cpu().numpy().astype(np.float64)) <= 1e-2
+    check_g1_g3(X, M)
+    c.close()
