@@ -379,6 +379,40 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
             del gr
         except Exception as e:                       # reported, not fatal
             graph_ms = str(e)[:200]
+    if dist_on and world > 1:
+        # SURVEY §8(d) multi-GPU: the compute span (this rank's pe_polar on its
+        # share) and the exchange span in isolation (one NCCL broadcast per
+        # matrix from its owner, through torch.distributed on the same
+        # buffers), next to the overlapped pe_polar_sharded step above
+        ys_own = [ys[i] for i in idx]
+
+        def span(fn, reps=max(3, steps)):
+            out = []
+            for _ in range(reps):
+                torch.distributed.barrier()
+                torch.cuda.synchronize(device)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize(device)
+                out.append(a.elapsed_time(b))
+            t = torch.tensor([sorted(out)[len(out) // 2]], device=device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return round(float(t.item()), 4)
+
+        def exchange():
+            works = [torch.distributed.broadcast(y, src=owner[i], async_op=True) for i, y in enumerate(ys)]
+            for w in works:
+                w.wait()
+
+        try:
+            graph_ms = {"compute_ms": span(lambda: ctx.polar(xs, ys_own, iters=T, stream=stream)),
+                        "exchange_ms": span(exchange),
+                        "note": "max over ranks of the median; exchange = one torch.distributed NCCL broadcast "
+                                "per matrix (not grouped); the timed step overlaps compute and exchange"}
+        except Exception as e:                       # reported, never fatal
+            graph_ms = {"error": str(e)[:200]}
     return ms, prof, launches, idx, xs, ys, graph_ms
 
 
@@ -467,7 +501,8 @@ def main():
         "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
         "ms_per_step_stats": pctl(ms),
-        "graph_replay": (pctl(graph_ms) if isinstance(graph_ms, list) else graph_ms),
+        "graph_replay": (pctl(graph_ms) if isinstance(graph_ms, list) else (None if world > 1 else graph_ms)),
+        "multi_gpu_spans": graph_ms if world > 1 else None,
         "norm_pass": norm_gbs(prof, [shapes[i] for i in idx], args.steps, peaks),
     }
 
