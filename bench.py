@@ -492,6 +492,8 @@ def main():
                    "parallelism": f"dp{world} (pe_polar_sharded: LPT shard + bucketed NCCL broadcasts)" if world > 1 else "single GPU"},
         "tflops": round(tflops, 2), "tflops_unit": "TFLOP/s (algorithmic, symmetric-aware)",
         "frac_of_bf16_peak": round(tflops / peaks[peak_key], 4),
+        "frac_of_bf16_peak_sustained": round(tflops / peaks["bf16_tflops_sustained"], 4),
+        "layer_sets_per_s": round(1e3 / mean_ms, 3),
         "peak_used": f"{peaks[peak_key]} TFLOP/s ({src} {'sustained' if peak_key.endswith('sustained') else 'burst'})",
         "e2e": {"value": round(len(shapes) / (e2e_mean * 1e-3), 3), "unit": UNIT,
                 "ms_per_step": round(e2e_mean, 3),
