@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
       const int seg = lane & 3, rs = r0 + seg * 8;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const bool full = rs + 8 <= m;
+#pragma unroll 4
       for (int c = warp * 8 + (lane >> 2); c < cl; c += kW * 8) {
         const float vc = v_at(c);
         const __nv_bfloat16* p = A + (size_t)c * ld + rs;
@@ -561,12 +562,13 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
       }
     }
     // part U: warp w takes rows r0 + 4w .. r0 + 4w + 3, 16 bytes of a row per lane
-#pragma unroll 1
+#pragma unroll
     for (int q = 0; q < kSymvRows / kW; ++q) {
       const int rr = r0 + warp * (kSymvRows / kW) + q;
       float acc = 0.f;
       if (rr < m) {
         const __nv_bfloat16* row = A + (size_t)rr * ld;
+#pragma unroll 4
         for (int c = cl + 8 * lane; c < m; c += 256) {
           float v[8];
           symv_v8(vin, vs, c, m, v);
