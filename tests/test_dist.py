@@ -1,6 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world size 2): every rank computes the
-same LPT shard plan (pe_shard_plan), owns a disjoint subset, and the
-all-gather leaves every rank with every matrix's bytes."""
+same LPT shard plan (pe_shard_plan) and exchange buckets (pe_shard_buckets),
+owns a disjoint subset, and both the torch-level all-gather and a replay of
+pe_polar_sharded's per-bucket owner broadcasts leave every rank with every
+matrix's bytes."""
 import os
 import socket
 
@@ -50,7 +52,24 @@ def _worker(rank, world, port, q):
             ok = ok and torch.equal(views[i], exp) and (views[i].data_ptr() - gp.recv.data_ptr()) % 256 == 0
         plans = [None] * world
         dist.all_gather_object(plans, owner)
-        q.put((rank, ok, all(p == owner for p in plans), sorted(idx)))
+        # pe_polar_sharded's exchange schedule (pe_dist.cpp), replayed with
+        # gloo: buckets from pe_shard_buckets (identical on every rank), each
+        # matrix broadcast from its pe_shard_plan owner into every rank's output
+        from paper_2505_16932_b200 import pe_shard_buckets
+        beg = pe_shard_buckets(shapes, 4)
+        begs = [None] * world
+        dist.all_gather_object(begs, beg)
+        outs = [torch.zeros(r * c, dtype=torch.bfloat16) for r, c in shapes]
+        for i in idx:
+            r, c = shapes[i]
+            outs[i].copy_((torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16))
+        for b in range(4):
+            for i in range(beg[b], beg[b + 1]):
+                dist.broadcast(outs[i], src=owner[i])
+        for i, (r, c) in enumerate(shapes):
+            ok = ok and torch.equal(outs[i], (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16))
+        same = all(p == owner for p in plans) and all(bb == beg for bb in begs)
+        q.put((rank, ok, same, sorted(idx)))
     finally:
         dist.destroy_process_group()
 
