@@ -485,8 +485,8 @@ struct SymvArgs {
   const int* item0;          // per matrix: first item
   const int* nitem;          // per matrix: items
   const int64_t* voff;       // per matrix: offset of its vector (floats)
-  const float* vin;          // previous w (nullptr: first iteration, v = v0)
-  const double* nrm2_in;     // ||previous w||^2 per matrix (normalises vin)
+  const float* vin;          // previous w, or the start vector v0 in the first iteration
+  const double* nrm2_in;     // ||previous w||^2 per matrix (normalises vin); nullptr: vin is v0
   float* wout;               // A v
   double* part;              // per item: v.w, w.w, v.v over its rows
   unsigned* counters;        // per matrix, zero at rest (self-resetting)
@@ -494,19 +494,20 @@ struct SymvArgs {
   double* nrm2_out;          // per matrix: w.w
 };
 
-// v0_i = frac((i + 1) / phi) + 0.5 (the oracle's power_start, same counter)
-__device__ __forceinline__ float power_v0(int i) {
-  const double x = (double)(i + 1) * 0.6180339887498949;
-  return (float)(x - floor(x) + 0.5);
-}
-
 // w = A v for every matrix (one launch per power iteration).  A(r, c) with
 // c's 256-block left of r's is read from the stored transposed block as
 // A[c][r0 .. r0+31] (4 lanes x 16 bytes per column, 8 columns per warp
 // instruction), the rest row-wise as A[r][c .. c+7] (16 bytes per lane).
 __device__ __forceinline__ void symv_v8(const float* vin, float vs, int c, int m, float* v) {
+  if (c + 8 <= m) {                                  // vin + c is 32-byte aligned (voff % 32 == 0, c % 8 == 0)
+    const float4 p = *reinterpret_cast<const float4*>(vin + c);
+    const float4 q = *reinterpret_cast<const float4*>(vin + c + 4);
+    v[0] = p.x * vs; v[1] = p.y * vs; v[2] = p.z * vs; v[3] = p.w * vs;
+    v[4] = q.x * vs; v[5] = q.y * vs; v[6] = q.z * vs; v[7] = q.w * vs;
+  } else {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = (c + k < m) ? (vin ? vin[c + k] * vs : power_v0(c + k)) : 0.f;
+    for (int k = 0; k < 8; ++k) v[k] = (c + k < m) ? vin[c + k] * vs : 0.f;
+  }
 }
 
 __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a) {
@@ -522,9 +523,9 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
     const MatDev md = a.mats[mat];
     const int m = md.m, ld = md.ldm;
     const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(md.A);
-    const float* vin = a.vin ? a.vin + a.voff[mat] : nullptr;
-    const float vs = vin ? (float)(1.0 / sqrt(a.nrm2_in[mat])) : 1.0f;
-    auto v_at = [&](int c) { return vin ? vin[c] * vs : power_v0(c); };
+    const float* vin = a.vin + a.voff[mat];          // iteration 0: the start vector v0 (unnormalised)
+    const float vs = a.nrm2_in ? (float)(1.0 / sqrt(a.nrm2_in[mat])) : 1.0f;
+    auto v_at = [&](int c) { return vin[c] * vs; };
     const int cl = (r0 / 256) * 256;                 // columns [0, cl): transposed stored blocks
     // part L: lane = (column offset lane / 4, row segment lane % 4 of 8 rows)
     {

@@ -153,7 +153,7 @@ struct Plan {
   // spectrum-aware first step (App. G, pe_set_spectrum_init): power-method
   // work items (matrix, 32 rows), vectors (two ping-pong sets of sum m floats),
   // per-item partials, per-matrix counters / lambda / ||w||^2 (x2) / sum of squares / (a, b)
-  size_t o_sitem_mat = 0, o_sitem_r0 = 0, o_sitem0 = 0, o_snitem = 0, o_svoff = 0, o_sv = 0, o_spart = 0;
+  size_t o_sitem_mat = 0, o_sitem_r0 = 0, o_sitem0 = 0, o_snitem = 0, o_svoff = 0, o_sv = 0, o_sv0 = 0, o_spart = 0;
   size_t o_scnt = 0, o_slam = 0, o_snrm = 0, o_sssq = 0, o_smcoef = 0;
   int n_sitems = 0;
   int64_t sv_len = 0;
@@ -707,6 +707,15 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     P->o_snitem = bl.add(ni);
     P->o_svoff = bl.add(voff);
     P->o_sv = bl.add(std::vector<float>(2 * (size_t)vlen, 0.f));
+    // the power method's start vector, v0_i = frac((i + 1) / phi) + 0.5 per
+    // matrix (the oracle's power_start, same counter; reading R17)
+    std::vector<float> v0((size_t)vlen, 0.f);
+    for (int i = 0; i < count; ++i)
+      for (int r = 0; r < mats[i].m; ++r) {
+        const double x = (double)(r + 1) * 0.6180339887498949;
+        v0[(size_t)voff[i] + r] = (float)(x - std::floor(x) + 0.5);
+      }
+    P->o_sv0 = bl.add(v0);
     P->o_spart = bl.add(std::vector<double>(3 * imat.size() + 3, 0.0));
     P->o_scnt = bl.add(std::vector<unsigned>(count, 0u));
     P->o_slam = bl.add(std::vector<double>(count, 0.0));
@@ -1348,8 +1357,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         double* nb = at<double>(P, P->o_snrm);
         const int sgrid = std::min(P->n_sitems, c->num_sms * 8);
         for (int k = 0; k < c->init_iters; ++k) {
-          sa.vin = (k == 0) ? nullptr : vb + (size_t)((k - 1) & 1) * P->sv_len;
-          sa.nrm2_in = nb + (size_t)((k - 1) & 1) * count;
+          sa.vin = (k == 0) ? at<float>(P, P->o_sv0) : vb + (size_t)((k - 1) & 1) * P->sv_len;
+          sa.nrm2_in = (k == 0) ? nullptr : nb + (size_t)((k - 1) & 1) * count;
           sa.wout = vb + (size_t)(k & 1) * P->sv_len;
           sa.nrm2_out = nb + (size_t)(k & 1) * count;
           launch(pe_symv_kernel, sgrid, kSymvThreads, 0, st, sa);
