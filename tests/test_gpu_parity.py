@@ -1177,3 +1177,34 @@ def test_spectrum_init_degenerate_inputs():
     ref, z, applied = oi.polar_express_init(row, TABLE, 5, power_iters=8)
     assert not applied and om.rel_frobenius(outs[2], ref) <= 1e-1
     c.close()
+
+
+def test_spectrum_init_with_polar_ex_and_graph():
+    """The App. G step composes with pe_polar_ex (fp32 momentum, R16's
+    explicit X_0) and with CUDA-graph capture: fp32 spiked input through
+    polar_ex matches the oracle on the fp32 values; a captured call replays
+    bit-identically to a direct one."""
+    c = pe.Context(0)
+    c.set_spectrum_init(4)
+    M = _spiked(384, 1024, seed=77).astype(np.float32)
+    x32 = torch.from_numpy(M).cuda()
+    y = c.polar_ex([x32], [torch.empty(M.shape, dtype=torch.bfloat16, device="cuda")], iters=6)[0]
+    torch.cuda.synchronize()
+    ref, z, applied = oi.polar_express_init(M.astype(np.float64), TABLE, 6, power_iters=4)
+    assert applied
+    assert om.rel_frobenius(y.float().cpu().numpy().astype(np.float64), ref) <= 2e-2
+    shapes = [(384, 1024), (1024, 384), (300, 700)]
+    xs = [to_dev_bf16(bf16_values(_spiked(*s_, seed=80 + i))) for i, s_ in enumerate(shapes)]
+    ys = [torch.empty_like(x) for x in xs]
+    c.reserve(shapes, pe.PE_BF16)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        c.polar(xs, ys, iters=5)
+    g.replay()
+    direct = c.polar(xs, iters=5)
+    torch.cuda.synchronize()
+    for a, b in zip(ys, direct):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    del g
+    c.close()
