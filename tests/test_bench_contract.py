@@ -1,0 +1,41 @@
+"""bench.py keeps the driver's contract: one JSON line with the required keys
+(reference arm on CPU; our arm on the GPU, short run)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches"}
+
+
+def _run(args, timeout):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], 600)
+    assert d["impl"] == "reference" and BASE_KEYS <= set(d)
+    assert d["unit"] == "matrices/s" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["config"]["workload"] == "gpt2-small"
+
+
+@pytest.mark.gpu
+def test_our_arm_line():
+    d = _run(["--steps", "2", "--warmup", "3", "--extra", "", "--no-cpu-baseline"], 900)
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["steps"] == 2 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["gpu_launches"] > 0 and d["dtype"] == "bf16"
+    assert d["roofline"]["bound"] == "tensor" and 0 < d["roofline"]["frac"] < 1
+    assert d["clocks"]["sm_max_mhz"] and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert len(d["ms_per_step_stats"]["all_ms"]) == 2
