@@ -61,7 +61,7 @@ __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const float2 f = __bfloat1622float2(h[q]);
-    acc += (double)(f.x * f.x) + (double)(f.y * f.y);   // bf16^2 is exact in fp32
+    acc += (double)f.x * f.x + (double)f.y * f.y;   // exact in fp64 (an fp32 square overflows past |x| ~ 1.8e19)
   }
   return acc;
 }
@@ -105,7 +105,7 @@ __device__ __forceinline__ void norm_chunk(const NormArgs& a, const int blk) {
         const __nv_bfloat16 v = upd(__bfloat162float(p[j]), __bfloat162float(gp[j]));
         p[j] = v;
         const float f = __bfloat162float(v);
-        acc += (double)(f * f);
+        acc += (double)f * f;
       }
   } else if (a.src_f32) {
     const float* p = reinterpret_cast<const float*>(a.srcs[mat]);
@@ -138,7 +138,7 @@ __device__ __forceinline__ void norm_chunk(const NormArgs& a, const int blk) {
     for (; i < end; i += kStride)
       for (int64_t j = i; j < min(i + 8, end); ++j) {
         const float f = __bfloat162float(p[j]);
-        acc += (double)(f * f);
+        acc += (double)f * f;
       }
   }
   // block reduction in a fixed order (deterministic)

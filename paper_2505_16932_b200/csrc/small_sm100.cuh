@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const float f = __bfloat162float(h[k]);
-            acc += (double)(f * f);
+            acc += (double)f * f;
             *reinterpret_cast<__nv_bfloat16*>(X + small_unit(roff + 8 * v + k, i >> 3) + col) = h[k];
           }
         }
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
 #pragma unroll
         for (int uu = 0; uu < 4; ++uu) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc += (kP == 1) ? (double)(f[uu][k] * f[uu][k]) : (double)f[uu][k] * f[uu][k];
+          for (int k = 0; k < 8; ++k) acc += (double)f[uu][k] * f[uu][k];
           if (fold && u0 + uu < nu && tid < m) small_store8<kP>(X, xplane, small_unit(roff + tid, u0 + uu), f[uu]);
         }
       }
@@ -341,13 +341,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
           float f[V];
           load_vec(row + (int64_t)jv * V, f);
 #pragma unroll
-          for (int k = 0; k < V; ++k) acc += (kP == 1) ? (double)(f[k] * f[k]) : (double)f[k] * f[k];
+          for (int k = 0; k < V; ++k) acc += (double)f[k] * f[k];
           if (fold)                                   // 8 columns of one row: one 16-byte unit
             *reinterpret_cast<uint4*>(X + small_unit(roff + i, jv)) =
                 __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.in) + row + jv * V));
         } else {
           const float v = load_one(row + jv);
-          acc += (kP == 1) ? (double)(v * v) : (double)v * v;
+          acc += (double)v * v;
           if (fold) put(i, jv, v);
         }
       }
