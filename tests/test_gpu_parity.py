@@ -1208,3 +1208,28 @@ def test_spectrum_init_with_polar_ex_and_graph():
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     del g
     c.close()
+
+
+def test_input_scale_range():
+    """Reading R18: Listing 2's +1e-7 makes tiny inputs scale-dependent and
+    the GPU follows the oracle there (entries ~1e-10); large inputs stay
+    scale-invariant on the fp32 path and on unfolded bf16 inputs (fp64 norm
+    squares), entries up to 1e30."""
+    rng = np.random.default_rng(9)
+    base = rng.standard_normal((256, 770))
+    c = pe.Context(0)
+    # tiny: the epsilon dominates s; GPU == oracle (both apply it)
+    for dt in ("f32", "bf16"):
+        M = base * 1e-10
+        M = M.astype(np.float32).astype(np.float64) if dt == "f32" else bf16_values(M)
+        X = run(c, [M], T=5, dtype=dt)[0]
+        ref = oi.polar_express(M, TABLE, 5)
+        assert om.rel_frobenius(X, ref) <= (1e-5 if dt == "f32" else 2e-2)
+    # huge: same result as at scale 1
+    for dt in ("f32", "bf16"):
+        M1 = base.astype(np.float32).astype(np.float64) if dt == "f32" else bf16_values(base)
+        X1 = run(c, [M1], T=5, dtype=dt)[0]
+        Mh = (base * 1e30).astype(np.float32).astype(np.float64) if dt == "f32" else bf16_values(base * 1e30)
+        Xh = run(c, [Mh], T=5, dtype=dt)[0]
+        assert np.all(np.isfinite(Xh)) and om.rel_frobenius(Xh, X1) <= (1e-5 if dt == "f32" else 2e-2)
+    c.close()
