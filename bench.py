@@ -236,7 +236,7 @@ def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
     from oracle import coeffs as oc, iteration as oi
     table, _ = oc.pe_coeffs(ELL, DEGREE, 8, 1.01)
     # sample: the first layer's matrices (or the first matrix for big sets)
-    nl = {"gpt2-small": 12, "gpt2-large": 36}.get(_workload_name[0], 32)
+    nl = {"gpt2-small": 12, "gpt2-small-fused": 12, "gpt2-large": 36}.get(_workload_name[0], 32)
     per_layer = max(1, len(shapes) // nl)
     sample = list(range(per_layer))
     if sum(min(shapes[i]) ** 2 * max(shapes[i]) for i in sample) > 4e11:

@@ -120,6 +120,10 @@ def diagonal(rows, cols, sigmas):
 LAYER_SETS = {
     # GPT-2 Small: d=768, 12 layers; q,k,v,o (768x768), c_fc 768x3072, c_proj 3072x768
     "gpt2-small": [(768, 768, 48), (768, 3072, 12), (3072, 768, 12)],
+    # GPT-2 Small with the fused attention projection as stored by GPT-2
+    # checkpoints (SURVEY §8d config 2 variant): c_attn 768x2304 (q,k,v),
+    # attn c_proj 768x768, c_fc 768x3072, mlp c_proj 3072x768 per layer
+    "gpt2-small-fused": [(768, 2304, 12), (768, 768, 12), (768, 3072, 12), (3072, 768, 12)],
     # GPT-2 Large: d=1280, 36 layers
     "gpt2-large": [(1280, 1280, 144), (1280, 5120, 36), (5120, 1280, 36)],
     # Llama-3-8B: q,o 4096^2; k,v 1024x4096 (GQA); gate,up 14336x4096; down 4096x14336
@@ -136,7 +140,7 @@ def layer_set_shapes(name, layers=None):
     k layers (parity subsets)."""
     spec = LAYER_SETS[name]
     if name.startswith("gpt2") or name.startswith("llama"):
-        nl = {"gpt2-small": 12, "gpt2-large": 36}.get(name, 32)
+        nl = {"gpt2-small": 12, "gpt2-small-fused": 12, "gpt2-large": 36}.get(name, 32)
         per_layer = []
         for r, c, cnt in spec:
             per_layer.append((r, c, cnt // nl))

@@ -269,6 +269,18 @@ def test_full_gpt2_small_set_sampled(ctx):
         check_g1_g3(outs[i], mats[i])
 
 
+@pytest.mark.slow
+def test_full_gpt2_small_fused_qkv_set_sampled(ctx):
+    """SURVEY §8(d) config 2 variant: the GPT-2 Small set with the fused
+    attention projection c_attn 768 x 2304 (48 matrices) in one call;
+    sampled matrices (each shape) against the oracle."""
+    shapes = syn.layer_set_shapes("gpt2-small-fused")
+    mats = [bf16_values(syn.gaussian(r, c, seed=3000 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    outs = run(ctx, mats)
+    for i in (0, 1, 2, 3, 46):
+        check_g1_g3(outs[i], mats[i])
+
+
 def test_empty_batch_and_single_rows(ctx):
     """Degenerate batches: no matrices (no launch), 1 x n and n x 1 rows in a
     mixed batch with a zero matrix (R9)."""
