@@ -2,13 +2,17 @@
 
 Every rank holds every momentum matrix; rank r orthogonalises the matrices
 ``pe_shard_plan`` assigns to it (deterministic LPT, identical on all ranks, no
-communication), then an all-gather gives every rank every result (each rank
-needs all of polar(M) for its weight update W <- W - lr * polar(M)).
+communication), then every rank receives every result (each rank needs all
+of polar(M) for its weight update W <- W - lr * polar(M)).
 
-torch.distributed is plumbing here (process group, NCCL/gloo transport); the
-compute runs in libpe.so.  Outputs are exchanged as raw bytes packed per rank
-in matrix-index order, so the same code runs on NCCL (GPU) and gloo (CPU
-tests).
+The product path is ``attach`` + ``polar_sharded``: libpe's own NCCL
+communicator (pe_attach_comm) and pe_polar_sharded, which broadcasts each
+result from its owner bucket by bucket while later buckets compute;
+torch.distributed only hands the NCCL unique id around.  ``polar_split``
+runs one matrix split by columns over the ranks.  ``GatherPlan`` and
+``gather_outputs`` are the torch-level alternative (one all-gather of
+per-rank packed results; NCCL or gloo), kept for users without libpe's
+communicator and exercised by the gloo tests.
 """
 from __future__ import annotations
 
