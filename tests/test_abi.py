@@ -180,3 +180,36 @@ def test_nccl_entry_points_validate_without_a_gpu():
     assert L.pe_comm_info(None, ctypes.byref(r), ctypes.byref(w)) == 1
     assert L.pe_set_spectrum_init(None, 8) == 1
     assert L.pe_polar_ex(None, None, None, None, 1, 5, 0, 0, 0, None) == 1
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/pe.h compiles as C99 (no C++ constructs cross the boundary) and
+    a C program links libpe.so and calls the host-only entry points."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "abi.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "pe.h"
+int main(void) {
+  double c[8 * 3];
+  int owner[3];
+  int64_t shapes[6] = {768, 768, 768, 3072, 3072, 768};
+  if (pe_coeffs(1e-3, 5, 8, 1.01, c) != PE_OK) return 1;
+  if (pe_shard_plan(shapes, 3, 2, owner) != PE_OK) return 2;
+  if (pe_polar(NULL, NULL, NULL, NULL, 1, 5, PE_BF16, NULL) != PE_ERR_INVALID_ARG) return 3;
+  printf("%s %.15f %d\n", pe_version(), c[0], owner[0] + owner[1] + owner[2]);
+  return 0;
+}
+''')
+    exe = tmp_path / "abi"
+    lib_dir = os.path.dirname(pe.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                        "-L", lib_dir, "-l:libpe.so", "-Wl,-rpath," + lib_dir, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    assert "sm_100a" in out.stdout and out.stdout.split()[-1] == "1"
