@@ -1245,3 +1245,24 @@ def test_input_scale_range():
         Xh = run(c, [Mh], T=5, dtype=dt)[0]
         assert np.all(np.isfinite(Xh)) and om.rel_frobenius(Xh, X1) <= (1e-5 if dt == "f32" else 2e-2)
     c.close()
+
+
+def test_c_program_uses_the_abi_on_the_gpu(tmp_path):
+    """examples/polar_c.c: a plain C program (no Python, no PyTorch) drives the
+    GPU path through include/pe.h -- pe_create, an in-place pe_polar on a
+    256 x 768 bf16 matrix, pe_destroy -- and finds rows orthonormal to 0.15."""
+    import os
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(pe.LIB_PATH)
+    exe = tmp_path / "polar_c"
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-Wall", "-I", os.path.join(root, "include"),
+                        "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "polar_c.c"),
+                        "-L", lib_dir, "-l:libpe.so", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                        "-Wl,-rpath," + lib_dir, "-lm", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
