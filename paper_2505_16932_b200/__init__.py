@@ -17,7 +17,7 @@ __all__ = [
     "PE_BF16", "PE_FP32", "PE_SAFETY_ALL", "PE_SAFETY_NOT_FINAL", "PE_NO_RECENTER",
     "PeError", "lib", "pe_coeffs", "pe_coeffs_ex", "pe_shard_plan", "pe_shard_buckets", "pe_flops",
     "pe_nccl_unique_id",
-    "Context", "pe_polar", "pe_polar_host", "EXPORTED_SYMBOLS",
+    "Context", "pe_polar", "pe_polar_host", "MuonPE", "EXPORTED_SYMBOLS",
 ]
 
 PE_BF16 = 0
@@ -417,3 +417,44 @@ def pe_polar(inputs, outputs=None, iters=5, coeffs=None, stream=None):
 
 def pe_polar_host(inputs, outputs, iters=5, device=0, stream=None):
     return _ctx_for(device).polar_host(inputs, outputs, iters, stream)
+
+
+class MuonPE:
+    """Muon with Polar Express as the polar step: a minimal
+    optimizer over bf16 2-D CUDA parameters whose whole step -- momentum
+    M <- beta M + (1 - beta) G, X = polar(M) by Polar Express, W <- W - lr X --
+    is one pe_muon_step call (momentum fused into the norm pass, the weight
+    update into the last update epilogue).  Parameters of other shapes or
+    dtypes are the caller's business (the paper optimises them with AdamW,
+    P:393).  Usage: opt = MuonPE(params, lr=0.02, beta=0.9); loss.backward();
+    opt.step()."""
+
+    def __init__(self, params, lr=0.02, beta=0.9, iters=5, device=None):
+        import torch
+        self.params = [p for p in params]
+        for p in self.params:
+            if p.dim() != 2 or p.dtype != torch.bfloat16 or not p.is_cuda or not p.is_contiguous():
+                raise ValueError("MuonPE takes contiguous 2-D bf16 CUDA parameters")
+        self.lr, self.beta, self.iters = float(lr), float(beta), int(iters)
+        self.momenta = [torch.zeros_like(p) for p in self.params]     # M_0 = 0 (P:45)
+        dev = self.params[0].device.index if self.params else (device or 0)
+        self.ctx = Context(dev or 0)
+        if self.params:
+            self.ctx.reserve([tuple(p.shape) for p in self.params])
+
+    def step(self):
+        import torch
+        live = [(p, m) for p, m in zip(self.params, self.momenta) if p.grad is not None]
+        if not live:
+            return
+        with torch.no_grad():
+            grads = [p.grad.to(torch.bfloat16).contiguous() for p, _ in live]
+            self.ctx.muon_step([p.data for p, _ in live], [m for _, m in live], grads, beta=self.beta, lr=self.lr,
+                               iters=self.iters)
+
+    def zero_grad(self, set_to_none=True):
+        for p in self.params:
+            if set_to_none:
+                p.grad = None
+            elif p.grad is not None:
+                p.grad.zero_()

@@ -1266,3 +1266,28 @@ def test_c_program_uses_the_abi_on_the_gpu(tmp_path):
     assert r.returncode == 0, r.stderr
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
+
+
+def test_muon_optimizer_wrapper():
+    """MuonPE (a thin optimizer over pe_muon_step): two steps on
+    bf16 parameters equal two direct pe_muon_step calls bit for bit, with
+    the momentum starting at zero."""
+    shapes = [(256, 768), (768, 256), (300, 520)]
+    w0 = [to_dev_bf16(syn.gaussian(r, c, seed=60 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    gs = [[to_dev_bf16(syn.gaussian(r, c, seed=70 + 10 * s_ + i, std=0.01)) for i, (r, c) in enumerate(shapes)]
+          for s_ in range(2)]
+    params = [torch.nn.Parameter(w.clone()) for w in w0]
+    opt = pe.MuonPE(params, lr=0.05, beta=0.9)
+    for s_ in range(2):
+        for p, g in zip(params, gs[s_]):
+            p.grad = g.clone()
+        opt.step()
+    c = pe.Context(0)
+    W = [w.clone() for w in w0]
+    M = [torch.zeros_like(w) for w in w0]
+    for s_ in range(2):
+        c.muon_step(W, M, [g.clone() for g in gs[s_]], beta=0.9, lr=0.05, iters=5)
+    torch.cuda.synchronize()
+    for p, w in zip(params, W):
+        assert torch.equal(p.data.view(torch.int16), w.view(torch.int16))
+    c.close()
