@@ -12,6 +12,12 @@
  *   online (device): pe_polar -- Listing 2: normalise by
  *       ||X||_F * 1.01 + 1e-7, transpose when rows > cols, then T steps of
  *       A = X X^T; B = b A + c A^2; X = a X + B X, transpose back.
+ *       Variants: pe_polar_ex (fp32 in / bf16 arithmetic / fp32 out),
+ *       pe_polar_host (host buffers), pe_muon_step (one fused Muon step,
+ *       P:41-49), pe_set_spectrum_init (App. G first step).
+ *   multi-GPU: pe_nccl_unique_id / pe_attach_comm / pe_polar_sharded (each
+ *       rank its pe_shard_plan share, results broadcast to every rank) and
+ *       pe_polar_split (one matrix split by columns, all-reduced Gram).
  *
  * Conventions common to every call:
  *   - plain C: no C++ types, no exceptions cross this boundary; every call
