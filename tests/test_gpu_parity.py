@@ -124,9 +124,13 @@ def test_batch_mixed_shapes_and_batch_independence(ctx):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("kappa", [10.0, 100.0, 1000.0])
+@pytest.mark.parametrize("kappa", [10.0, 100.0, 1000.0, 1e6])
 @pytest.mark.parametrize("shape", [(256, 1024), (512, 512)])
 def test_prescribed_spectrum(ctx, kappa, shape):
+    """Prescribed spectra sigma log-spaced in [1/kappa, 1],
+    kappa up to 1/ell and the §4.1 stress kappa = 1e6: G2 (whole
+    matrix within twice the oracle's own bf16-input sensitivity, and 2e-2 on
+    the directions with sigma >= 0.1 sigma_max) and G3."""
     k = min(shape)
     M = syn.prescribed_spectrum(*shape, syn.logspaced(k, kappa), seed=int(kappa))
     Mb = bf16_values(M)
