@@ -4,13 +4,15 @@
 
 One step = one pe_polar call over a whole Muon layer set (all §8(a) rows:
 Frobenius norm, scale/orient, T x {Gram, b A + c A^2, a X + B X}, transpose
-back), inputs resident in HBM.  Default workload: BASELINE.json configs[1]
-(GPT-2 Small layer set, 72 matrices, bf16, T=5, degree 5).  With N ranks each
+back), inputs resident in HBM.  Default workload: the north-star
+configuration (BASELINE.json north_star / configs[3]): the full Llama-3-8B
+Muon layer set, 224 matrices, bf16, T=5, degree 5 (reading R12); the GPT-2
+Small / Large sets (configs[1], [2]) are reported under `extra_workloads`.  With N ranks each
 rank computes its pe_shard_plan share and the results are all-gathered
 over NCCL inside libpe (pe_polar_sharded; strong scaling of one layer set).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
-                       [--impl ours|reference] [--extra llama3-8b,...]
+                       [--impl ours|reference] [--extra gpt2-small,...]
 Prints ONE JSON line (rank 0).
 """
 from __future__ import annotations
@@ -188,10 +190,13 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
     tot, cnt = prof[kind]
     per_launch_ms = tot / max(cnt, 1)
     sustained = step_ms > 50.0
-    traffic = None
+    traffic, traffic_src = None, None
     try:
+        # written by profiles/ncu_traffic.py from an `ncu --set full` capture
+        # (dram__bytes_read.sum + dram__bytes_write.sum of that kernel)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(workload or "", {}).get(kind)
+            tj = json.load(f).get(workload or "", {})
+            traffic, traffic_src = tj.get(kind), tj.get("_source")
     except Exception:
         pass
     if kind in fl:
@@ -204,7 +209,8 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
         out = {"bound": "hbm", "unit": "GB/s"}
     out.update({"kernel": f"pe_gemm_sm100[{kind}]" if kind in fl else kind, "achieved": round(achieved, 2),
                 "peak": peak, "peak_source": f"{src} {'sustained' if (sustained and kind in fl) else 'burst'}",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_per_launch": (fl[kind] if kind in fl else by[kind]),
                 "launch_ms": round(per_launch_ms, 4),
                 "timing": "CUDA events around each launch of this kernel, on its stream, in a second pass of the same K steps",
                 "share_of_step": round(tot / max(sum(v[0] for v in prof.values()), 1e-9), 4)})
@@ -230,8 +236,10 @@ def norm_gbs(prof, shapes, steps, peaks):
             "peak_gbs": peaks["hbm_gbs"], "frac": round(gbs / peaks["hbm_gbs"], 4)}
 
 
-def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
-    """The fp64 oracle (as it stands) on host cores over a bounded sample."""
+def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0, steps=None):
+    """The fp64 oracle (as it stands) on host cores over a bounded sample.
+    steps=None: repeat the sample for ~budget_s; steps=K: exactly K passes
+    (the reference arm's timed steps, one pass each)."""
     import pe_synth as syn
     from oracle import coeffs as oc, iteration as oi
     table, _ = oc.pe_coeffs(ELL, DEGREE, 8, 1.01)
@@ -250,12 +258,18 @@ def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
     except Exception:
         cores, blas = os.cpu_count(), "?"
     passes, t0 = 0, time.perf_counter()
+    step_s = []
     while True:
+        ts = time.perf_counter()
         for M in mats:
             oi.polar_express(M, table, T)
+        step_s.append(time.perf_counter() - ts)
         passes += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or el * (passes + 1) / passes > max_s:
+        if steps is not None:
+            if passes >= steps:
+                break
+        elif el >= budget_s or el * (passes + 1) / passes > max_s:
             break
     dense = lambda s: T * (4 * min(s) ** 2 * max(s) + 2 * min(s) ** 3)
     f_sample = sum(dense(shapes[i]) for i in sample)
@@ -263,12 +277,15 @@ def oracle_time(shapes, T, budget_s=10.0, max_s=30.0, seed=0):
     t_sample = el / passes
     t_set = t_sample * f_set / f_sample
     return {"value": round(len(shapes) / t_set, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{len(sample)} of {len(shapes)} matrices (layer 0), {passes} passes in {el:.1f}s, "
-                      f"numpy fp64 ({blas}); set time extrapolated by dense-flop ratio {f_set / f_sample:.1f}",
+            "sample": f"{len(sample)} of {len(shapes)} matrices ({'x'.join(map(str, shapes[sample[0]]))}"
+                      f"{' ...' if len(sample) > 1 else ''}), {passes} passes in {el:.1f}s, "
+                      f"numpy fp64 ({blas}); value = set size / set time extrapolated by the dense-flop ratio "
+                      f"{f_set / f_sample:.1f}",
+            "sample_ms_per_pass": round(1e3 * t_sample, 3), "step_ms": [round(1e3 * x, 3) for x in step_s],
             "s_per_set_extrapolated": round(t_set, 3), "gflops_fp64": round(f_sample / t_sample / 1e9, 2)}
 
 
-_workload_name = ["gpt2-small"]
+_workload_name = ["llama3-8b"]
 
 
 def run_reference(args):
@@ -276,15 +293,21 @@ def run_reference(args):
     if rank != 0:
         return
     shapes = layer_set(args.workload)
-    # each step = one bounded-sample pass; warmup passes untimed
-    cb = oracle_time(shapes, args.iters, budget_s=max(2.0, 1.0 * (args.steps + args.warmup)),
-                     max_s=120.0)
+    # each step = one pass of the oracle over the bounded sample (timed; the
+    # warm-up passes are run and discarded); `value` extrapolates the sample's
+    # rate to the whole set by the dense-flop ratio, `ms_per_step` is what one
+    # timed step took
+    oracle_time(shapes, args.iters, steps=max(0, args.warmup)) if args.warmup > 0 else None
+    cb = oracle_time(shapes, args.iters, steps=max(1, args.steps))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * cb["s_per_set_extrapolated"], 3), "higher_is_better": True,
+            "ms_per_step": cb["sample_ms_per_pass"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "matrices": len(shapes), "T": args.iters, "degree": DEGREE,
                        "ell": ELL},
+            "note": "reference = the fp64 CPU oracle (the tier has no reference implementation); one step = one "
+                    "pass over the sample named in cpu_baseline.sample, ms_per_step its measured time; value "
+                    "extrapolates to the whole set (s_per_set_extrapolated)",
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -330,7 +353,6 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         torch.cuda.synchronize(device)
         if clocks is not None and not profile:
             clocks.active = True
-        ctx.profile_enable(profile)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         # the last warm-up step is enqueued right before the timed ones (no
         # idle gap before the first timed step).  Warm-up steps flush L2 like
@@ -339,6 +361,7 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         # land on timed step 1.
         flush.zero_()
         step()
+        ctx.profile_enable(profile)          # the K timed steps only (not the warm-up step above)
         for k in range(steps):
             flush.zero_()                    # evict L2 (buffer > 126 MB) between timed steps
             evs[k][0].record(stream)
@@ -422,9 +445,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gpt2-small")
+    ap.add_argument("--workload", default="llama3-8b")
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--extra", default="gpt2-large,llama3-8b", help="comma list of extra layer sets (N=1 only), or ''")
+    ap.add_argument("--extra", default="gpt2-small,gpt2-large", help="comma list of extra layer sets (N=1 only), or ''")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     _workload_name[0] = args.workload
@@ -517,17 +540,18 @@ def main():
             ctx2 = pe.Context(local_rank)
             c2 = ClockSampler(local_rank)
             c2.start()
-            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, 3, 3, 1, 0, device, flush, False, c2)
+            st2 = 10
+            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, st2, 3, 1, 0, device, flush, False, c2)
             ck2 = c2.stop()
             m2 = sum(ms2) / len(ms2)
             f2 = pe.pe_flops(sh, T, DEGREE)
             extras[name] = {"matrices": len(sh), "value": round(len(sh) / (m2 * 1e-3), 3), "unit": UNIT,
-                            "ms_per_step": round(m2, 3), "steps": 3, "warmup": 3,
+                            "ms_per_step": round(m2, 3), "steps": st2, "warmup": 3,
                             "tflops": round(f2 / (m2 * 1e-3) / 1e12, 2),
                             "frac_of_bf16_peak_sustained": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
                             "frac_of_bf16_peak_burst": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
                             "roofline": roofline(prof2, sh, T, m2, peaks, src, name),
-                            "per_kernel_ms_per_step": {k: round(v[0] / 3, 3) for k, v in prof2.items()},
+                            "per_kernel_ms_per_step": {k: round(v[0] / st2, 4) for k, v in prof2.items()},
                             "clocks": ck2}
             del xs2, ys2
             ctx2.close()

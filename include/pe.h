@@ -141,8 +141,13 @@ pe_status pe_set_coeffs(pe_ctx ctx, const double* coeffs, int ntuples, int degre
  * upload slots pe_reserve keeps in reserve (4 per call of pe_reserve,
  * iters <= 64) for the lifetime of the context, since the graph's copy node
  * re-reads it at every replay. Graph replays see the current contents of the
- * captured buffers. Errors: PE_ERR_INVALID_ARG, PE_ERR_WORKSPACE (also: a
- * captured call without a reservation). */
+ * captured buffers.  A captured graph stays valid until pe_destroy: the plan
+ * and the workspace it points into are retired, never freed, when the
+ * workspace later grows or the plan leaves the context's 8-plan cache.  A
+ * one-step (iters = 1) call whose outputs overlap its inputs uses a separate
+ * plan (see pe_polar) that pe_reserve does not build: issue it once
+ * uncaptured before capturing it.  Errors: PE_ERR_INVALID_ARG,
+ * PE_ERR_WORKSPACE (also: a captured call without a reservation). */
 pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtype);
 
 /*
@@ -154,6 +159,9 @@ pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtyp
  *                  P_i Q_j^T, i + j <= 2, of the three-plane split
  *                  v = p0 + p1 + p2; relF <= 1e-5).  in[i] == out[i]
  *                  (in place) is allowed; distinct matrices must not overlap.
+ *                  (With iters = 1 the single update reads the inputs while
+ *                  it stores results, so a call whose outputs overlap its
+ *                  inputs stores through the workspace plus one copy pass.)
  *   iters          T >= 1; tuples past the table repeat its last tuple
  *                  (P:495-496).
  *   stream         a cudaStream_t (NULL = legacy default stream); all work is

@@ -163,6 +163,7 @@ struct Plan {
   size_t fused_cap = 0;
   size_t ws_needed = 0;
   uint64_t last_use = 0;
+  bool pinned = false;          // used by a captured CUDA graph: kept (with its workspace) until pe_destroy
 };
 
 // One pinned upload buffer of the per-call ring.
@@ -190,6 +191,10 @@ struct pe_ctx_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   std::vector<Plan*> plans;
+  // plans a captured graph points into, and workspaces they carve, retired
+  // from the cache (workspace growth, LRU) but alive until pe_destroy
+  std::vector<Plan*> retired_plans;
+  std::vector<void*> retired_ws;
   uint64_t use_clock = 0;
 
   CallSlot calls[kCallSlots];
@@ -369,6 +374,8 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   cudaDeviceSynchronize();
   if (c->ws) cudaFree(c->ws);
   for (Plan* p : c->plans) free_plan(p);
+  for (Plan* p : c->retired_plans) free_plan(p);
+  for (void* w : c->retired_ws) cudaFree(w);
   for (CallSlot& cs : c->calls) {
     if (cs.d) cudaFree(cs.d);
     if (cs.h) cudaFreeHost(cs.h);
@@ -456,13 +463,24 @@ static pe_status make_emap(CUtensorMap* map, void* base, int rows, int cols, int
 }
 
 // Grow the shared workspace; every cached plan points into it, so growth
-// drops the cache (after the device has finished with it).
+// drops the cache (after the device has finished with it).  Plans a captured
+// CUDA graph uses (pinned) and the workspace they carve are retired instead of
+// freed: the graph may be replayed until pe_destroy.
 static pe_status ensure_workspace(pe_ctx c, size_t bytes) {
   if (bytes <= c->ws_bytes) return PE_OK;
   PE_CUDA(cudaDeviceSynchronize());
-  for (Plan* p : c->plans) free_plan(p);
+  bool keep_ws = false;
+  for (Plan* p : c->plans) {
+    if (p->pinned) { c->retired_plans.push_back(p); keep_ws = true; }
+    else free_plan(p);
+  }
   c->plans.clear();
-  if (c->ws) { cudaFree(c->ws); c->ws = nullptr; c->ws_bytes = 0; }
+  if (c->ws) {
+    if (keep_ws) c->retired_ws.push_back(c->ws);
+    else cudaFree(c->ws);
+    c->ws = nullptr;
+    c->ws_bytes = 0;
+  }
   if (cudaMalloc(&c->ws, bytes) != cudaSuccess) {
     cudaGetLastError();
     g_last_error = "workspace allocation of " + std::to_string(bytes) + " bytes failed";
@@ -483,11 +501,21 @@ static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size
 // io (bf16 compute only, pe_polar_ex): bit 0 = the caller's input is fp32,
 // bit 1 = the caller's output is fp32; such matrices go through the copy
 // passes (conversion) instead of being folded into the first / last GEMM.
-static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
-                            bool no_orient = false, int io = 0) {
+// no_direct: the last update never writes the caller's buffer (it writes the
+// workspace and the finalize pass copies out) -- a one-step call whose output
+// overlaps an input: that update reads the caller's M across whole column
+// panels while other tiles store, so a direct store would race (in == out).
+static std::vector<int64_t> plan_key(const int64_t* shapes, int count, bool no_orient, int io, bool no_direct) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
   if (no_orient) key.push_back(-1);
   if (io) key.push_back(-2 - io);
+  if (no_direct) key.push_back(-100);
+  return key;
+}
+
+static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
+                            bool no_orient = false, int io = 0, bool no_direct = false) {
+  const std::vector<int64_t> key = plan_key(shapes, count, no_orient, io, no_direct);
   for (Plan* p : c->plans)
     if (p->dtype == dtype && p->key == key) {
       p->last_use = ++c->use_clock;
@@ -624,7 +652,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     const MatDev& md = mats[i];
     const bool foldable = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
     const bool folded = foldable && !(io & 1);
-    const bool direct = foldable && !(io & 2);
+    const bool direct = foldable && !(io & 2) && !no_direct;
     mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0);
     x0[i] = md.X[0];
     const int64_t pst = (int64_t)md.m * md.ldx;
@@ -744,12 +772,14 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->n_upd = (int)upd.size();
   for (int k = 0; k < 4; ++k) P->n_it[k] = (int)it[k].size();
   P->n_chunks = (int)cmat.size();
-  // LRU eviction (the evicted plan's kernels may still be queued: sync first)
+  // LRU eviction (the evicted plan's kernels may still be queued: sync
+  // first); a pinned plan leaves the cache but stays alive (retired)
   if ((int)c->plans.size() >= kMaxPlans) {
     auto lru = std::min_element(c->plans.begin(), c->plans.end(),
                                 [](const Plan* a, const Plan* b) { return a->last_use < b->last_use; });
     PE_CUDA(cudaDeviceSynchronize());
-    free_plan(*lru);
+    if ((*lru)->pinned) c->retired_plans.push_back(*lru);
+    else free_plan(*lru);
     c->plans.erase(lru);
   }
   P->last_use = ++c->use_clock;
@@ -1044,6 +1074,27 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
   return PE_OK;
 }
 
+// Does any output range overlap any input range (byte intervals)?
+static bool outputs_overlap_inputs(const void* const* in, void* const* out, const int64_t* shapes, int count,
+                                   pe_dtype dtype, int io) {
+  const size_t ies = (dtype == PE_FP32 || (io & 1)) ? 4 : 2, oes = (dtype == PE_FP32 || (io & 2)) ? 4 : 2;
+  std::vector<std::pair<uintptr_t, uintptr_t>> ri(count), ro(count);
+  for (int i = 0; i < count; ++i) {
+    const size_t e = (size_t)shapes[2 * i] * (size_t)shapes[2 * i + 1];
+    ri[i] = {reinterpret_cast<uintptr_t>(in[i]), reinterpret_cast<uintptr_t>(in[i]) + e * ies};
+    ro[i] = {reinterpret_cast<uintptr_t>(out[i]), reinterpret_cast<uintptr_t>(out[i]) + e * oes};
+  }
+  std::sort(ri.begin(), ri.end());
+  std::vector<uintptr_t> end_max(count);            // max end over the first k + 1 sorted inputs
+  for (int i = 0; i < count; ++i) end_max[i] = std::max(ri[i].second, i ? end_max[i - 1] : 0);
+  for (const auto& o : ro) {
+    // inputs starting before o's end overlap o iff one of them ends after o's start
+    const size_t k = std::lower_bound(ri.begin(), ri.end(), std::make_pair(o.second, (uintptr_t)0)) - ri.begin();
+    if (k > 0 && end_max[k - 1] > o.first) return true;
+  }
+  return false;
+}
+
 // pe_polar_split: the all-reduce hook of one call
 struct SplitCtx {
   pe_allreduce_fn fn;
@@ -1090,11 +1141,14 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   const bool init = c->init_iters > 0 && dtype == PE_BF16 && !muon && !sh;
   if (!muon && !sh && !io && !init && small_eligible(shapes, count, dtype, &max_npad))
     return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad, up);
+  // one-step call (T = 1 without the App. G step): its only update reads the
+  // caller's inputs while storing results, so an output overlapping any input
+  // goes through the workspace and the finalize pass
+  const bool no_direct = (iters + (init ? 1 : 0) == 1) && outputs_overlap_inputs(in, out, shapes, count, dtype, io);
   Plan* P = nullptr;
   if (capturing) {
     // no allocation or synchronisation is allowed: the plan must be cached
-    std::vector<int64_t> key(shapes, shapes + 2 * count);
-    if (io) key.push_back(-2 - io);
+    const std::vector<int64_t> key = plan_key(shapes, count, false, io, no_direct);
     for (Plan* q : c->plans)
       if (q->dtype == dtype && q->key == key) P = q;
     if (!P || (dtype == PE_FP32 && !c->scratch)) {
@@ -1102,7 +1156,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       return PE_ERR_WORKSPACE;
     }
     P->last_use = ++c->use_clock;
-  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr, io)) != PE_OK) {
+    P->pinned = true;       // the graph keeps pointers into it: never evicted or freed before pe_destroy
+  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr, io, no_direct)) != PE_OK) {
     return s;
   }
 

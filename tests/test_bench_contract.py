@@ -27,12 +27,15 @@ def test_reference_arm_line():
     assert d["unit"] == "matrices/s" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["config"]["workload"] == "gpt2-small"
+    assert d["config"]["workload"] == "llama3-8b"            # the north-star set is the default
+    # the reference arm reports what it timed: one pass per step
+    assert len(d["cpu_baseline"]["step_ms"]) == d["steps"]
+    assert abs(d["ms_per_step"] - sum(d["cpu_baseline"]["step_ms"]) / d["steps"]) <= 1e-3 * d["ms_per_step"] + 1e-3
 
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _run(["--steps", "2", "--warmup", "3", "--extra", "", "--no-cpu-baseline"], 900)
+    d = _run(["--workload", "gpt2-small", "--steps", "2", "--warmup", "3", "--extra", "", "--no-cpu-baseline"], 900)
     assert BASE_KEYS <= set(d) and "impl" not in d
     assert d["steps"] == 2 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
     assert d["gpu_launches"] > 0 and d["dtype"] == "bf16"

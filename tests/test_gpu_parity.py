@@ -1316,3 +1316,60 @@ def test_power_law_spectrum(ctx, shape):
     # rounding (as G2 does for prescribed spectra)
     S = om.rel_frobenius(oi.polar_express(M, TABLE, 5), ref)
     assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + max(1e-2, 2 * S)
+
+
+@pytest.mark.parametrize("shape", [(768, 768), (4096, 4096), (1024, 3072), (3072, 1024)])
+def test_inplace_single_iteration(ctx, shape):
+    """iters = 1 in place: the one update reads M across whole
+    column panels while other tiles store, so the library routes the result
+    through the workspace; in-place must equal out-of-place bit for bit and
+    pe_polar_host (in place on its staging buffer) must equal both."""
+    r, c = shape
+    M = bf16_values(syn.gaussian(r, c, seed=901, std=0.02))
+    ref = run(ctx, [M], T=1)[0]
+    x = to_dev_bf16(M)
+    ctx.polar([x], [x], iters=1)
+    torch.cuda.synchronize()
+    assert np.array_equal(x.float().cpu().numpy().astype(np.float64), ref)
+    # an output overlapping another matrix's input also takes the safe route
+    a = to_dev_bf16(M)
+    b = to_dev_bf16(M)
+    ctx.polar([a, b], [b, a], iters=1)
+    torch.cuda.synchronize()
+    for t in (a, b):
+        assert np.array_equal(t.float().cpu().numpy().astype(np.float64), ref)
+    h = to_dev_bf16(M).cpu().pin_memory()
+    ho = torch.empty_like(h).pin_memory()
+    ctx.polar_host([h], [ho], iters=1)
+    assert np.array_equal(ho.float().numpy().astype(np.float64), ref)
+    check_g1_g3(ref, M, T=1, g1=3e-2)
+
+
+def test_captured_graph_survives_workspace_growth_and_eviction():
+    """a captured graph keeps pointers into its plan and the
+    workspace; growing the workspace (a bigger batch) and pushing the plan out
+    of the 8-plan cache must not free them while the context lives."""
+    c = pe.Context(0)
+    shapes = [(512, 1024), (1024, 512)]
+    c.reserve(shapes, pe.PE_BF16)
+    xs = [to_dev_bf16(syn.gaussian(r, s, seed=950 + i, std=0.02)) for i, (r, s) in enumerate(shapes)]
+    ys = [torch.empty_like(x) for x in xs]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        c.polar(xs, ys, iters=5)
+    # grow the workspace, then cycle more than 8 other plans through the cache
+    big = [to_dev_bf16(syn.gaussian(2048, 4096, seed=960, std=0.02))]
+    c.polar(big, iters=2)
+    for k in range(10):
+        c.polar([to_dev_bf16(syn.gaussian(256 + 8 * k, 512, seed=970 + k, std=0.02))], iters=2)
+    torch.cuda.synchronize()
+    for i, (r, s) in enumerate(shapes):
+        xs[i].copy_(to_dev_bf16(syn.gaussian(r, s, seed=980 + i, std=0.02)))
+    g.replay()
+    torch.cuda.synchronize()
+    direct = c.polar([x.clone() for x in xs], iters=5)
+    torch.cuda.synchronize()
+    for a, b in zip(ys, direct):
+        assert torch.equal(a, b)
+    del g
+    c.close()
