@@ -275,6 +275,18 @@ pe_status pe_polar_split(pe_ctx ctx, const void* in, void* out, int64_t rows, in
  */
 pe_status pe_set_spectrum_init(pe_ctx ctx, int power_iters);
 
+/*
+ * Same, with the bf16 stabilisation margin of reading R17 made explicit: the
+ * cubic of eq. (init_poly) is divided by 1 + |b| * margin.  margin = 0 applies
+ * eq. (init_poly) exactly as P:1256-1263 states it (what the oracle computes);
+ * pe_set_spectrum_init uses margin = 2^-7, which keeps p(sigma_1) <= 1.01
+ * under the bf16 error (~|b| 2^-8) of the cancellation a s + b s^3 when z is
+ * close to 1 (margin 0 diverges to NaN at z = 0.9995 in bf16).  Errors:
+ * PE_ERR_INVALID_ARG (NULL, power_iters outside 0..1000, margin outside
+ * [0, 1] or NaN).
+ */
+pe_status pe_set_spectrum_init_ex(pe_ctx ctx, int power_iters, double margin);
+
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */
 pe_status pe_last_launch_count(pe_ctx ctx, int* launches);

@@ -106,7 +106,6 @@ def muon_step(W, M, G, beta, lr, table, T):
 # ---------------------------------------------------------------- App. G
 INIT_Z_MIN = 1.0 / np.sqrt(2.0)     # P:1252 "the intervals do not overlap ... z >= 1/sqrt(2)"
 INIT_Z_MAX = 1.0 - 1e-6             # reading R17: numerically rank one -> no init
-INIT_SAFETY = 2.0 ** -7             # reading R17: p_G = p / (1 + |b| 2^-7), see spectrum_init
 
 
 def power_start(m):
@@ -130,12 +129,11 @@ def spectrum_init(X, power_iters):
     method on A = X X^T (the k = 1 case of the footnote's subspace iteration,
     P:1237-1239: Rayleigh quotient of the last vector, sigma~_1 <= sigma_1),
     and if 1/sqrt(2) <= z apply p(x) = a (x/F) + b (x/F)^3 with
-    (a, b) = init_cubic(z) (eq. init_poly), i.e. X <- (a/F) X + (b/F^3) A X,
-    divided by 1 + |b| 2^-7 (reading R17: as z -> 1, |a| ~ |b| ~ 1/sqrt(1-z^2)
-    and p(sigma_1) = a sigma_1 + b sigma_1^3 is a cancellation whose bf16
-    error ~ |b| 2^-8 would push sigma_1 past the 1.01 margin the Polar Express
-    table allows; the scale keeps p <= 1 under that error, and the GPU path
-    computes the same step).  Returns (X', z, applied)."""
+    (a, b) = init_cubic(z) exactly as eq. (init_poly) gives them (P:1256-1263;
+    App. G assumes ||M||_F = 1, hence the x/F -- reading R17), i.e.
+    X <- (a/F) X + (b/F^3) A X.  Nothing else: the product's bf16 margin
+    (reading R17) is the product's own stabilisation and is gated against
+    this step, not built into it.  Returns (X', z, applied)."""
     X = np.asarray(X, dtype=np.float64)
     F = np.sqrt(np.sum(X * X))
     A = X @ X.T
@@ -148,9 +146,8 @@ def spectrum_init(X, power_iters):
     z = np.sqrt(max(lam, 0.0)) / F if F > 0 else 0.0
     if not (INIT_Z_MIN <= z <= INIT_Z_MAX):
         return X, z, False
-    a, b = init_cubic(z)
-    sc = 1.0 / (1.0 + abs(b) * INIT_SAFETY)
-    return (a * sc / F) * X + (b * sc / F ** 3) * (A @ X), z, True
+    a, b = init_cubic(z)                           # eq. (init_poly)
+    return (a / F) * X + (b / F ** 3) * (A @ X), z, True
 
 
 def polar_express_init(M, table, T, power_iters=8, norm="listing2"):

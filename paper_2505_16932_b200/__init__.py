@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = [
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
+    "pe_set_spectrum_init_ex",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -76,6 +77,7 @@ def lib():
         "pe_polar_host": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
         "pe_polar_ex": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, I, I, P]),
         "pe_set_spectrum_init": (I, [P, I]),
+        "pe_set_spectrum_init_ex": (I, [P, I, D]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -207,10 +209,16 @@ class Context:
         arr = (ctypes.c_double * len(flat))(*flat)
         _check(lib().pe_set_coeffs(self._h, arr, len(tuples), deg), "pe_set_coeffs")
 
-    def set_spectrum_init(self, power_iters):
+    def set_spectrum_init(self, power_iters, margin=None):
         """pe_set_spectrum_init: App. G's spectrum-aware first step with
-        `power_iters` power-method steps (0 = off)."""
-        _check(lib().pe_set_spectrum_init(self._h, int(power_iters)), "pe_set_spectrum_init")
+        `power_iters` power-method steps (0 = off); `margin` (reading R17,
+        default 2^-7 = pe_set_spectrum_init) goes to pe_set_spectrum_init_ex,
+        0 = eq. (init_poly) exactly."""
+        if margin is None:
+            _check(lib().pe_set_spectrum_init(self._h, int(power_iters)), "pe_set_spectrum_init")
+        else:
+            _check(lib().pe_set_spectrum_init_ex(self._h, int(power_iters), float(margin)),
+                   "pe_set_spectrum_init_ex")
 
     def reserve(self, shapes, dtype=PE_BF16):
         _check(lib().pe_reserve(self._h, _shapes_arr(shapes), len(shapes), int(dtype)), "pe_reserve")

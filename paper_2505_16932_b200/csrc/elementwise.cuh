@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
 // Per matrix: z = sqrt(lambda / F^2), F^2 = ssq * inv^2 (= ||X_0||_F^2), and
 // the first step's (a/F, b/F^3) from eq. (init_poly), or (1, 0).
 __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const float* inv, float* mcoef,
-                                    int count) {
+                                    int count, double margin) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -651,10 +651,12 @@ __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const 
     const double den = z * t * (2.0 * z * z - 1.0);
     const double F = sqrt(f2);
     const double a = (z * z * (z + t) - t) / den, b = (t - z) / den;
-    // reading R17: divide by 1 + |b| 2^-7 -- p(sigma_1) = a s + b s^3 cancels
-    // (|a| ~ |b| ~ 1/t as z -> 1), and its bf16 error ~ |b| 2^-8 must not push
-    // sigma_1 past the table's 1.01 margin (unscaled: NaN at z = 0.9995)
-    const double sc = 1.0 / (1.0 + fabs(b) * 0.0078125);
+    // reading R17 (product-side stabilisation, not part of eq. (init_poly)):
+    // divide by 1 + |b| * margin (default 2^-7) -- p(sigma_1) = a s + b s^3
+    // cancels (|a| ~ |b| ~ 1/t as z -> 1), and its bf16 error ~ |b| 2^-8 must
+    // not push sigma_1 past the table's 1.01 margin (margin 0: NaN at
+    // z = 0.9995); margin = 0 is the paper's step exactly
+    const double sc = 1.0 / (1.0 + fabs(b) * margin);
     ca = (float)(a * sc / F);
     cb = (float)(b * sc / (F * F * F));
   }

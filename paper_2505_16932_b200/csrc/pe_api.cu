@@ -233,6 +233,7 @@ struct pe_ctx_s {
 
   PeDist* dist = nullptr;       // pe_attach_comm (pe_dist.cpp)
   int init_iters = 0;           // pe_set_spectrum_init: power iterations of App. G's first step (0 = off)
+  double init_margin = 0.0078125;  // pe_set_spectrum_init_ex: R17's 1 / (1 + |b| margin) (0 = eq. (init_poly) exactly)
 };
 
 PeDist*& pe_ctx_dist(pe_ctx c) { return c->dist; }
@@ -416,6 +417,15 @@ extern "C" pe_status pe_set_coeffs(pe_ctx c, const double* coeffs, int ntuples, 
 extern "C" pe_status pe_set_spectrum_init(pe_ctx c, int power_iters) {
   if (!c || power_iters < 0 || power_iters > 1000) return PE_ERR_INVALID_ARG;
   c->init_iters = power_iters;
+  c->init_margin = 0.0078125;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_set_spectrum_init_ex(pe_ctx c, int power_iters, double margin) {
+  if (!c || power_iters < 0 || power_iters > 1000 || !(margin >= 0.0) || !(margin <= 1.0))
+    return PE_ERR_INVALID_ARG;
+  c->init_iters = power_iters;
+  c->init_margin = margin;
   return PE_OK;
 }
 
@@ -1421,7 +1431,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         }
         launch(pe_init_coef_kernel, cdiv(count, 128), 128, 0, st, (const double*)sa.lam,
                (const double*)at<double>(P, P->o_sssq), (const float*)at<float>(P, P->o_inv),
-               at<float>(P, P->o_smcoef), count);
+               at<float>(P, P->o_smcoef), count, c->init_margin);
         ++launches;
       }
       if (sh && mode == kModeGram) {

@@ -179,6 +179,7 @@ def test_nccl_entry_points_validate_without_a_gpu():
     r, w = ctypes.c_int(), ctypes.c_int()
     assert L.pe_comm_info(None, ctypes.byref(r), ctypes.byref(w)) == 1
     assert L.pe_set_spectrum_init(None, 8) == 1
+    assert L.pe_set_spectrum_init_ex(None, 8, 0.0) == 1
     assert L.pe_polar_ex(None, None, None, None, 1, 5, 0, 0, 0, None) == 1
 
 

@@ -521,9 +521,11 @@ def test_init_cubic_interpolates_and_bounds():
 
 
 def test_spectrum_init_is_the_scalar_map_and_a_lower_bound():
-    """spectrum_init(X) = U p(Sigma/F) V^T / (1 + |b| 2^-7) with p from the z it
-    found (matrix function, via an independent SVD route; R17's
-    scale); z <= sigma_1 / F (Rayleigh
+    """spectrum_init(X) = U p(Sigma/F) V^T with p = eq. (init_poly) at the z it
+    found (matrix function, via an independent SVD route; no margin:
+    P:1256-1263 has none); the result's largest singular value is <= 1
+    (P:1263: "the largest singular value of p(M) is still at most 1");
+    z <= sigma_1 / F (Rayleigh
     quotient bound) and -> sigma_1 / F as the power method
     converges; no gap (Gaussian, z < 1/sqrt(2)) leaves X unchanged."""
     rng = np.random.default_rng(5)
@@ -542,9 +544,8 @@ def test_spectrum_init_is_the_scalar_map_and_a_lower_bound():
             assert np.array_equal(Y, X)
             continue
         a, b = oi.init_cubic(z)
-        sc = 1.0 / (1.0 + abs(b) * 2.0 ** -7)        # reading R17's margin for the bf16 cancellation
         sh = s * 0.37 / F
-        ref = (U * (sc * (a * sh + b * sh ** 3))) @ V.T
+        ref = (U * (a * sh + b * sh ** 3)) @ V.T
         assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
         assert np.linalg.svd(Y, compute_uv=False)[0] <= 1 + 1e-9
     assert zs == sorted(zs) and abs(zs[-1] - s[0] * 0.37 / F) < 1e-12
