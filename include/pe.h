@@ -313,9 +313,12 @@ pe_status pe_profile_read(pe_ctx ctx, double* ms, int* counts, int nkinds);
 /*
  * Deterministic matrix-to-rank partition for data-parallel Muon:
  * longest-processing-time greedy on the per-matrix cost 3 m^2 n + m^3
- * (m = min side), ties broken by matrix index, so every rank computes the
- * same plan with no communication.  owner[i] in [0, world).
- * Errors: PE_ERR_INVALID_ARG (world < 1, count < 0, NULL).
+ * (m = min side), run bucket by bucket over pe_polar_sharded's buckets
+ * (pe_shard_nbuckets / pe_shard_buckets): largest first, to the rank with
+ * the least work in the bucket, ties to the least total work, then the
+ * lowest rank.  Every bucket is balanced, hence the whole set; every rank
+ * computes the same plan with no communication.  owner[i] in [0, world).
+ * Errors: PE_ERR_INVALID_ARG (world < 1, count < 0, NULL, a side < 1).
  */
 pe_status pe_shard_plan(const int64_t* shapes, int count, int world, int* owner);
 
@@ -345,22 +348,73 @@ pe_status pe_shard_buckets(const int64_t* shapes, int count, int nbuckets, int* 
  * pe_polar_sharded: same arguments and semantics as pe_polar, called by every
  *   rank with the same shape list.  Rank r computes the matrices
  *   pe_shard_plan(shapes, count, world) assigns to it, in buckets of
- *   consecutive matrices (pe_shard_buckets, 4 by default or $PE_SHARD_BUCKETS);
- *   as soon as bucket b is computed its matrices are broadcast from their
- *   owners into every rank's out[i] on the side stream (ncclBroadcast, one
- *   NCCL group per bucket) while bucket b+1 is computed.  When the work
- *   enqueued on `stream` completes, out[i] holds polar(M_i) on every rank.
- *   in[i] is read only on the owner of matrix i (it may be NULL elsewhere);
- *   out[i] must be valid on every rank; in[i] == out[i] is allowed.
+ *   consecutive matrices (pe_shard_buckets; their number pe_shard_nbuckets
+ *   gives, or $PE_SHARD_BUCKETS); as soon as bucket b is computed it is
+ *   exchanged on the side stream while bucket b+1 is computed:
+ *     - if out[] is the pe_shard_layout of one flat buffer (out[i] =
+ *       base + offsets[i] on every rank), the owned matrices' last update
+ *       epilogues store straight into this rank's chunk and ONE in-place
+ *       all-gather per bucket (ncclAllGather, or the exchange function's
+ *       PE_EXCHANGE_ALLGATHER) fills the other chunks -- no packing copy;
+ *     - otherwise every matrix is broadcast from its owner into every rank's
+ *       out[i] (ncclBroadcast, one NCCL group per bucket, or
+ *       PE_EXCHANGE_BROADCAST per matrix).
+ *   When the work enqueued on `stream` completes, out[i] holds polar(M_i) on
+ *   every rank.  in[i] is read only on the owner of matrix i (it may be NULL
+ *   elsewhere); out[i] must be valid on every rank; in[i] == out[i] is
+ *   allowed.  On an error after part of the exchange was enqueued, `stream`
+ *   still waits for what was enqueued before the error returns.
  *   Errors: PE_ERR_INVALID_ARG (no communicator, bad arguments),
  *   PE_ERR_NCCL (NCCL missing or failed; an earlier asynchronous NCCL error),
- *   and pe_polar's.
+ *   the exchange function's status, and pe_polar's.
  */
 pe_status pe_nccl_unique_id(char id[128]);
 pe_status pe_attach_comm(pe_ctx ctx, const char id[128], int rank, int world);
 pe_status pe_comm_info(pe_ctx ctx, int* rank, int* world);
 pe_status pe_polar_sharded(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
                            int count, int iters, pe_dtype dtype, void* stream);
+
+/*
+ * Caller-supplied exchange instead of NCCL (virtual ranks, other transports).
+ * pe_polar_sharded calls fn on the enqueueing host thread, after the bucket's
+ * compute is ordered before `stream` (the side stream, a cudaStream_t), with
+ *   op = PE_EXCHANGE_ALLGATHER: buf holds world chunks of `bytes` bytes; this
+ *        rank's chunk (index `root` = this rank) is complete once `stream`
+ *        reaches this point; fn must make every chunk complete on `stream`;
+ *   op = PE_EXCHANGE_BROADCAST: `bytes` bytes at buf, complete on rank `root`,
+ *        to be made complete on every rank on `stream`.
+ * fn returns PE_OK or an error, which pe_polar_sharded returns.
+ * pe_attach_exchange replaces any attached communicator.
+ * Errors: PE_ERR_INVALID_ARG (NULL ctx or fn, rank outside [0, world)).
+ */
+#define PE_EXCHANGE_ALLGATHER 0
+#define PE_EXCHANGE_BROADCAST 1
+typedef pe_status (*pe_exchange_fn)(int op, void* buf, int64_t bytes, int root, void* user, void* stream);
+pe_status pe_attach_exchange(pe_ctx ctx, int rank, int world, pe_exchange_fn fn, void* user);
+
+/*
+ * Bucket count pe_polar_sharded uses for this shape list and world: one
+ * bucket per ~2.4 TFLOP of per-rank work (about 2 ms of compute, long next to
+ * a bucket's fixed fill/drain cost; the exposed tail is the last bucket's
+ * exchange), at most 8; 1 when world = 1; $PE_SHARD_BUCKETS overrides.
+ */
+pe_status pe_shard_nbuckets(const int64_t* shapes, int count, int world, int* nbuckets);
+
+/*
+ * Flat output layout for pe_polar_sharded's zero-copy all-gather: bucket after
+ * bucket (pe_shard_nbuckets buckets, pe_shard_buckets boundaries), each bucket
+ * `world` equal chunks of the largest rank's share, rank r's matrices of the
+ * bucket packed in index order inside chunk r, each at a 256-byte granule.
+ * offsets[i] (caller-owned, count int64) receives matrix i's byte offset,
+ * chunk_bytes[b] (caller-owned, pe_shard_nbuckets int64, or NULL) bucket b's
+ * per-rank chunk size (bucket b spans world * chunk_bytes[b] bytes, buckets
+ * back to back from offset 0), *total_bytes the buffer size; the same on
+ * every rank.  Matrix i of dtype's
+ * element size then lives at base + offsets[i] (row-major, lda = cols).
+ * Errors: PE_ERR_INVALID_ARG.
+ */
+pe_status pe_shard_layout(const int64_t* shapes, int count, int world, pe_dtype dtype, int64_t* offsets,
+                          int64_t* chunk_bytes, int64_t* total_bytes);
 
 /* Algorithmic flops of one pe_polar call (symmetric Gram and A^2 counted
  * once): sum_i T [ m(m+1) n + m^2 (m+1) + 2 m^2 n ]; degree-3

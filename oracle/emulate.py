@@ -16,6 +16,8 @@ the reading, not from the kernels (the two share no code):
   Gram (P:498):      A = bf16(x*x)
   poly:      B = bf16(fp32(b*A) + fp32(c*(A*A)))   (no FMA contraction)
   update:    X' = bf16(fp32(a*X) + (B*X))          (no FMA contraction)
+  degree 3 (B = b A, eq. deg3_solution P:808): B is never formed;
+                     X' = bf16(fp32(a*X) + fp32(b*(A*X)))
 with a, b, c the fp32-rounded table entries.
 """
 from __future__ import annotations
@@ -51,10 +53,11 @@ def diagonal_bf16(sigmas_bf16, table, T, folded=True):
         if len(tup) == 3:
             c = np.float32(tup[2])
             B = _bf16(np.float32(b * A) + np.float32(c * np.float32(A * A)))
+            BX = np.float32(B * x)
         else:
-            B = _bf16(np.float32(b * A))
+            BX = np.float32(b * np.float32(A * x))
         if first:
-            x = _bf16(np.float32(np.float32(a * x) + np.float32(B * x)) * inv)
+            x = _bf16(np.float32(np.float32(a * x) + BX) * inv)
         else:
-            x = _bf16(np.float32(a * x) + np.float32(B * x))
+            x = _bf16(np.float32(a * x) + BX)
     return x

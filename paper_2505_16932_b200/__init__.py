@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "pe_last_launch_count", "pe_shard_plan", "pe_flops", "pe_profile_enable", "pe_profile_read",
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
-    "pe_set_spectrum_init_ex",
+    "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -90,6 +90,9 @@ def lib():
         "pe_attach_comm": (I, [P, ctypes.c_char_p, I, I]),
         "pe_comm_info": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
         "pe_polar_sharded": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, P]),
+        "pe_attach_exchange": (I, [P, I, I, EXCHANGE_FN, P]),
+        "pe_shard_nbuckets": (I, [I64P, I, I, ctypes.POINTER(I)]),
+        "pe_shard_layout": (I, [I64P, I, I, I, I64P, I64P, I64P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -102,6 +105,12 @@ def lib():
 # pe_allreduce_fn (include/pe.h): (buf, count, dtype 0 fp32 / 1 fp64, user, stream) -> pe_status
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                                 ctypes.c_void_p)
+
+
+# pe_exchange_fn (include/pe.h): (op, buf, bytes, root, user, stream) -> pe_status
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                               ctypes.c_void_p, ctypes.c_void_p)
+PE_EXCHANGE_ALLGATHER, PE_EXCHANGE_BROADCAST = 0, 1
 
 
 class _DevBuf:
@@ -158,6 +167,31 @@ def pe_shard_buckets(shapes, nbuckets):
     beg = (ctypes.c_int * (nbuckets + 1))()
     _check(lib().pe_shard_buckets(_shapes_arr(shapes), n, int(nbuckets), beg), "pe_shard_buckets")
     return list(beg)
+
+
+def pe_shard_nbuckets(shapes, world):
+    """pe.h pe_shard_nbuckets: pe_polar_sharded's bucket count for this set."""
+    n = ctypes.c_int()
+    _check(lib().pe_shard_nbuckets(_shapes_arr(shapes), len(shapes), int(world), ctypes.byref(n)),
+           "pe_shard_nbuckets")
+    return n.value
+
+
+def pe_shard_layout(shapes, world, dtype=PE_BF16, chunks=False):
+    """pe.h pe_shard_layout: (byte offset of every matrix, total bytes) of the
+    flat output buffer that makes pe_polar_sharded's exchange one in-place
+    all-gather per bucket; with chunks=True also the per-rank chunk bytes of
+    every bucket: (offsets, chunk_bytes, total)."""
+    n = len(shapes)
+    offs = (ctypes.c_int64 * max(n, 1))()
+    nb = pe_shard_nbuckets(shapes, world)
+    ch = (ctypes.c_int64 * max(nb, 1))()
+    tot = ctypes.c_int64()
+    _check(lib().pe_shard_layout(_shapes_arr(shapes), n, int(world), int(dtype), offs, ch, ctypes.byref(tot)),
+           "pe_shard_layout")
+    if chunks:
+        return list(offs[:n]), list(ch[:nb]), tot.value
+    return list(offs[:n]), tot.value
 
 
 def pe_nccl_unique_id():
@@ -355,6 +389,23 @@ class Context:
         _check(lib().pe_attach_comm(self._h, ctypes.create_string_buffer(bytes(unique_id), 128), int(rank),
                                     int(world)), "pe_attach_comm")
 
+    def attach_exchange(self, rank, world, fn):
+        """pe_attach_exchange: pe_polar_sharded exchanges through the Python
+        callable fn(op, ptr, nbytes, root, stream) (op PE_EXCHANGE_ALLGATHER /
+        PE_EXCHANGE_BROADCAST, ptr an integer device address, stream a
+        cudaStream_t handle) instead of NCCL; it raises on failure."""
+        self._x_errors = []
+
+        def cb(op, buf, nbytes, root, user, st):
+            try:
+                fn(int(op), int(buf or 0), int(nbytes), int(root), int(st or 0))
+                return 0
+            except Exception as e:          # reported when pe_polar_sharded returns
+                self._x_errors.append(e)
+                return 5                    # PE_ERR_NCCL
+        self._xfn = EXCHANGE_FN(cb)         # kept alive as long as the context uses it
+        _check(lib().pe_attach_exchange(self._h, int(rank), int(world), self._xfn, None), "pe_attach_exchange")
+
     def comm_info(self):
         r, w = ctypes.c_int(), ctypes.c_int()
         _check(lib().pe_comm_info(self._h, ctypes.byref(r), ctypes.byref(w)), "pe_comm_info")
@@ -363,7 +414,9 @@ class Context:
     def polar_sharded(self, inputs, outputs, iters=5, stream=None):
         """pe_polar_sharded: every rank passes the whole layer set (same shapes
         on every rank); this rank computes its pe_shard_plan share and the
-        results are broadcast from their owners into every rank's `outputs`.
+        results reach every rank's `outputs` (one all-gather per bucket when
+        `outputs` are the views of dist.sharded_outputs, else per-matrix
+        broadcasts).
         ``inputs[i]`` may be None on ranks that do not own matrix i."""
         import torch
         n = len(outputs)
@@ -384,8 +437,14 @@ class Context:
         shp = _shapes_arr([tuple(y.shape) for y in outputs])
         if stream is None:
             stream = torch.cuda.current_stream(outputs[0].device)
-        _check(lib().pe_polar_sharded(self._h, ins, outs, shp, n, int(iters), dt,
-                                      ctypes.c_void_p(stream.cuda_stream)), "pe_polar_sharded")
+        status = lib().pe_polar_sharded(self._h, ins, outs, shp, n, int(iters), dt,
+                                        ctypes.c_void_p(stream.cuda_stream))
+        errs = getattr(self, "_x_errors", None)
+        if errs:
+            e = errs[0]
+            errs.clear()
+            raise e
+        _check(status, "pe_polar_sharded")
         return outputs
 
     def polar_host(self, inputs, outputs, iters=5, stream=None):

@@ -99,6 +99,8 @@ struct GemmArgs {
   int* done;                   // per (matrix, phase) completion counters, zero at launch
   const int* need;             // per (matrix, mode): 2 * kEpiWarps * tiles
   const float* mcoef;          // spectrum-aware first step (App. G): per matrix (a, b), c = 0; else nullptr
+  int lin;                     // odd cubic step (degree-3 table, App. G step): no poly phase; the update
+                               // reads A as its left operand and computes X' = a X + b (A X)
   int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
                                // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
                                // stores, 256 = every result store to the same box, 2048 = right
@@ -132,6 +134,7 @@ struct TileCfg {
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
   bool scaled;                 // first iteration of a folded matrix
   bool muon;                   // result chunk is a Muon weight update of the chunk already at eout
+  bool lin;                    // update of a cubic step: left operand A, epilogue a X + b acc
   int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
@@ -181,6 +184,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   const bool tall = kEdge && (fl & kFlagTall) != 0;
   c.scaled = fold;
   c.muon = false;
+  c.lin = false;
   c.a_wide = c.b_wide = false;
   c.Amn = c.Bmn = nullptr;
   c.pan_a = tl.tm;
@@ -202,8 +206,9 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.ein = em + 2 * kP;
     c.eout = em + 3 * kP;
   } else {
-    c.A = maps + 3;
-    c.Amn = maps + 5;
+    c.lin = g.nphase == 0 && g.lin != 0;
+    c.A = maps + (c.lin ? 2 : 3);     // cubic: B = b A is never formed, the update reads A
+    c.Amn = maps + (c.lin ? 4 : 5);
     c.a_mn = false;
     c.a_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
@@ -291,8 +296,13 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
         for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.b, o[j]), __fmul_rn(cfg.c, wq[j]));
       } else {
+        if (cfg.lin) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.a, o[j]), wq[j]);
+          for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.a, o[j]), __fmul_rn(cfg.b, wq[j]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) wq[j] = __fadd_rn(__fmul_rn(cfg.a, o[j]), wq[j]);
+        }
         if (kEdge && cfg.scaled) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv);
@@ -390,7 +400,8 @@ __device__ __forceinline__ void epilogue_math_p3(const TileCfg& cfg, uint8_t* sl
         for (int j = 0; j < 8; ++j) {
           const float o = __fadd_rn(__fadd_rn(o0[j], o1[j]), o2[j]);
           wv[j] = (cfg.mode == kModePoly) ? __fadd_rn(__fmul_rn(cfg.b, o), __fmul_rn(cfg.c, wv[j]))
-                                        : __fadd_rn(__fmul_rn(cfg.a, o), wv[j]);
+                  : cfg.lin ? __fadd_rn(__fmul_rn(cfg.a, o), __fmul_rn(cfg.b, wv[j]))
+                            : __fadd_rn(__fmul_rn(cfg.a, o), wv[j]);
         }
       }
       float p0[8], p1[8], p2[8];

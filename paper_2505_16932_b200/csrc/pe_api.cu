@@ -1064,6 +1064,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     hc[3 * t + 2] = (nq == 3) ? (float)tup[2] : 0.0f;
   }
   a.T = T;
+  a.lin = (nq == 2) ? 1 : 0;
   if (inl) {
     a.mats = nullptr;
     a.ctas = nullptr;
@@ -1179,8 +1180,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   // PE_FUSED=1; measured equal to one launch per phase on the GPT-2 sets and
   // within noise on Llama, profiles/r1_variants.md)
   static const bool fused_on = getenv("PE_FUSED") && strcmp(getenv("PE_FUSED"), "0") != 0;
-  const bool fused = fused_on && dtype == PE_BF16 && !capturing && !sh && !init;   // (its setup may synchronise)
   const int nq = (c->degree + 1) / 2;
+  const bool fused = fused_on && dtype == PE_BF16 && !capturing && !sh && !init && nq == 3;   // (its setup may synchronise)
   if (fused) {
     if ((s = ensure_fused(c, P, T)) != PE_OK) return s;
     const size_t need_done = (size_t)count * 3 * T;
@@ -1349,6 +1350,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     g.dbg = c->dbg;
     g.stats = nullptr;
     g.mcoef = nullptr;
+    g.lin = 0;
   };
   if (fused) {
     // one persistent launch: all 3T phases of all matrices, dataflow-ordered
@@ -1372,9 +1374,14 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     const float fa = (float)tup[0], fb = (float)tup[1], fc = (nq == 3) ? (float)tup[2] : 0.0f;
     const int xin = sidx & 1;
     const int fin = (sidx == S - 1);
+    // odd cubic step (degree-3 table, or App. G's p(x) = a x + b x^3): no
+    // poly launch; the update reads A and computes a X + b (A X)
+    const bool cubic = istep || nq == 2;
     for (int mode = kModeGram; mode <= kModeUpdate; ++mode) {
+      if (cubic && mode == kModePoly) continue;
       GemmArgs g;
       base_args(g);
+      g.lin = cubic ? 1 : 0;
       static const bool alt = !(getenv("PE_ORDER") && !strcmp(getenv("PE_ORDER"), "fwd"));   // A/B knob
       const bool rev = alt && ((3 * sidx + mode) & 1);
       g.tiles = at<Tile>(P, mode == kModeUpdate ? (rev ? P->o_upd_r : P->o_upd) : (rev ? P->o_sym_r : P->o_sym));
@@ -1600,29 +1607,6 @@ extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const*
 }
 
 // ---------------------------------------------------------------- host utils
-extern "C" pe_status pe_shard_plan(const int64_t* shapes, int count, int world, int* owner) {
-  if (world < 1 || count < 0 || (count > 0 && (!shapes || !owner))) return PE_ERR_INVALID_ARG;
-  std::vector<double> cost(count);
-  for (int i = 0; i < count; ++i) {
-    const double r = (double)shapes[2 * i], cc = (double)shapes[2 * i + 1];
-    if (r < 1 || cc < 1) return PE_ERR_INVALID_ARG;
-    const double m = std::min(r, cc), n = std::max(r, cc);
-    cost[i] = 3.0 * m * m * n + m * m * m;
-  }
-  std::vector<int> idx(count);
-  std::iota(idx.begin(), idx.end(), 0);
-  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<double> load(world, 0.0);
-  for (int i : idx) {
-    int best = 0;
-    for (int w = 1; w < world; ++w)
-      if (load[w] < load[best]) best = w;
-    owner[i] = best;
-    load[best] += cost[i];
-  }
-  return PE_OK;
-}
-
 extern "C" pe_status pe_flops(const int64_t* shapes, int count, int iters, int degree, double* flops) {
   if (!flops || count < 0 || iters < 0 || (count > 0 && !shapes)) return PE_ERR_INVALID_ARG;
   if (degree != 3 && degree != 5) return PE_ERR_UNSUPPORTED;

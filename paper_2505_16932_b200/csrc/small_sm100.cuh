@@ -69,6 +69,7 @@ struct SmallArgs {
   const SmallCta* ctas;
   const float* coef;     // per iteration fp32 (a, b, c); nullptr: use inl_coef
   int T;
+  int lin;               // degree-3 table: no A A product, X' = a X + b (A X) (as the large path)
 };
 
 // byte offset of 16-byte unit u (columns 8u .. 8u+7) of row r in a
@@ -438,21 +439,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
         for (int q = 0; q < 4; ++q) small_store8<kP>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
       }
     }
-    // ---- B = b A + c A A, in place over A
-    sync_for_mma();
-    run_and_wait([&] { small_mma<kP, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
+    // ---- B = b A + c A A, in place over A (cubic: not formed)
+    if (!args.lin) {
+      sync_for_mma();
+      run_and_wait([&] { small_mma<kP, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
 #pragma unroll 1
-    for (int g = 0; g < 4; ++g) {
-      float w[32];
-      small_acc32<kP>(trow + 32 * g, true, w);
+      for (int g = 0; g < 4; ++g) {
+        float w[32];
+        small_acc32<kP>(trow + 32 * g, true, w);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float o[8];
-        const uint32_t off = small_unit(r, 4 * g + q);
-        small_load8<kP>(A, aplane, off, o);
+        for (int q = 0; q < 4; ++q) {
+          float o[8];
+          const uint32_t off = small_unit(r, 4 * g + q);
+          small_load8<kP>(A, aplane, off, o);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(__fmul_rn(b, o[j]), __fmul_rn(cc3, w[8 * q + j]));
-        small_store8<kP>(A, aplane, off, o);
+          for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(__fmul_rn(b, o[j]), __fmul_rn(cc3, w[8 * q + j]));
+          small_store8<kP>(A, aplane, off, o);
+        }
       }
     }
     // ---- X' = a X + B X, column chunks in place
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
           small_load8<kP>(X, xplane, off, o);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            o[j] = __fadd_rn(__fmul_rn(a, o[j]), w[8 * q + j]);
+            o[j] = __fadd_rn(__fmul_rn(a, o[j]), args.lin ? __fmul_rn(b, w[8 * q + j]) : w[8 * q + j]);
             if (fold && first) o[j] = __fmul_rn(o[j], inv);
           }
           small_store8<kP>(X, xplane, off, o);

@@ -5,9 +5,11 @@ Every rank holds every momentum matrix; rank r orthogonalises the matrices
 communication), then every rank receives every result (each rank needs all
 of polar(M) for its weight update W <- W - lr * polar(M)).
 
-The product path is ``attach`` + ``polar_sharded``: libpe's own NCCL
-communicator (pe_attach_comm) and pe_polar_sharded, which broadcasts each
-result from its owner bucket by bucket while later buckets compute;
+The product path is ``attach`` + ``sharded_outputs`` + ``polar_sharded``:
+libpe's own NCCL communicator (pe_attach_comm) and pe_polar_sharded, whose
+outputs live in one flat buffer laid out by pe_shard_layout, so every rank's
+last update epilogue writes its own chunk and one in-place all-gather per
+bucket fills the rest while later buckets compute;
 torch.distributed only hands the NCCL unique id around.  ``polar_split``
 runs one matrix split by columns over the ranks.  ``GatherPlan`` and
 ``gather_outputs`` are the torch-level alternative (one all-gather of
@@ -16,7 +18,7 @@ communicator and exercised by the gloo tests.
 """
 from __future__ import annotations
 
-from . import pe_nccl_unique_id, pe_shard_plan
+from . import PE_BF16, PE_FP32, pe_nccl_unique_id, pe_shard_layout, pe_shard_plan
 
 
 def owned(shapes, rank, world):
@@ -113,11 +115,26 @@ def attach(ctx, group=None):
     return rank, world
 
 
+def sharded_outputs(shapes, world, dtype, device):
+    """One flat output buffer in pe_shard_layout order (identical on every
+    rank) and the per-matrix views into it.  Passing the views as
+    pe_polar_sharded's outputs turns its exchange into one in-place
+    all-gather per bucket with no packing copy.  Returns (flat, views)."""
+    import torch
+    code = PE_BF16 if dtype == torch.bfloat16 else PE_FP32
+    es = 2 if code == PE_BF16 else 4
+    offs, total = pe_shard_layout(shapes, world, code)
+    flat = torch.empty(total, dtype=torch.uint8, device=device)
+    views = [flat[o:o + int(r) * int(c) * es].view(dtype).view(int(r), int(c)) for o, (r, c) in zip(offs, shapes)]
+    return flat, views
+
+
 def polar_sharded(ctx, inputs, outputs, iters=5, stream=None):
     """pe_polar_sharded: the layer set is split over the
-    ranks by pe_shard_plan, each rank computes its share and libpe broadcasts
-    every result from its owner into every rank's ``outputs`` over NCCL,
-    bucket by bucket, overlapping the remaining compute.  Needs ``attach``."""
+    ranks by pe_shard_plan, each rank computes its share and libpe exchanges
+    the results over NCCL bucket by bucket, overlapping the remaining
+    compute: one in-place all-gather per bucket when ``outputs`` are the views
+    of ``sharded_outputs``, else per-matrix broadcasts.  Needs ``attach``."""
     return ctx.polar_sharded(inputs, outputs, iters=iters, stream=stream)
 
 

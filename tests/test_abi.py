@@ -164,6 +164,40 @@ def test_shard_buckets_cover_the_set_in_order_with_balanced_cost():
         pe.pe_shard_buckets([(0, 4)], 2)
 
 
+def test_shard_layout_chunks_hold_each_owners_matrices():
+    """pe_shard_layout (the zero-copy all-gather layout): buckets back to back,
+    each `world` equal chunks; every matrix lies inside its owner's chunk of
+    its bucket (pe_shard_buckets x pe_shard_plan), 256-byte aligned, ranges
+    disjoint; the bucket count follows the per-rank work (1 for one rank, 8
+    for the Llama-3-8B set over 8 ranks, 1 for GPT-2 S over 8)."""
+    import pe_synth as syn
+    for wl, world in (("gpt2-small", 3), ("llama3-8b", 8), ("llama3-8b", 2), ("gpt2-large", 4)):
+        shapes = syn.layer_set_shapes(wl)
+        nb = pe.pe_shard_nbuckets(shapes, world)
+        offs, chunks, total = pe.pe_shard_layout(shapes, world, pe.PE_BF16, chunks=True)
+        owner = pe.pe_shard_plan(shapes, world)
+        beg = pe.pe_shard_buckets(shapes, nb)
+        assert len(chunks) == nb and total == world * sum(chunks)
+        spans = []
+        base = 0
+        for b in range(nb):
+            for i in range(beg[b], beg[b + 1]):
+                lo = base + owner[i] * chunks[b]
+                nbytes = 2 * shapes[i][0] * shapes[i][1]
+                assert offs[i] % 256 == 0 and lo <= offs[i] and offs[i] + nbytes <= lo + chunks[b]
+                spans.append((offs[i], offs[i] + nbytes))
+            base += world * chunks[b]
+        spans.sort()
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+        assert total < 1.12 * sum(2 * r * c for r, c in shapes)       # padding of the per-rank chunks
+    llama = syn.layer_set_shapes("llama3-8b")
+    assert pe.pe_shard_nbuckets(llama, 1) == 1 and pe.pe_shard_nbuckets(llama, 8) == 8
+    assert pe.pe_shard_nbuckets(syn.layer_set_shapes("gpt2-small"), 8) == 1
+    L = pe.lib()
+    assert L.pe_shard_layout(None, 0, 1, 0, None, None, None) == 1
+    assert L.pe_attach_exchange(None, 0, 1, pe.EXCHANGE_FN(), None) == 1
+
+
 def test_nccl_entry_points_validate_without_a_gpu():
     """pe_nccl_unique_id needs no device (NCCL bootstrap only); the collective
     calls reject a NULL context synchronously."""

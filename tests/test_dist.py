@@ -1,8 +1,9 @@
 """Multi-rank host logic on CPU (gloo, world size 2): every rank computes the
 same LPT shard plan (pe_shard_plan) and exchange buckets (pe_shard_buckets),
-owns a disjoint subset, and both the torch-level all-gather and a replay of
-pe_polar_sharded's per-bucket owner broadcasts leave every rank with every
-matrix's bytes."""
+owns a disjoint subset, and the torch-level all-gather, a replay of
+pe_polar_sharded's per-bucket owner broadcasts and a replay of its zero-copy
+per-bucket all-gather over the pe_shard_layout buffer each leave every rank
+with every matrix's bytes."""
 import os
 import socket
 
@@ -22,6 +23,7 @@ def _free_port():
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["PE_SHARD_BUCKETS"] = "3"       # several buckets on a small set (plan, layout, call agree)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import pe_synth as syn
@@ -68,7 +70,29 @@ def _worker(rank, world, port, q):
                 dist.broadcast(outs[i], src=owner[i])
         for i, (r, c) in enumerate(shapes):
             ok = ok and torch.equal(outs[i], (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16))
+        # the zero-copy layout (pe_shard_layout, dist.sharded_outputs): every
+        # rank writes its owned results into its chunk of each bucket, one
+        # all-gather per bucket over the chunks completes every output
+        from paper_2505_16932_b200 import pe_shard_layout
+        offs, chunks, total = pe_shard_layout(shapes, world, chunks=True)
+        flat, views = pdist.sharded_outputs(shapes, world, torch.bfloat16, "cpu")
+        ok = ok and len(chunks) == 3 and flat.numel() == total == world * sum(chunks)
+        flat.zero_()
+        for i in idx:
+            r, c = shapes[i]
+            views[i].copy_((torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16).view(r, c))
+        base = 0
+        for ch in chunks:
+            parts = [flat[base + k * ch:base + (k + 1) * ch] for k in range(world)]
+            dist.all_gather(parts, parts[rank].clone())
+            base += world * ch
+        for i, (r, c) in enumerate(shapes):
+            exp = (torch.arange(r * c, dtype=torch.float32) % 251 + i).to(torch.bfloat16).view(r, c)
+            ok = ok and torch.equal(views[i], exp) and offs[i] % 256 == 0
+        layouts = [None] * world
+        dist.all_gather_object(layouts, (offs, chunks))
         same = all(p == owner for p in plans) and all(bb == beg for bb in begs)
+        same = same and all(lay == (offs, chunks) for lay in layouts)
         q.put((rank, ok, same, sorted(idx)))
     finally:
         dist.destroy_process_group()

@@ -15,6 +15,7 @@ reading names is an explicit round-to-nearest-even to the stated format
   Gram:          A  = bf16(acc),                           acc = x x
   poly:          B  = bf16(fp32(b A) + fp32(c acc)),       acc = A A
   update:          X' = bf16(fp32(a X) + acc),               acc = B X
+  degree 3:        no B;  X' = bf16(fp32(a X) + fp32(b acc)), acc = A X
   a, b, c the table entries rounded to fp32; fp32 products of two bf16
   values are exact (on a diagonal every accumulator holds one product).
 
@@ -113,14 +114,14 @@ def pin_trajectory(sig_bf16, tuples, folded, variant=None):
             elif variant == "A_round_then_scale" and first:
                 A = bf16(f32(bf16(acc) * inv2))
             if c is None:
-                B = bf16(f32(b * A))
+                B = None
             elif variant == "poly_fma":
                 B = bf16(f32(b * A + c * (A * A)))
             elif variant == "B_fp32":
                 B = f32(f32(b * A) + f32(c * (A * A)))
             else:
                 B = bf16(f32(b * A) + f32(c * (A * A)))
-            acc = B * v                                           # exact
+            acc = B * v if B is not None else f32(b * (A * v))     # cubic: b (A X), B never formed
             if first:
                 if variant == "inv_early":
                     y = bf16(f32(f32(a * v) * inv + f32(acc * inv)))
@@ -174,7 +175,8 @@ def test_emulation_bit_exact_against_fraction_pin(folded):
 
 
 def test_emulation_bit_exact_degree3_table():
-    """Same pin for a degree-3 table (B = b A, eq. deg3_solution), both paths."""
+    """Same pin for a degree-3 table (eq. deg3_solution; the product
+    never forms B = b A: X' = a X + b (A X)), both paths."""
     tab3, _ = oc.pe_coeffs(1e-3, 3, 8, 1.01)
     sig = _sigma_sets()[0]
     for folded in (True, False):

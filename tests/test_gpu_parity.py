@@ -262,6 +262,42 @@ def test_other_tables(ctx):
     ctx.set_coeffs(TABLE)
 
 
+@pytest.mark.parametrize("shape", [(64, 96), (90, 68), (300, 1100), (600, 200)])
+def test_degree3_table_skips_the_square(ctx, shape):
+    """Degree-3 tables (eq. deg3_solution): B = b A needs no A^2, so a
+    call launches two GEMMs per iteration (Gram, update reading A with the
+    epilogue a X + b (A X)) instead of three, and pe_flops' count (no A^2
+    term) is the work launched.  Diagonal inputs: bit-exact against the R8
+    emulation of that step (small path: 64 x 96, 90 x 68; large path: the
+    others); Gaussian: G1 against the oracle."""
+    tab3 = oc.pe_coeffs(1e-3, 3, 8, 1.01)[0]
+    k = min(shape)
+    sig = syn.to_bf16_values(np.linspace(1.0, 0.02, k)).astype(np.float64)
+    M = syn.diagonal(*shape, sig)
+    G = bf16_values(syn.gaussian(*shape, seed=33, std=0.02))
+    launches = {}
+    try:
+        for deg, tab in ((5, TABLE), (3, tab3)):
+            ctx.set_coeffs(tab)
+            for T in (1, 4, 8):
+                X = run(ctx, [M], T=T)[0]
+                launches[(deg, T)] = ctx.last_launch_count()
+                if deg == 3:
+                    emu = emulate.diagonal_bf16(sig, tab3, T, folded=shape[1] % 8 == 0).astype(np.float64)
+                    assert np.array_equal(np.diag(X)[:k], emu), T
+            if deg == 3:
+                X = run(ctx, [G], T=8)[0]
+                assert om.rel_frobenius(X, oi.polar_express(G, tab3, 8)) <= g1_gate(k)
+    finally:
+        ctx.set_coeffs(TABLE)
+    if k > 128:       # large path: one launch per GEMM phase
+        for T in (4, 8):
+            assert launches[(5, T)] - launches[(3, T)] == T, launches
+    f5, f3 = pe.pe_flops([shape], 5, 5), pe.pe_flops([shape], 5, 3)
+    m = float(k)
+    assert f5 - f3 == pytest.approx(5 * m * m * (m + 1))
+
+
 @pytest.mark.slow
 def test_full_gpt2_small_set_sampled(ctx):
     """BASELINE configs[1] at full size in the bench launch configuration (one
@@ -963,6 +999,128 @@ def test_polar_sharded_single_rank_communicator():
         for y, z, r in zip(ys, inplace, ref):
             assert torch.equal(y.view(torch.int16), r.view(torch.int16))
             assert torch.equal(z.view(torch.int16), r.view(torch.int16))
+    c.close()
+
+
+class _VirtualRanks:
+    """W ranks as host threads on one GPU for pe_polar_sharded's exchange
+    function (pe_attach_exchange): each exchange step waits on the host for
+    this rank's side stream (so no kernel ever waits on another rank), meets
+    the other threads at a barrier, and copies the peers' bytes on its side
+    stream.  Matrices are independent, so every rank's gathered
+    outputs must equal a single pe_polar call bit for bit."""
+
+    def __init__(self, W):
+        import threading
+        self.W = W
+        self.bar = threading.Barrier(W, timeout=120)
+        self.ptr = [0] * W
+        self.calls = [[] for _ in range(W)]
+
+    def fn(self, rank):
+        def bytes_at(ptr, n):
+            return torch.as_tensor(pe._DevBuf(ptr, n, "|u1"), device="cuda")
+
+        def ex(op, ptr, nbytes, root, st):
+            s = torch.cuda.ExternalStream(st, device=0)
+            s.synchronize()
+            self.calls[rank].append((op, nbytes, root))
+            self.ptr[rank] = ptr
+            self.bar.wait()
+            with torch.cuda.stream(s):
+                if op == pe.PE_EXCHANGE_ALLGATHER:
+                    mine = bytes_at(ptr, self.W * nbytes)
+                    for r in range(self.W):
+                        if r != rank:
+                            mine[r * nbytes:(r + 1) * nbytes].copy_(bytes_at(self.ptr[r], self.W * nbytes)[r * nbytes:(r + 1) * nbytes])
+                elif rank != root:
+                    bytes_at(ptr, nbytes).copy_(bytes_at(self.ptr[root], nbytes))
+            s.synchronize()
+            self.bar.wait()
+        return ex
+
+
+@pytest.mark.parametrize("W,layout,nb", [(2, True, "3"), (3, True, None), (4, True, "2"), (2, False, "2"),
+                                         (4, False, None)])
+def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
+    """pe_polar_sharded's exchange path at world > 1 (2-4 virtual ranks in
+    threads on one GPU, each with its own context, stream and exchange
+    function): with outputs in the pe_shard_layout buffer the exchange is one
+    in-place all-gather per bucket (and each owner's last epilogue writes its
+    chunk directly), otherwise one broadcast per matrix from its owner; every
+    rank's outputs equal one pe_polar over the whole set bit for bit, and the
+    exchange steps are the ones the layout predicts."""
+    import threading
+    from paper_2505_16932_b200 import dist as pdist
+    if nb:
+        monkeypatch.setenv("PE_SHARD_BUCKETS", nb)
+    shapes = syn.layer_set_shapes("gpt2-small", layers=2) + [(130, 1000), (1000, 130), (64, 96), (300, 520)]
+    xs = [to_dev_bf16(bf16_values(syn.gaussian(r, c, seed=900 + i, std=0.02))) for i, (r, c) in enumerate(shapes)]
+    c0 = pe.Context(0)
+    ref = c0.polar(xs, iters=5)
+    torch.cuda.synchronize()
+    c0.close()
+    vr = _VirtualRanks(W)
+    outs, errs = [None] * W, []
+
+    def rank_main(r):
+        try:
+            c = pe.Context(0)
+            c.attach_exchange(r, W, vr.fn(r))
+            assert c.comm_info() == (r, W)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                if layout:
+                    _, ys = pdist.sharded_outputs(shapes, W, torch.bfloat16, "cuda")
+                else:
+                    ys = [torch.empty_like(x) for x in xs]
+                c.polar_sharded(xs, ys, iters=5, stream=st)
+            st.synchronize()
+            outs[r] = ys
+            c.close()
+        except Exception as e:          # surfaced below
+            errs.append(e)
+            vr.bar.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    nbk = pe.pe_shard_nbuckets(shapes, W)
+    for r in range(W):
+        for y, z in zip(outs[r], ref):
+            assert torch.equal(y.view(torch.int16), z.view(torch.int16))
+        ops = [op for op, _, _ in vr.calls[r]]
+        if layout:
+            assert ops == [pe.PE_EXCHANGE_ALLGATHER] * nbk
+        else:
+            assert ops == [pe.PE_EXCHANGE_BROADCAST] * len(shapes)
+            assert [root for _, _, root in vr.calls[r]] == pe.pe_shard_plan(shapes, W)
+
+
+def test_polar_sharded_exchange_error_is_reported():
+    """An exchange function that fails: pe_polar_sharded returns its status
+    (the Python exception is re-raised), the caller's stream is still joined
+    with the side stream, and the context keeps working afterwards."""
+    shapes = [(256, 512), (512, 256), (384, 384)]
+    xs = [to_dev_bf16(bf16_values(syn.gaussian(r, c, seed=950 + i, std=0.02))) for i, (r, c) in enumerate(shapes)]
+    c = pe.Context(0)
+
+    def bad(op, ptr, nbytes, root, st):
+        raise RuntimeError("exchange down")
+
+    c.attach_exchange(0, 2, bad)
+    with pytest.raises(RuntimeError, match="exchange down"):
+        c.polar_sharded(xs, [torch.empty_like(x) for x in xs], iters=5)
+    torch.cuda.synchronize()
+    ys = c.polar(xs, iters=5)
+    c.attach_exchange(0, 1, bad)              # world 1: no exchange step at all
+    zs = c.polar_sharded(xs, [torch.empty_like(x) for x in xs], iters=5)
+    torch.cuda.synchronize()
+    for y, z in zip(ys, zs):
+        assert torch.equal(y.view(torch.int16), z.view(torch.int16))
     c.close()
 
 
