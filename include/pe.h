@@ -287,6 +287,28 @@ pe_status pe_set_spectrum_init(pe_ctx ctx, int power_iters);
  */
 pe_status pe_set_spectrum_init_ex(pe_ctx ctx, int power_iters, double margin);
 
+/*
+ * Fast polynomial iteration for rectangular matrices (App. H, Alg. 4,
+ * P:1303-1316), opt-in for the context's later bf16 pe_polar / pe_polar_ex /
+ * pe_polar_host calls with a degree-5 table.  A matrix with min side
+ * m > 128 and max side n > min_aspect * m (min_aspect <= 0: the paper's rule
+ * n / m > 1.5 T / (T - 1)) is computed as
+ *     Y = X X^T (+ shift I in the first application), Q_0 = I,
+ *     R_t = Q_{t-1} Y Q_{t-1},  Q_t = Q_{t-1} h_t(R_t),  X' = Q X
+ * (wide orientation; p_t(x) = x h_t(x^2), h_t(y) = a_t + b_t y + c_t y^2),
+ * restarted every `restart` iterations (1 = Listing 2 exactly,
+ * >= T = one application).  Rectangular products: 2 per application instead
+ * of 2 per iteration; per further iteration four m x m products.  Other
+ * matrices of the call run Listing 2 (a mixed call becomes two grouped
+ * calls).  Rounding points (R19): Y, T = Y Q, R, H = b R + c R^2,
+ * Q and X' each rounded once to bf16 from fp32 accumulators.  Not with
+ * pe_set_spectrum_init, degree-3 tables, fp32, pe_muon_step, pe_polar_split
+ * or under graph capture (PE_ERR_UNSUPPORTED).  restart = 0 turns it off
+ * (the default).  Errors: PE_ERR_INVALID_ARG (NULL, restart < 0, shift
+ * outside [0, 1), NaN min_aspect).
+ */
+pe_status pe_set_rect_iteration(pe_ctx ctx, int restart, double min_aspect, double shift);
+
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */
 pe_status pe_last_launch_count(pe_ctx ctx, int* launches);

@@ -61,3 +61,105 @@ def diagonal_bf16(sigmas_bf16, table, T, folded=True):
         else:
             x = _bf16(np.float32(a * x) + BX)
     return x
+
+
+def r8_polar_express(M_bf16, table, T, folded=True):
+    """The bf16 design of reading R8 on a general matrix: bf16 operands and an
+    exact-products accumulation rounded once to fp32 (fp64 matmul of the
+    bf16-valued operands, then fp32 -- the tensor cores' fp32 accumulation
+    differs only in its order and truncation.),
+    and the same rounding points as ``diagonal_bf16`` (which it equals bit for
+    bit on diagonal inputs -- its pin).  Listing 2's orientation (P:493,
+    P:501).  Used to measure how widely the design's own rounding points
+    spread against the fp64 oracle (tests/test_r8_spread.py), i.e. what a
+    bf16 gate can demand of the GPU at a given size."""
+    def mm(P, Q):
+        return (P.astype(np.float64) @ Q.astype(np.float64)).astype(np.float32)
+
+    M = np.asarray(M_bf16, dtype=np.float32)
+    tall = M.shape[0] > M.shape[1]
+    X = (M.T if tall else M).copy()
+    nrm = np.sqrt(float(np.sum(X.astype(np.float64) ** 2))) * 1.01 + 1e-7
+    inv = np.float32(1.0 / nrm)
+    if not folded:
+        X = _bf16(X * inv)
+    for it, tup in enumerate(schedule(table, T)):
+        a, b = np.float32(tup[0]), np.float32(tup[1])
+        first = folded and it == 0
+        acc = mm(X, X.T)
+        A = _bf16(acc * np.float32(inv * inv)) if first else _bf16(acc)
+        if len(tup) == 3:
+            c = np.float32(tup[2])
+            B = _bf16(np.float32(b * A) + np.float32(c * mm(A, A)))
+            BX = mm(B, X)
+        else:
+            BX = np.float32(b * mm(A, X))
+        X = _bf16(np.float32(np.float32(a * X) + BX) * inv) if first else _bf16(np.float32(a * X) + BX)
+    return X.T if tall else X
+
+
+def _sym_upper(S, blk=256):
+    """The symmetric matrix a kernel that stores only the blk x blk blocks on
+    or above the block diagonal hands to its consumers: blocks below the
+    diagonal are the transposes of the stored ones."""
+    n = S.shape[0]
+    bi = np.arange(n) // blk
+    lower = bi[:, None] > bi[None, :]
+    return np.where(lower, S.T, S)
+
+
+def r19_alg4(M_bf16, table, T, restart=None, shift=1e-3, folded=True):
+    """The bf16 design of Alg. 4 (App. H) on the GPU (DESIGN.md
+    reading R19), in the wide orientation with products accumulated exactly
+    and rounded once to fp32 (as r8_polar_express):
+        Y   = bf16(fp32(acc [* inv^2]) + shift)   acc = X X^T (shift: first application)
+        H_1 = bf16(fp32(b Y) + fp32(c acc))       acc = Y Y
+        Q_1 = H_1, diagonal bf16(fp32(H_1) + a)
+        then per further iteration t of the application:
+        T   = bf16(acc)   acc = Y Q
+        R   = bf16(acc)   acc = Q T   (upper blocks stored, symmetrised)
+        H   = bf16(fp32(b R) + fp32(c acc))       acc = R R
+        Q   = bf16(fp32(a Q) + acc)               acc = H Q
+        X'  = bf16(acc [* inv])                   acc = Q X
+    An application of one iteration is Listing 2's step (r8).  Equal to the
+    GPU bit for bit on diagonal inputs (every product has one term)."""
+    def mm(P, Q):
+        return (P.astype(np.float64) @ Q.astype(np.float64)).astype(np.float32)
+
+    M = np.asarray(M_bf16, dtype=np.float32)
+    tall = M.shape[0] > M.shape[1]
+    X = (M.T if tall else M).copy()
+    nrm = np.sqrt(float(np.sum(X.astype(np.float64) ** 2))) * 1.01 + 1e-7
+    inv = np.float32(1.0 / nrm)
+    inv2 = np.float32(inv * inv)
+    if not folded:
+        X = _bf16(X * inv)
+    tups = schedule(table, T)
+    k = T if restart is None else min(int(restart), T)
+    m = X.shape[0]
+    eye = np.eye(m, dtype=bool)
+    for b, t0 in enumerate(range(0, T, k)):
+        first = b == 0
+        scaled = folded and first
+        sh = np.float32(shift if first else 0.0)
+        blk = tups[t0:t0 + k]
+        a, bb, c = (np.float32(v) for v in blk[0])
+        acc = mm(X, X.T)
+        if scaled:
+            acc = np.float32(acc * inv2)
+        Y = _bf16(np.where(eye, np.float32(acc + sh), acc))
+        H = _bf16(np.float32(bb * Y) + np.float32(c * mm(Y, Y)))
+        if len(blk) == 1:
+            Xn = np.float32(np.float32(a * X) + mm(H, X))
+            X = _bf16(np.float32(Xn * inv) if scaled else Xn)
+            continue
+        Q = np.where(eye, _bf16(np.float32(H + a)), H)
+        for tup in blk[1:]:
+            a, bb, c = (np.float32(v) for v in tup)
+            Tm = _bf16(mm(Y, Q))
+            R = _sym_upper(_bf16(mm(Q, Tm)))
+            H = _bf16(np.float32(bb * R) + np.float32(c * mm(R, R)))
+            Q = _bf16(np.float32(a * Q) + mm(H, Q))
+        acc = mm(Q, X)
+        X = _bf16(np.float32(acc * inv) if scaled else acc)
+    return X.T if tall else X

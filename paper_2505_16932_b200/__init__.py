@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = [
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
     "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
+    "pe_set_rect_iteration",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -78,6 +79,7 @@ def lib():
         "pe_polar_ex": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P), I64P, I, I, I, I, I, P]),
         "pe_set_spectrum_init": (I, [P, I]),
         "pe_set_spectrum_init_ex": (I, [P, I, D]),
+        "pe_set_rect_iteration": (I, [P, I, D, D]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -253,6 +255,14 @@ class Context:
         else:
             _check(lib().pe_set_spectrum_init_ex(self._h, int(power_iters), float(margin)),
                    "pe_set_spectrum_init_ex")
+
+    def set_rect_iteration(self, restart, min_aspect=0.0, shift=1e-3):
+        """pe_set_rect_iteration: App. H's Alg. 4 for matrices with aspect
+        ratio above `min_aspect` (<= 0: the paper's 1.5 T / (T - 1)),
+        restarted every `restart` iterations (0 = off), Y shifted by `shift` I
+        in the first application."""
+        _check(lib().pe_set_rect_iteration(self._h, int(restart), float(min_aspect), float(shift)),
+               "pe_set_rect_iteration")
 
     def reserve(self, shapes, dtype=PE_BF16):
         _check(lib().pe_reserve(self._h, _shapes_arr(shapes), len(shapes), int(dtype)), "pe_reserve")

@@ -465,6 +465,48 @@ __global__ void __launch_bounds__(256) pe_upload_kernel(const uint4* __restrict_
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
+// ---------------------------------------------------------------- App. H
+// Fast rectangular iteration (Alg. 4): with Q_0 = I the first
+// iteration of an application is R_1 = Y and Q_1 = h_1(Y) = a_1 I + H_1,
+// H_1 = b_1 Y + c_1 Y^2 (the poly GEMM).  This pass writes Q_1 in full
+// storage (the later products read it as a plain m x m operand) from H_1's
+// upper-block-triangle storage: Q_1 = bf16(fp32(H_1) + a_1) on the diagonal,
+// H_1 elsewhere (blocks below the diagonal read transposed).  One 64 x 64
+// tile per block, through shared memory (coalesced both ways).
+struct ExpandArgs {
+  const CopyItem* items;       // (mat, tile row, tile col) of 64 x 64 tiles
+  int nitems;
+  const MatDev* mats;          // source mats[i].B (H_1), destination mats[i].E[0] (Q_1)
+  float a;
+};
+__global__ void __launch_bounds__(256) pe_expand_kernel(const ExpandArgs e) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ __nv_bfloat16 t[64][66];
+  for (int it = blockIdx.x; it < e.nitems; it += gridDim.x) {
+    const CopyItem ci = e.items[it];
+    const MatDev md = e.mats[ci.mat];
+    const int r0 = ci.a * 64, c0 = ci.b * 64;
+    const bool upper = (r0 / kBM) <= (c0 / kBM);
+    const int sr0 = upper ? r0 : c0, sc0 = upper ? c0 : r0;
+    const __nv_bfloat16* H = reinterpret_cast<const __nv_bfloat16*>(md.B);
+    __nv_bfloat16* Q = reinterpret_cast<__nv_bfloat16*>(md.E[0]);
+    __syncthreads();                                   // previous tile's reads of t are done
+    for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
+      const int i = k >> 6, j = k & 63, gr = sr0 + i, gc = sc0 + j;
+      t[i][j] = (gr < md.m && gc < md.m) ? H[(int64_t)gr * md.ldm + gc] : __float2bfloat16_rn(0.f);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
+      const int i = k >> 6, j = k & 63, gr = r0 + i, gc = c0 + j;
+      if (gr >= md.m || gc >= md.m) continue;
+      __nv_bfloat16 v = upper ? t[i][j] : t[j][i];
+      if (gr == gc) v = __float2bfloat16_rn(__fadd_rn(__bfloat162float(v), e.a));
+      Q[(int64_t)gr * md.ldm + gc] = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- App. G
 // Spectrum-aware first step (k = 1; reading R17): the power
 // method on A_0 = X_0 X_0^T (the iteration-1 Gram, bf16, upper 256-block
@@ -492,6 +534,8 @@ struct SymvArgs {
   unsigned* counters;        // per matrix, zero at rest (self-resetting)
   double* lam;               // per matrix: v.w / v.v
   double* nrm2_out;          // per matrix: w.w
+  float* const* a32;         // per matrix: the Gram in fp32 (upper blocks, leading dim ldm), read instead of
+                             // the bf16 A (the Rayleigh quotient of bf16(A) can exceed sigma_1^2, R17)
 };
 
 // w = A v for every matrix (one launch per power iteration).  A(r, c) with
@@ -510,6 +554,26 @@ __device__ __forceinline__ void symv_v8(const float* vin, float vs, int c, int m
   }
 }
 
+template <typename TA> __device__ __forceinline__ float symv_ld(const TA* p);
+template <> __device__ __forceinline__ float symv_ld<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <> __device__ __forceinline__ float symv_ld<float>(const float* p) { return *p; }
+// 8 consecutive elements (16 or 32 bytes, aligned) as floats
+__device__ __forceinline__ void symv_ld8(const __nv_bfloat16* p, float* f) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 t = __bfloat1622float2(h[q]);
+    f[2 * q] = t.x;
+    f[2 * q + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void symv_ld8(const float* p, float* f) {
+  const float4 x = *reinterpret_cast<const float4*>(p), y = *reinterpret_cast<const float4*>(p + 4);
+  f[0] = x.x; f[1] = x.y; f[2] = x.z; f[3] = x.w; f[4] = y.x; f[5] = y.y; f[6] = y.z; f[7] = y.w;
+}
+
+template <typename TA>
 __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a) {
   pdl_trigger();
   pdl_wait();
@@ -522,7 +586,7 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
     const int mat = a.item_mat[it], r0 = a.item_r0[it];
     const MatDev md = a.mats[mat];
     const int m = md.m, ld = md.ldm;
-    const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(md.A);
+    const TA* A = a.a32 ? reinterpret_cast<const TA*>(a.a32[mat]) : reinterpret_cast<const TA*>(md.A);
     const float* vin = a.vin + a.voff[mat];          // iteration 0: the start vector v0 (unnormalised)
     const float vs = a.nrm2_in ? (float)(1.0 / sqrt(a.nrm2_in[mat])) : 1.0f;
     auto v_at = [&](int c) { return vin[c] * vs; };
@@ -535,20 +599,16 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
 #pragma unroll 4
       for (int c = warp * 8 + (lane >> 2); c < cl; c += kW * 8) {
         const float vc = v_at(c);
-        const __nv_bfloat16* p = A + (size_t)c * ld + rs;
+        const TA* p = A + (size_t)c * ld + rs;
         if (full) {
-          const uint4 u = *reinterpret_cast<const uint4*>(p);
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+          float f[8];
+          symv_ld8(p, f);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f = __bfloat1622float2(h[q]);
-            acc[2 * q] += f.x * vc;
-            acc[2 * q + 1] += f.y * vc;
-          }
+          for (int q = 0; q < 8; ++q) acc[q] += f[q] * vc;
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            if (rs + k < m) acc[k] += __bfloat162float(p[k]) * vc;
+            if (rs + k < m) acc[k] += symv_ld<TA>(p + k) * vc;
         }
       }
       // lanes with the same segment hold the same rows: reduce over lane / 4
@@ -568,21 +628,18 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
       const int rr = r0 + warp * (kSymvRows / kW) + q;
       float acc = 0.f;
       if (rr < m) {
-        const __nv_bfloat16* row = A + (size_t)rr * ld;
+        const TA* row = A + (size_t)rr * ld;
 #pragma unroll 4
         for (int c = cl + 8 * lane; c < m; c += 256) {
           float v[8];
           symv_v8(vin, vs, c, m, v);
           if (c + 8 <= m) {
-            const uint4 u = *reinterpret_cast<const uint4*>(row + c);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+            float f[8];
+            symv_ld8(row + c, f);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __bfloat1622float2(h[k]);
-              acc += f.x * v[2 * k] + f.y * v[2 * k + 1];
-            }
+            for (int k = 0; k < 8; ++k) acc += f[k] * v[k];
           } else {
-            for (int k = 0; k < 8 && c + k < m; ++k) acc += __bfloat162float(row[c + k]) * v[k];
+            for (int k = 0; k < 8 && c + k < m; ++k) acc += symv_ld<TA>(row + c + k) * v[k];
           }
         }
       }
@@ -638,13 +695,17 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
 // Per matrix: z = sqrt(lambda / F^2), F^2 = ssq * inv^2 (= ||X_0||_F^2), and
 // the first step's (a/F, b/F^3) from eq. (init_poly), or (1, 0).
 __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const float* inv, float* mcoef,
-                                    int count, double margin) {
+                                    int count, double margin, const int* mflags) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
+  // lam is the Rayleigh quotient of the fp32 Gram the iteration-1 GEMM
+  // accumulated: of M M^T (unscaled) for folded matrices, of X_0 X_0^T for
+  // the others; z = sigma_1 / ||.||_F on the same scale
   const double f2 = ssq[i] * (double)inv[i] * (double)inv[i];
-  const double z = (f2 > 0.0 && lam[i] > 0.0) ? sqrt(lam[i] / f2) : 0.0;
+  const double den2 = (mflags[i] & 1) ? ssq[i] : f2;
+  const double z = (den2 > 0.0 && lam[i] > 0.0) ? sqrt(lam[i] / den2) : 0.0;
   float ca = 1.f, cb = 0.f;
   if (z >= 0.70710678118654752 && z <= 1.0 - 1e-6) {
     const double t = sqrt(1.0 - z * z);

@@ -101,6 +101,16 @@ struct GemmArgs {
   const float* mcoef;          // spectrum-aware first step (App. G): per matrix (a, b), c = 0; else nullptr
   int lin;                     // odd cubic step (degree-3 table, App. G step): no poly phase; the update
                                // reads A as its left operand and computes X' = a X + b (A X)
+  // Fast rectangular iteration (App. H, Alg. 4; plans built for it carry
+  // kMapsRect main-loop and kEmapsRect epilogue maps per matrix, see below)
+  int tstride, estride;        // main-loop / epilogue (per plane) maps per matrix: 6 / 4, or 11 / 8
+  float shift;                 // Gram: added to the diagonal after the scale (Alg. 4's 10^-3 I)
+  int psrc;                    // poly source: 0 = A (Y), 1 = R
+  int gen;                     // update phase as a generic product of Alg. 4 (the fields below), else 0
+  int g_l, g_lmn, g_lsym;      // left operand map (and its transposed-block map when symmetric-stored)
+  int g_rx, g_r;               // right operand: the iterate X (caller M when folded), else map g_r (MN-major)
+  int g_ein, g_eout;           // epilogue operand map (-1: none, result = acc) / result map (-1: the X logic)
+  int g_wide;                  // result columns: 1 = n (X-shaped), 0 = m (square)
   int dbg;                     // timing experiments only: 1 = no epilogue work, 2 = no operand loads,
                                // 8 = all loads hit the same boxes, 16 = no TMEM loads, 32 = no result
                                // stores, 256 = every result store to the same box, 2048 = right
@@ -135,6 +145,9 @@ struct TileCfg {
   bool scaled;                 // first iteration of a folded matrix
   bool muon;                   // result chunk is a Muon weight update of the chunk already at eout
   bool lin;                    // update of a cubic step: left operand A, epilogue a X + b acc
+  bool has_ein;                // the epilogue reads an operand chunk (poly: A/R, update: X/Q)
+  int ncols;                   // result columns (n for X-shaped results, m for square ones)
+  float shift;                 // Gram: diagonal shift
   int prow;                    // kP = 3: rows per plane of the stacked buffers (= m)
 };
 
@@ -145,8 +158,8 @@ struct TileCfg {
 template <bool kEdge, int kP = 1>
 __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, uint32_t rank) {
   const MatDev& md = g.mats[tl.mat];
-  const CUtensorMap* maps = g.tmaps + 6 * tl.mat;
-  const CUtensorMap* em = g.emaps + 4 * kP * tl.mat;
+  const CUtensorMap* maps = g.tmaps + g.tstride * tl.mat;
+  const CUtensorMap* em = g.emaps + g.estride * kP * tl.mat;
   TileCfg c;
   c.dep = nullptr;
   c.pub = nullptr;
@@ -185,6 +198,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   c.scaled = fold;
   c.muon = false;
   c.lin = false;
+  c.shift = 0.f;
   c.a_wide = c.b_wide = false;
   c.Amn = c.Bmn = nullptr;
   c.pan_a = tl.tm;
@@ -197,22 +211,36 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.a_mn = c.b_mn = fold && tall;
     c.nk = (md.n + kBK - 1) / kBK;
     c.eout = em + 2 * kP;
+    c.shift = g.nphase == 0 ? g.shift : 0.f;
   } else if (c.mode == kModePoly) {
-    c.A = c.B = maps + 2;
-    c.Amn = c.Bmn = maps + 4;
+    const bool r = g.nphase == 0 && g.psrc != 0;      // Alg. 4: h(R) from R (maps 9 / 10, emap 7)
+    c.A = c.B = maps + (r ? 9 : 2);
+    c.Amn = c.Bmn = maps + (r ? 10 : 4);
     c.a_mn = c.b_mn = false;
     c.a_wide = c.b_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
-    c.ein = em + 2 * kP;
+    c.ein = em + (r ? 7 : 2) * kP;
     c.eout = em + 3 * kP;
   } else {
+    const bool gen = g.nphase == 0 && g.gen != 0;
+    const bool rx = !gen || g.g_rx != 0;             // right operand is the iterate
+    c.scaled = fold && rx;
     c.lin = g.nphase == 0 && g.lin != 0;
-    c.A = maps + (c.lin ? 2 : 3);     // cubic: B = b A is never formed, the update reads A
-    c.Amn = maps + (c.lin ? 4 : 5);
+    if (gen) {
+      c.A = maps + g.g_l;
+      c.Amn = g.g_lsym ? maps + g.g_lmn : nullptr;
+      c.a_wide = g.g_lsym != 0;      // symmetric-stored (Y, H) or full (Q: K-major 64 x 64 boxes)
+    } else {
+      c.A = maps + (c.lin ? 2 : 3);   // cubic: B = b A is never formed, the update reads A
+      c.Amn = maps + (c.lin ? 4 : 5);
+      c.a_wide = true;
+    }
     c.a_mn = false;
-    c.a_wide = true;
     c.nk = (md.m + kBK - 1) / kBK;
-    if (fold) {
+    if (!rx) {
+      c.B = maps + g.g_r;
+      c.b_mn = true;
+    } else if (fold) {
       c.B = g.imaps + 2 * tl.mat;
       c.b_mn = !tall;                 // wide: M is N-contiguous; tall: M^T rows are M's rows (K-contiguous)
       c.ein = g.imaps + 2 * tl.mat + 1;
@@ -222,7 +250,13 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
       c.b_mn = true;
       c.ein = em + kP * c.xin;
     }
-    if (kEdge && c.last && (fl & kFlagDirect)) {
+    if (gen) {
+      c.ein = g.g_ein >= 0 ? em + kP * g.g_ein : nullptr;
+      if (c.ein == nullptr) c.ein_tr = false;
+    }
+    if (gen && g.g_eout >= 0) {
+      c.eout = em + kP * g.g_eout;
+    } else if (kEdge && c.last && (fl & kFlagDirect)) {
       c.eout = g.omaps + tl.mat;
       c.eout_tr = tall;
       c.muon = g.muon != 0;
@@ -230,6 +264,8 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
       c.eout = em + kP * (c.xin ^ 1);
     }
   }
+  c.has_ein = c.mode != kModeGram && c.ein != nullptr;
+  c.ncols = (c.mode == kModeUpdate && !(g.nphase == 0 && g.gen != 0 && !g.g_wide)) ? md.n : md.m;
   c.diag = (kP == 1) && (c.mode != kModeUpdate) && (tl.tm == tl.tn);
   c.prow = (kP == 1) ? 0 : md.m;
   c.row_a = tl.tm * kBM + (int)rank * (kBM / 2);
@@ -266,7 +302,8 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int j) { return r * 128 + (
 
 template <bool kEdge>
 __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& cfg, float inv, uint8_t* slot,
-                                             int lane, int half32, float* w, const uint32_t* pre) {
+                                             int lane, int half32, float* w, const uint32_t* pre, int dj) {
+  // dj: column (within these 32) of this row's diagonal element, if any (Gram shift)
   // pre != nullptr: the operand half was read into packed bf16 pairs before
   // any result of this chunk was written (mixed layouts, see caller)
   const bool tr_in = kEdge && cfg.ein_tr;
@@ -274,7 +311,13 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
 #pragma unroll
   for (int qq = 0; qq < 2; ++qq) {           // 16 columns at a time (register pressure)
     float* wq = w + 16 * qq;
-    if (cfg.mode != kModeGram) {
+    if (cfg.mode == kModeUpdate && !cfg.has_ein) {
+      // generic product of Alg. 4 with no epilogue operand: the result is acc
+      if (kEdge && cfg.scaled) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv);
+      }
+    } else if (cfg.mode != kModeGram) {
       float o[16];
       if (kEdge && pre != nullptr) {
 #pragma unroll
@@ -308,10 +351,17 @@ __device__ __forceinline__ void epilogue_math(const GemmArgs& g, const TileCfg& 
           for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv);
         }
       }
-    } else if (kEdge && cfg.scaled) {
-      const float inv2 = __fmul_rn(inv, inv);
+    } else {
+      if (kEdge && cfg.scaled) {
+        const float inv2 = __fmul_rn(inv, inv);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv2);
+        for (int j = 0; j < 16; ++j) wq[j] = __fmul_rn(wq[j], inv2);
+      }
+      if (cfg.shift != 0.f) {            // Alg. 4: Y = X X^T + shift I
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (16 * qq + j == dj) wq[j] = __fadd_rn(wq[j], cfg.shift);
+      }
     }
     if (kEdge && cfg.muon) {
       // Muon: the slot holds the weight chunk; W <- bf16(W - lr * bf16(X'))
@@ -439,7 +489,7 @@ __device__ __forceinline__ void epilogue_role_p3(const GemmArgs& args, uint8_t* 
     if (lane == 0 && need_load && cfg.dep != nullptr) acquire_counter(cfg.dep, cfg.dep_need);
     const int r0 = tl.tm * kBM + row_off;
     const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
-    const int ncols = (mode == kModeUpdate) ? md.n : md.m;
+    const int ncols = cfg.ncols;
     const int npass = p3_passes(cfg.nk);
     for (int ps = 0; ps < npass; ++ps) {
       // accumulator of the pass = buffer 0 (+ buffer 1 when the pass's big
@@ -727,16 +777,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     const int half = ew >> 2;
     uint8_t* slots = epi_smem + ew * kSl * kEpiSlotBytes;
     uint64_t* xbar = xbars + ew * kSl;
-    auto needs_load = [&](const TileCfg& c2) { return c2.mode != kModeGram && !(args.dbg & 3); };
+    auto needs_load = [&](const TileCfg& c2) { return c2.has_ein && !(args.dbg & 3); };
     const bool do_work = !(args.dbg & 1);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const int row_off = (int)rank * (kBM / 2) + q * 32;
 
     auto col0 = [&](const Tile& tl2, int kk) { return tl2.tn * kBN + half * (kBN / 2) + kk * kEpiCols; };
-    auto ncols_of = [&](const Tile& tl2, const TileCfg& c2) {
-      const MatDev& m2 = args.mats[tl2.mat];
-      return (c2.mode == kModeUpdate) ? m2.n : m2.m;
-    };
+    auto ncols_of = [&](const Tile&, const TileCfg& c2) { return c2.ncols; };
     auto issue_tile = [&](const Tile& tl2, const TileCfg& c2, int nc) {
       if (c2.dep != nullptr) acquire_counter(c2.dep, c2.dep_need);   // fused: the operand is complete
       const int r0 = tl2.tm * kBM + row_off;
@@ -779,7 +826,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       const int r0 = tl.tm * kBM + row_off;
       const int r = r0 + lane;
       const uint32_t t_row = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kBN / 2);
-      const int ncols = (cfg.mode == kModeUpdate) ? md.n : md.m;
+      const int ncols = cfg.ncols;
 #pragma unroll 1
       for (int k = 0; k < kEpiChunks; ++k) {
         const int c0 = col0(tl, k);
@@ -857,7 +904,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             if (c0 + 32 * h < ncols) {
               float w[32];
               tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
-              epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, pre[h]);
+              epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, pre[h], r - (c0 + 32 * h));
             }
           }
         } else {
@@ -871,7 +918,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             } else {
               tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
             }
-            epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr);
+            epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr, r - (c0 + 32 * h));
           }
         }
         {                                       // each chunk leaves as soon as it is done

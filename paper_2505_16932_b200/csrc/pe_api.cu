@@ -155,12 +155,20 @@ struct Plan {
   // per-item partials, per-matrix counters / lambda / ||w||^2 (x2) / sum of squares / (a, b)
   size_t o_sitem_mat = 0, o_sitem_r0 = 0, o_sitem0 = 0, o_snitem = 0, o_svoff = 0, o_sv = 0, o_sv0 = 0, o_spart = 0;
   size_t o_scnt = 0, o_slam = 0, o_snrm = 0, o_sssq = 0, o_smcoef = 0;
+  size_t o_a32 = 0;             // per matrix fp32 Gram (App. G plans, `init`), device pointers
+  bool init = false;
   int n_sitems = 0;
   int64_t sv_len = 0;
   // fused schedule (one launch for all 3T phases), built for one T at a time
   int fused_T = 0, n_fused = 0;
   Tile* fused = nullptr;
   size_t fused_cap = 0;
+  // fast rectangular iteration (App. H, Alg. 4): map strides, full m x m
+  // tile lists (both directions) and the Q_1 expansion items
+  bool rect = false;
+  int tstride = 6, estride = 4;
+  size_t o_sq = 0, o_sq_r = 0, o_exp = 0;
+  int n_sq = 0, n_exp = 0;
   size_t ws_needed = 0;
   uint64_t last_use = 0;
   bool pinned = false;          // used by a captured CUDA graph: kept (with its workspace) until pe_destroy
@@ -234,6 +242,11 @@ struct pe_ctx_s {
   PeDist* dist = nullptr;       // pe_attach_comm (pe_dist.cpp)
   int init_iters = 0;           // pe_set_spectrum_init: power iterations of App. G's first step (0 = off)
   double init_margin = 0.0078125;  // pe_set_spectrum_init_ex: R17's 1 / (1 + |b| margin) (0 = eq. (init_poly) exactly)
+  // pe_set_rect_iteration (App. H, Alg. 4): iterations per application (0 = off)
+  int rect_restart = 0;
+  double rect_min_aspect = 0.0;  // <= 0: the paper's rule alpha > 1.5 T / (T - 1)
+  double rect_shift = 1e-3;      // added to Y's diagonal in the first application
+  int rect_mode = 0;             // internal: 0 = split the batch by aspect, 1 = Listing 2 only, 2 = Alg. 4 only
 };
 
 PeDist*& pe_ctx_dist(pe_ctx c) { return c->dist; }
@@ -429,6 +442,14 @@ extern "C" pe_status pe_set_spectrum_init_ex(pe_ctx c, int power_iters, double m
   return PE_OK;
 }
 
+extern "C" pe_status pe_set_rect_iteration(pe_ctx c, int restart, double min_aspect, double shift) {
+  if (!c || restart < 0 || !(shift >= 0.0) || !(shift < 1.0) || std::isnan(min_aspect)) return PE_ERR_INVALID_ARG;
+  c->rect_restart = restart;
+  c->rect_min_aspect = min_aspect;
+  c->rect_shift = shift;
+  return PE_OK;
+}
+
 extern "C" pe_status pe_last_launch_count(pe_ctx c, int* n) {
   if (!c || !n) return PE_ERR_INVALID_ARG;
   *n = c->last_launches;
@@ -515,17 +536,21 @@ static size_t call_bytes(int count, int T) { return call_coef_off(count) + (size
 // workspace and the finalize pass copies out) -- a one-step call whose output
 // overlaps an input: that update reads the caller's M across whole column
 // panels while other tiles store, so a direct store would race (in == out).
-static std::vector<int64_t> plan_key(const int64_t* shapes, int count, bool no_orient, int io, bool no_direct) {
+static std::vector<int64_t> plan_key(const int64_t* shapes, int count, bool no_orient, int io, bool no_direct,
+                                     bool rect = false, bool init = false) {
   std::vector<int64_t> key(shapes, shapes + 2 * count);
   if (no_orient) key.push_back(-1);
   if (io) key.push_back(-2 - io);
   if (no_direct) key.push_back(-100);
+  if (rect) key.push_back(-200);
+  if (init) key.push_back(-300);
   return key;
 }
 
 static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype dtype, Plan** out,
-                            bool no_orient = false, int io = 0, bool no_direct = false) {
-  const std::vector<int64_t> key = plan_key(shapes, count, no_orient, io, no_direct);
+                            bool no_orient = false, int io = 0, bool no_direct = false, bool rect = false,
+                            bool init = false) {
+  const std::vector<int64_t> key = plan_key(shapes, count, no_orient, io, no_direct, rect, init);
   for (Plan* p : c->plans)
     if (p->dtype == dtype && p->key == key) {
       p->last_use = ++c->use_clock;
@@ -538,7 +563,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
 
   // workspace carve-up
   std::vector<MatDev> mats(count);
-  std::vector<size_t> offs(count * 4);
+  std::vector<size_t> offs(count * 9, 0);
   size_t total = 0;
   for (int i = 0; i < count; ++i) {
     MatDev& md = mats[i];
@@ -551,10 +576,12 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     md.ldm = (int)rup(md.m, 8);
     const size_t xb = rup(np * md.m * md.ldx * 2, 256);
     const size_t mb = rup(np * md.m * md.ldm * 2, 256);
-    offs[4 * i + 0] = total; total += xb;
-    offs[4 * i + 1] = total; total += xb;
-    offs[4 * i + 2] = total; total += mb;
-    offs[4 * i + 3] = total; total += mb;
+    offs[9 * i + 0] = total; total += xb;
+    offs[9 * i + 1] = total; total += xb;
+    offs[9 * i + 2] = total; total += mb;
+    offs[9 * i + 3] = total; total += mb;
+    for (int e = 0; e < 4 && rect; ++e) { offs[9 * i + 4 + e] = total; total += mb; }   // Q_0, Q_1, T, R
+    if (init) { offs[9 * i + 8] = total; total += rup((size_t)md.m * md.ldm * 4, 256); }  // fp32 Gram
   }
   pe_status s = ensure_workspace(c, std::max<size_t>(total, 256));
   if (s != PE_OK) return s;
@@ -563,12 +590,17 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   P->dtype = dtype;
   P->ws_needed = total;
   uint8_t* ws = reinterpret_cast<uint8_t*>(c->ws);
+  P->rect = rect;
+  P->tstride = rect ? 11 : 6;
+  P->estride = rect ? 8 : 4;
   for (int i = 0; i < count; ++i) {
-    mats[i].X[0] = ws + offs[4 * i + 0];
-    mats[i].X[1] = ws + offs[4 * i + 1];
-    mats[i].A = ws + offs[4 * i + 2];
-    mats[i].B = ws + offs[4 * i + 3];
+    mats[i].X[0] = ws + offs[9 * i + 0];
+    mats[i].X[1] = ws + offs[9 * i + 1];
+    mats[i].A = ws + offs[9 * i + 2];
+    mats[i].B = ws + offs[9 * i + 3];
+    for (int e = 0; e < 4; ++e) mats[i].E[e] = rect ? ws + offs[9 * i + 4 + e] : nullptr;
   }
+  P->init = init;
 
   // GEMM tile lists: 256x256 pair tiles, symmetric phases only I <= J.
   // Update tiles are generated row-block fastest so concurrently running
@@ -609,30 +641,52 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   };
   std::stable_sort(sym.begin(), sym.end(), by_k(true));
   std::stable_sort(upd.begin(), upd.end(), by_k(false));
+  // Alg. 4 plans: every 256 x 256 tile of the m x m products (T = Y Q,
+  // Q' = a Q + H Q), and the 64 x 64 tiles of the Q_1 expansion
+  std::vector<Tile> sq;
+  std::vector<CopyItem> exp_items;
+  for (int i = 0; i < count && rect; ++i) {
+    const int nm = cdiv(mats[i].m, tile);
+    for (int tm = 0; tm < nm; ++tm)
+      for (int tn = 0; tn < nm; ++tn) sq.push_back({i, tm, tn, 0});
+    for (int a = 0; a < cdiv(mats[i].m, 64); ++a)
+      for (int b = 0; b < cdiv(mats[i].m, 64); ++b) exp_items.push_back({i, a, b, 0});
+  }
+  std::stable_sort(sq.begin(), sq.end(), by_k(false));
 
   // tensor maps: main loop over all planes of a buffer stacked (plane p =
   // rows [p m, (p+1) m)), epilogue one map per plane (stores clip at row m)
   // (A and B: 128-row boxes for the stored blocks, 64x64 boxes for the
   // transposed reads of the blocks below the diagonal, gemm_sm100.cuh)
-  std::vector<CUtensorMap> tmaps(6 * (size_t)count), emaps(4 * np * (size_t)count);
+  // Alg. 4 plans add main-loop maps 6 Q_0, 7 Q_1, 8 T (64 x 64 boxes: read
+  // K-major as a left operand or MN-major as a right one), 9 / 10 R (as A),
+  // and epilogue maps 4 Q_0, 5 Q_1, 6 T, 7 R
+  const int ts = P->tstride, es = P->estride;
+  std::vector<CUtensorMap> tmaps(ts * (size_t)count), emaps(es * np * (size_t)count);
   for (int i = 0; i < count; ++i) {
     const MatDev& md = mats[i];
     const int pr = (int)np * md.m;
-    if ((s = make_tmap(&tmaps[6 * i + 0], md.X[0], pr, md.n, md.ldx)) != PE_OK ||
-        (s = make_tmap(&tmaps[6 * i + 1], md.X[1], pr, md.n, md.ldx)) != PE_OK ||
-        (s = make_tmap(&tmaps[6 * i + 2], md.A, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
-        (s = make_tmap(&tmaps[6 * i + 3], md.B, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
-        (s = make_tmap(&tmaps[6 * i + 4], md.A, pr, md.m, md.ldm)) != PE_OK ||
-        (s = make_tmap(&tmaps[6 * i + 5], md.B, pr, md.m, md.ldm)) != PE_OK) {
+    CUtensorMap* tm = &tmaps[(size_t)ts * i];
+    if ((s = make_tmap(&tm[0], md.X[0], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tm[1], md.X[1], pr, md.n, md.ldx)) != PE_OK ||
+        (s = make_tmap(&tm[2], md.A, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
+        (s = make_tmap(&tm[3], md.B, pr, md.m, md.ldm, 64, 128)) != PE_OK ||
+        (s = make_tmap(&tm[4], md.A, pr, md.m, md.ldm)) != PE_OK ||
+        (s = make_tmap(&tm[5], md.B, pr, md.m, md.ldm)) != PE_OK ||
+        (rect && ((s = make_tmap(&tm[6], md.E[0], md.m, md.m, md.ldm)) != PE_OK ||
+                  (s = make_tmap(&tm[7], md.E[1], md.m, md.m, md.ldm)) != PE_OK ||
+                  (s = make_tmap(&tm[8], md.E[2], md.m, md.m, md.ldm)) != PE_OK ||
+                  (s = make_tmap(&tm[9], md.E[3], md.m, md.m, md.ldm, 64, 128)) != PE_OK ||
+                  (s = make_tmap(&tm[10], md.E[3], md.m, md.m, md.ldm)) != PE_OK))) {
       delete P;
       return s;
     }
-    void* bufs[4] = {md.X[0], md.X[1], md.A, md.B};
-    for (int b = 0; b < 4; ++b) {
+    void* bufs[8] = {md.X[0], md.X[1], md.A, md.B, md.E[0], md.E[1], md.E[2], md.E[3]};
+    for (int b = 0; b < es; ++b) {
       const int cols = (b < 2) ? md.n : md.m, ld = (b < 2) ? md.ldx : md.ldm;
       for (size_t p = 0; p < np; ++p) {
         void* base = reinterpret_cast<uint8_t*>(bufs[b]) + p * md.m * ld * 2;
-        if ((s = make_emap(&emaps[(4 * i + b) * np + p], base, md.m, cols, ld)) != PE_OK) {
+        if ((s = make_emap(&emaps[((size_t)es * i + b) * np + p], base, md.m, cols, ld)) != PE_OK) {
           delete P;
           return s;
         }
@@ -706,6 +760,14 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
   std::vector<Tile> sym_r(sym.rbegin(), sym.rend()), upd_r(upd.rbegin(), upd.rend());
   P->o_sym_r = bl.add(sym_r);
   P->o_upd_r = bl.add(upd_r);
+  if (rect) {
+    std::vector<Tile> sq_r(sq.rbegin(), sq.rend());
+    P->o_sq = bl.add(sq);
+    P->o_sq_r = bl.add(sq_r);
+    P->o_exp = bl.add(exp_items);
+    P->n_sq = (int)sq.size();
+    P->n_exp = (int)exp_items.size();
+  }
   for (int k = 0; k < 4; ++k) P->o_it[k] = bl.add(it[k]);
   P->o_smats = bl.add(smats);
   P->o_fmats = bl.add(fmats);
@@ -760,6 +822,9 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     P->o_snrm = bl.add(std::vector<double>(2 * (size_t)count, 0.0));
     P->o_sssq = bl.add(std::vector<double>(count, 0.0));
     P->o_smcoef = bl.add(std::vector<float>(2 * (size_t)count, 0.f));
+    std::vector<float*> a32(count, nullptr);
+    for (int i = 0; i < count && init; ++i) a32[i] = reinterpret_cast<float*>(ws + offs[9 * i + 8]);
+    P->o_a32 = bl.add(a32);
     P->n_sitems = (int)imat.size();
     P->sv_len = vlen;
   }
@@ -1150,16 +1215,63 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   if (io && (dtype != PE_BF16 || muon || sh)) return PE_ERR_UNSUPPORTED;
   // App. G first step (pe_set_spectrum_init): bf16 pe_polar / pe_polar_ex, large path
   const bool init = c->init_iters > 0 && dtype == PE_BF16 && !muon && !sh;
-  if (!muon && !sh && !io && !init && small_eligible(shapes, count, dtype, &max_npad))
+  // App. H fast rectangular iteration (pe_set_rect_iteration): the matrices
+  // whose aspect ratio passes the threshold run Alg. 4, the
+  // others Listing 2; a mixed batch becomes two grouped calls on the stream
+  const bool rect_ok = c->rect_restart > 0 && dtype == PE_BF16 && !muon && !sh && !init && c->degree == 5;
+  if (rect_ok && c->rect_mode == 0) {
+    const double thr = c->rect_min_aspect > 0.0 ? c->rect_min_aspect
+                       : (iters > 1 ? 1.5 * iters / (iters - 1) : 1e300);
+    std::vector<int> ri, bi;
+    for (int i = 0; i < count; ++i) {
+      const double m = (double)std::min(shapes[2 * i], shapes[2 * i + 1]);
+      const double n = (double)std::max(shapes[2 * i], shapes[2 * i + 1]);
+      ((m > kSmallMaxM && n > thr * m) ? ri : bi).push_back(i);
+    }
+    if (!ri.empty()) {
+      if (capturing) {
+        g_last_error = "pe_set_rect_iteration: Alg. 4 calls are not capturable";
+        return PE_ERR_UNSUPPORTED;
+      }
+      int launches = 0;
+      for (int part = 0; part < 2; ++part) {
+        const std::vector<int>& idx = part == 0 ? bi : ri;
+        if (idx.empty()) continue;
+        std::vector<const void*> pin;
+        std::vector<void*> pout;
+        std::vector<int64_t> psh;
+        for (int i : idx) {
+          pin.push_back(in[i]);
+          pout.push_back(out[i]);
+          psh.push_back(shapes[2 * i]);
+          psh.push_back(shapes[2 * i + 1]);
+        }
+        c->rect_mode = part == 0 ? 1 : 2;
+        s = polar_impl(c, pin.data(), pout.data(), nullptr, psh.data(), (int)idx.size(), iters, dtype, stream_,
+                       beta, lr, up, nullptr, io);
+        c->rect_mode = 0;
+        if (s != PE_OK) return s;
+        launches += c->last_launches;
+      }
+      c->last_launches = launches;
+      return PE_OK;
+    }
+  }
+  const bool rect = rect_ok && c->rect_mode == 2;
+  const int T_ = iters;
+  const int rk = rect ? std::min(c->rect_restart, T_) : 1;    // iterations per application
+  const int nblocks = rect ? (T_ + rk - 1) / rk : 0;
+  if (!muon && !sh && !io && !init && !rect && small_eligible(shapes, count, dtype, &max_npad))
     return small_call(c, in, out, shapes, count, iters, dtype, st, capturing, max_npad, up);
   // one-step call (T = 1 without the App. G step): its only update reads the
   // caller's inputs while storing results, so an output overlapping any input
   // goes through the workspace and the finalize pass
-  const bool no_direct = (iters + (init ? 1 : 0) == 1) && outputs_overlap_inputs(in, out, shapes, count, dtype, io);
+  const bool no_direct = (rect ? nblocks == 1 : iters + (init ? 1 : 0) == 1) &&
+                         outputs_overlap_inputs(in, out, shapes, count, dtype, io);
   Plan* P = nullptr;
   if (capturing) {
     // no allocation or synchronisation is allowed: the plan must be cached
-    const std::vector<int64_t> key = plan_key(shapes, count, false, io, no_direct);
+    const std::vector<int64_t> key = plan_key(shapes, count, false, io, no_direct, rect, init);
     for (Plan* q : c->plans)
       if (q->dtype == dtype && q->key == key) P = q;
     if (!P || (dtype == PE_FP32 && !c->scratch)) {
@@ -1168,20 +1280,20 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     }
     P->last_use = ++c->use_clock;
     P->pinned = true;       // the graph keeps pointers into it: never evicted or freed before pe_destroy
-  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr, io, no_direct)) != PE_OK) {
+  } else if ((s = build_plan(c, shapes, count, dtype, &P, sh != nullptr, io, no_direct, rect, init)) != PE_OK) {
     return s;
   }
 
   // per-call pointers: [in | outs_direct | fin_src | out] + caller tensor maps
   const int T = iters;
   const int S = T + (init ? 1 : 0);     // GEMM steps: [App. G step] + T iterations
-  const int xfinal = S & 1;
+  const int xfinal = (rect ? nblocks : S) & 1;   // Alg. 4: one X-producing step per application
   // fused schedule: every GEMM phase in one launch (bf16, opt-in with
   // PE_FUSED=1; measured equal to one launch per phase on the GPT-2 sets and
   // within noise on Llama, profiles/r1_variants.md)
   static const bool fused_on = getenv("PE_FUSED") && strcmp(getenv("PE_FUSED"), "0") != 0;
   const int nq = (c->degree + 1) / 2;
-  const bool fused = fused_on && dtype == PE_BF16 && !capturing && !sh && !init && nq == 3;   // (its setup may synchronise)
+  const bool fused = fused_on && dtype == PE_BF16 && !capturing && !sh && !init && !rect && nq == 3;   // (its setup may synchronise)
   if (fused) {
     if ((s = ensure_fused(c, P, T)) != PE_OK) return s;
     const size_t need_done = (size_t)count * 3 * T;
@@ -1351,6 +1463,13 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     g.stats = nullptr;
     g.mcoef = nullptr;
     g.lin = 0;
+    g.tstride = P->tstride;
+    g.estride = P->estride;
+    g.shift = 0.f;
+    g.psrc = 0;
+    g.gen = 0;
+    g.g_l = g.g_lmn = g.g_lsym = g.g_rx = g.g_r = g.g_wide = 0;
+    g.g_ein = g.g_eout = -1;
   };
   if (fused) {
     // one persistent launch: all 3T phases of all matrices, dataflow-ordered
@@ -1366,7 +1485,115 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     launch(pe_gemm_sm100<kLongStages, kOpSlots, true>, grid, kGemmThreads, gemm_smem_bytes<kLongStages, kOpSlots>(), st, g);
     ++launches;
   }
-  for (int sidx = 0; sidx < S && !fused; ++sidx) {
+  if (rect) {
+    // Alg. 4 in applications of rk iterations (restarts,
+    // P:1337-1341).  Workspace per matrix (wide orientation, m <= n):
+    // A = Y, B = H, E[0] / E[1] = Q (ping-pong), E[2] = T = Y Q, E[3] = R.
+    // Main-loop maps: 2 / 4 A, 3 / 5 B, 6 / 7 Q, 8 T, 9 / 10 R; epilogue
+    // maps: 2 A, 3 B, 4 / 5 Q, 6 T, 7 R (gemm_sm100.cuh GemmArgs).
+    auto coef_t = [&](int t, float* f) {
+      const double* tup = &c->table[(size_t)std::min(t, c->ntab - 1) * nq];
+      f[0] = (float)tup[0]; f[1] = (float)tup[1]; f[2] = (float)tup[2];
+    };
+    auto run = [&](GemmArgs& g, const Tile* tiles, int ntiles, bool edge, int kind) {
+      g.tiles = tiles;
+      g.ntiles = ntiles;
+      const int grid = 2 * std::min(ntiles, c->num_sms / 2);
+      ProfScope ps(c, kind, st);
+      if (g.mode == kModeGram) {
+        const size_t sm = gemm_smem_bytes<kGramStages, 1>();
+        if (edge) launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kGramStages, 1, false>, grid, kGemmThreads, sm, st, g);
+      } else {
+        const size_t sm = gemm_smem_bytes<kLongStages, kOpSlots>();
+        if (edge) launch(pe_gemm_sm100<kLongStages, kOpSlots, true>, grid, kGemmThreads, sm, st, g);
+        else launch(pe_gemm_sm100<kLongStages, kOpSlots, false>, grid, kGemmThreads, sm, st, g);
+      }
+      ++launches;
+    };
+    const Tile* sym_f = at<Tile>(P, P->o_sym);
+    const Tile* sym_r = at<Tile>(P, P->o_sym_r);
+    const Tile* sq_f = at<Tile>(P, P->o_sq);
+    const Tile* sq_r = at<Tile>(P, P->o_sq_r);
+    int ph = 0;                                    // phase counter: alternate the tile-list direction
+    for (int b = 0, t0 = 0; b < nblocks; ++b, t0 += rk) {
+      const int kb = std::min(rk, T - t0);
+      const bool firstb = (b == 0), lastb = (b == nblocks - 1);
+      const int xin = b & 1;
+      float f[3];
+      coef_t(t0, f);
+      {  // Y = X X^T (+ shift I in the first application)
+        GemmArgs g;
+        base_args(g);
+        g.mode = kModeGram; g.xin = xin; g.first_iter = firstb; g.final_iter = 0;
+        g.a = f[0]; g.b = f[1]; g.c = f[2];
+        g.shift = firstb ? (float)c->rect_shift : 0.f;
+        run(g, (ph++ & 1) ? sym_r : sym_f, P->n_sym, firstb, 2);
+      }
+      {  // H_1 = b_1 Y + c_1 Y^2 (R_1 = Y since Q_0 = I)
+        GemmArgs g;
+        base_args(g);
+        g.mode = kModePoly; g.xin = xin; g.first_iter = 0; g.final_iter = 0;
+        g.a = f[0]; g.b = f[1]; g.c = f[2];
+        run(g, (ph++ & 1) ? sym_r : sym_f, P->n_sym, false, 3);
+      }
+      if (kb == 1) {
+        // a one-iteration application is Listing 2's step: X' = a X + H X
+        GemmArgs g;
+        base_args(g);
+        g.mode = kModeUpdate; g.xin = xin; g.first_iter = firstb; g.final_iter = lastb;
+        g.a = f[0]; g.b = f[1]; g.c = f[2];
+        run(g, at<Tile>(P, (ph++ & 1) ? P->o_upd_r : P->o_upd), P->n_upd, firstb || lastb, 4);
+        continue;
+      }
+      {  // Q_1 = a_1 I + H_1, full storage
+        ExpandArgs ea;
+        ea.items = at<CopyItem>(P, P->o_exp);
+        ea.nitems = P->n_exp;
+        ea.mats = at<MatDev>(P, P->o_mats);
+        ea.a = f[0];
+        ProfScope ps(c, 1, st);
+        launch(pe_expand_kernel, std::min(P->n_exp, c->num_sms * 8), 256, 0, st, ea);
+        ++launches;
+      }
+      int q = 0;                                   // Q_{t-1} lives in E[q]
+      for (int j = 1; j < kb; ++j) {
+        coef_t(t0 + j, f);
+        GemmArgs g;
+        // T = Y Q (first half of R_t = Q^T Y Q)
+        base_args(g);
+        g.mode = kModeUpdate; g.xin = xin; g.first_iter = 0; g.final_iter = 0; g.a = 0.f;
+        g.gen = 1; g.g_l = 2; g.g_lmn = 4; g.g_lsym = 1; g.g_rx = 0; g.g_r = 6 + q; g.g_ein = -1; g.g_eout = 6;
+        g.g_wide = 0;
+        run(g, (ph++ & 1) ? sq_r : sq_f, P->n_sq, false, 4);
+        // R = Q T (symmetric: upper block triangle only)
+        base_args(g);
+        g.mode = kModeUpdate; g.xin = xin; g.first_iter = 0; g.final_iter = 0; g.a = 0.f;
+        g.gen = 1; g.g_l = 6 + q; g.g_lsym = 0; g.g_rx = 0; g.g_r = 8; g.g_ein = -1; g.g_eout = 7; g.g_wide = 0;
+        run(g, (ph++ & 1) ? sym_r : sym_f, P->n_sym, false, 4);
+        // H = b R + c R^2 (Horner's inner part)
+        base_args(g);
+        g.mode = kModePoly; g.xin = xin; g.first_iter = 0; g.final_iter = 0;
+        g.a = f[0]; g.b = f[1]; g.c = f[2]; g.psrc = 1;
+        run(g, (ph++ & 1) ? sym_r : sym_f, P->n_sym, false, 3);
+        // Q_t = Q_{t-1} h_t(R_t) = a Q + H Q (H and Q commute in exact arithmetic)
+        base_args(g);
+        g.mode = kModeUpdate; g.xin = xin; g.first_iter = 0; g.final_iter = 0; g.a = f[0];
+        g.gen = 1; g.g_l = 3; g.g_lmn = 5; g.g_lsym = 1; g.g_rx = 0; g.g_r = 6 + q; g.g_ein = 4 + q;
+        g.g_eout = 4 + (q ^ 1); g.g_wide = 0;
+        run(g, (ph++ & 1) ? sq_r : sq_f, P->n_sq, false, 4);
+        q ^= 1;
+      }
+      {  // X' = Q X (P:1312 in the wide orientation: the result is Q_T^T X^T's transpose)
+        GemmArgs g;
+        base_args(g);
+        g.mode = kModeUpdate; g.xin = xin; g.first_iter = firstb; g.final_iter = lastb; g.a = 0.f;
+        g.gen = 1; g.g_l = 6 + q; g.g_lsym = 0; g.g_rx = 1; g.g_ein = -1; g.g_eout = -1; g.g_wide = 1;
+        run(g, at<Tile>(P, (ph++ & 1) ? P->o_upd_r : P->o_upd), P->n_upd, firstb || lastb, 4);
+      }
+    }
+  }
+  for (int sidx = 0; sidx < S && !fused && !rect; ++sidx) {
     // step sidx: the App. G first step (init, sidx == 0) or iteration t
     const bool istep = init && sidx == 0;
     const int t = sidx - (init ? 1 : 0);
@@ -1396,6 +1623,18 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       }
       const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
       if (sh && mode == kModeGram) g.out32 = c->sh_ptr;         // partial Gram in fp32
+      if (istep && mode == kModeGram) {
+        // App. G: the Gram once more with its raw fp32 accumulator stored, for
+        // the power method (its Rayleigh quotient on bf16(A_0) can exceed
+        // sigma_1^2 by ~2^-9 relative, which breaks z <= sigma_1
+        // and with it the tail bound sqrt(1 - z^2): R17)
+        GemmArgs g32 = g;
+        g32.out32 = at<float*>(P, P->o_a32);
+        ProfScope ps(c, 2, st);
+        const size_t sm = gemm_smem_bytes<kGramStages, 1>();
+        launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g32);
+        ++launches;
+      }
       {
       ProfScope ps(c, 2 + mode, st);
       const bool edge = (sidx == 0) || (sidx == S - 1);
@@ -1425,6 +1664,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         sa.part = at<double>(P, P->o_spart);
         sa.counters = at<unsigned>(P, P->o_scnt);
         sa.lam = at<double>(P, P->o_slam);
+        sa.a32 = at<float*>(P, P->o_a32);
         float* vb = at<float>(P, P->o_sv);
         double* nb = at<double>(P, P->o_snrm);
         const int sgrid = std::min(P->n_sitems, c->num_sms * 8);
@@ -1433,12 +1673,12 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
           sa.nrm2_in = (k == 0) ? nullptr : nb + (size_t)((k - 1) & 1) * count;
           sa.wout = vb + (size_t)(k & 1) * P->sv_len;
           sa.nrm2_out = nb + (size_t)(k & 1) * count;
-          launch(pe_symv_kernel, sgrid, kSymvThreads, 0, st, sa);
+          launch(pe_symv_kernel<float>, sgrid, kSymvThreads, 0, st, sa);
           ++launches;
         }
         launch(pe_init_coef_kernel, cdiv(count, 128), 128, 0, st, (const double*)sa.lam,
                (const double*)at<double>(P, P->o_sssq), (const float*)at<float>(P, P->o_inv),
-               at<float>(P, P->o_smcoef), count, c->init_margin);
+               at<float>(P, P->o_smcoef), count, c->init_margin, (const int*)at<int>(P, P->o_flags));
         ++launches;
       }
       if (sh && mode == kModeGram) {

@@ -35,6 +35,8 @@ struct MatDev {
   int rows, cols;    // caller's shape
   int tall;          // rows > cols: caller matrix is X^T
   int pad;
+  void* E[4];        // fast rectangular iteration (App. H, Alg. 4) plans: Q_0, Q_1 (ping-pong Q,
+                     // full m x m), T = Y Q (full), R = Q^T Y Q (symmetric); else nullptr
 };
 
 // One output tile of a GEMM phase (units: kBM rows, kBN columns).

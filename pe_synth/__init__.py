@@ -97,12 +97,18 @@ def sylvester_hadamard(n):
     return H
 
 
-def hadamard_rows(rows, cols):
+def hadamard_rows(rows, cols, dtype=np.float64):
     """First min(rows,cols) rows of H_max: all singular values equal to
     sqrt(max(rows, cols)); entries +-1 (exact in bf16).  Tall shapes are the
-    transpose."""
+    transpose.  Built entry-wise from H[i, j] = (-1)^popcount(i & j) (the
+    Sylvester recursion), so large shapes need only the m x n result."""
     m, n = min(rows, cols), max(rows, cols)
-    H = sylvester_hadamard(n)[:m, :]
+    assert n >= 1 and (n & (n - 1)) == 0
+    i = np.arange(m, dtype=np.uint32)[:, None]
+    H = np.empty((m, n), dtype=dtype)
+    for j0 in range(0, n, 4096):
+        par = np.bitwise_count(i & np.arange(j0, min(n, j0 + 4096), dtype=np.uint32)[None, :]) & 1
+        H[:, j0:j0 + par.shape[1]] = 1.0 - 2.0 * par
     return H if rows <= cols else H.T.copy()
 
 

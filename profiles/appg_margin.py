@@ -37,7 +37,28 @@ def run(c, M, T):
     return y.float().cpu().numpy().astype(np.float64)
 
 
+def sweep_m():
+    """Smallest safe margin per size: sigma_j = j^-5 (z ~ 0.9995, |b| ~ 30),
+    margins k * 2^-7 / sqrt(m)."""
+    c = pe.Context(0)
+    for m in (8, 16, 32, 64, 128, 256, 512, 1024):
+        for seed in (11, 12, 13):
+            M = syn.to_bf16_values(spiked(m, 3 * m, seed, law=5.0)).astype(np.float64)
+            P = oi.exact_polar(M)
+            ref, z, applied = oi.polar_express_init(M, TABLE, 5, power_iters=8)
+            line = [f"m={m} seed={seed} z={z:.6f} oracle {om.rel_frobenius(ref, P):.4f}"]
+            for k in (0.0, 0.125, 0.25, 0.5, 1.0, 2.0):
+                c.set_spectrum_init(8, k * 2.0 ** -7 / np.sqrt(m))
+                X = run(c, M, 5)
+                fin = np.all(np.isfinite(X)) and np.abs(X).max() < 1e3
+                line.append(f"k={k}: " + (f"{om.rel_frobenius(X, P):.4f}" if fin else "DIVERGED"))
+            print(" | ".join(line), flush=True)
+    c.close()
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "sweep":
+        return sweep_m()
     rng = np.random.default_rng(3)
     cases = [("32x32 j^-5", spiked(32, 32, 11, law=5.0), (4, 5)),
              ("256x512 j^-3", spiked(256, 512, 11, law=3.0), (4, 5)),
