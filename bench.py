@@ -153,7 +153,34 @@ class ClockSampler:
 
 def layer_set(name):
     import pe_synth as syn
-    return syn.layer_set_shapes(name)
+    return syn.layer_set_shapes(name.split(":")[0])
+
+
+def rect_restart(name):
+    """'<set>:alg4r<k>' runs the set with App. H's Alg. 4 (pe_set_rect_iteration,
+    restart every k iterations, shift 1e-3) on the matrices past the aspect
+    rule alpha > 1.5 T / (T - 1); 0 = Listing 2."""
+    tag = name.split(":")[1] if ":" in name else ""
+    return int(tag[len("alg4r"):]) if tag.startswith("alg4r") else 0
+
+
+def alg4_flops(shapes, T, restart):
+    """Algorithmic flops of a call with Alg. 4 on the qualifying matrices
+    (symmetric products counted once): per application
+    3 l s^2 (Y, X Q) + s^3 (h_1's square) + 6 s^3 per further iteration
+    (Y Q, Q^T (Y Q) upper half, R^2, H Q); the others pe_flops' count."""
+    thr = 1.5 * T / (T - 1) if T > 1 else float("inf")
+    f = 0.0
+    for r, c in shapes:
+        s_, l_ = min(r, c), max(r, c)
+        if restart > 0 and s_ > 128 and l_ > thr * s_:
+            k = min(restart, T)
+            for t0 in range(0, T, k):
+                kb = min(k, T - t0)
+                f += 3.0 * l_ * s_ * s_ + s_ ** 3 + 6.0 * (kb - 1) * s_ ** 3
+        else:
+            f += T * (s_ * (s_ + 1) * l_ + s_ * s_ * (s_ + 1) + 2.0 * s_ * s_ * l_)
+    return f
 
 
 def make_inputs(shapes, idx, device, seed=0):
@@ -314,10 +341,10 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dist_on, clocks=None):
+def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dist_on, clocks=None, rect=0):
     """Device-timed steps of one layer set; returns per-step ms list, profile, extras."""
     import torch
-    import paper_2505_16932_b200 as pe
+    import paper_2505_16932_b200 as pe  # noqa: F401
     from paper_2505_16932_b200 import dist as pdist
     idx, owner = pdist.owned(shapes, rank, world) if world > 1 else (list(range(len(shapes))), [0] * len(shapes))
     xs = make_inputs(shapes, idx, device)
@@ -329,10 +356,14 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
         xin = [None] * len(shapes)
         for i, x in zip(idx, xs):
             xin[i] = x
-        ys = [torch.empty(s_, dtype=torch.bfloat16, device=device) for s_ in shapes]
+        # outputs in the pe_shard_layout buffer: each rank's last update
+        # epilogues write its chunk, one in-place all-gather per bucket
+        _flat, ys = pdist.sharded_outputs(shapes, world, torch.bfloat16, device)
     else:
         ys = [torch.empty_like(x) for x in xs]
     ctx.reserve([shapes[i] for i in idx])
+    if rect:
+        ctx.set_rect_iteration(rect, 0.0, 1e-3)
     stream = torch.cuda.current_stream(device)
 
     def step():
@@ -382,7 +413,7 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
     ms, _ = timed(False)
     _, prof = timed(True)
     graph_ms = None
-    if not (dist_on and world > 1):
+    if not (dist_on and world > 1) and not rect:
         # the whole layer set replayed from one CUDA graph (the
         # reserved plan: no allocation or synchronisation while capturing)
         try:
@@ -404,9 +435,9 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
             graph_ms = str(e)[:200]
     if dist_on and world > 1:
         # SURVEY §8(d) multi-GPU: the compute span (this rank's pe_polar on its
-        # share) and the exchange span in isolation (one NCCL broadcast per
-        # matrix from its owner, through torch.distributed on the same
-        # buffers), next to the overlapped pe_polar_sharded step above
+        # share) and the exchange span in isolation (pe_sharded_exchange: the
+        # library's own per-bucket all-gathers on the same buffers), next to
+        # the overlapped pe_polar_sharded step above
         ys_own = [ys[i] for i in idx]
 
         def span(fn, reps=max(3, steps)):
@@ -425,15 +456,15 @@ def time_workload(ctx, shapes, T, steps, warmup, world, rank, device, flush, dis
             return round(float(t.item()), 4)
 
         def exchange():
-            works = [torch.distributed.broadcast(y, src=owner[i], async_op=True) for i, y in enumerate(ys)]
-            for w in works:
-                w.wait()
+            ctx.sharded_exchange(ys, stream=stream)
 
         try:
             graph_ms = {"compute_ms": span(lambda: ctx.polar(xs, ys_own, iters=T, stream=stream)),
                         "exchange_ms": span(exchange),
-                        "note": "max over ranks of the median; exchange = one torch.distributed NCCL broadcast "
-                                "per matrix (not grouped); the timed step overlaps compute and exchange"}
+                        "buckets": pe.pe_shard_nbuckets(shapes, world),
+                        "note": "max over ranks of the median; exchange = pe_sharded_exchange (libpe's per-bucket "
+                                "in-place NCCL all-gathers over the pe_shard_layout buffer); the timed step "
+                                "overlaps compute and exchange"}
         except Exception as e:                       # reported, never fatal
             graph_ms = {"error": str(e)[:200]}
     return ms, prof, launches, idx, xs, ys, graph_ms
@@ -447,7 +478,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama3-8b")
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--extra", default="gpt2-small,gpt2-large", help="comma list of extra layer sets (N=1 only), or ''")
+    ap.add_argument("--extra", default="gpt2-small,gpt2-large,llama3-8b:alg4r3",
+                    help="comma list of extra layer sets (N=1 only; '<set>:alg4r<k>' = with App. H Alg. 4), or ''")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     _workload_name[0] = args.workload
@@ -512,7 +544,8 @@ def main():
         "config": {"workload": args.workload, "matrices": len(shapes), "T": T, "degree": DEGREE, "ell": ELL,
                    "coeffs": "pe_coeffs(1e-3,5,8,1.01) (Listing 2 table)",
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "parallelism": f"dp{world} (pe_polar_sharded: LPT shard + bucketed NCCL broadcasts)" if world > 1 else "single GPU"},
+                   "parallelism": f"dp{world} (pe_polar_sharded: bucket-balanced LPT shard + per-bucket in-place "
+                                  f"NCCL all-gather)" if world > 1 else "single GPU"},
         "tflops": round(tflops, 2), "tflops_unit": "TFLOP/s (algorithmic, symmetric-aware)",
         "frac_of_bf16_peak": round(tflops / peaks[peak_key], 4),
         "frac_of_bf16_peak_sustained": round(tflops / peaks["bf16_tflops_sustained"], 4),
@@ -541,16 +574,21 @@ def main():
             c2 = ClockSampler(local_rank)
             c2.start()
             st2 = 10
-            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, st2, 3, 1, 0, device, flush, False, c2)
+            rk = rect_restart(name)
+            ms2, prof2, l2, idx2, xs2, ys2, _ = time_workload(ctx2, sh, T, st2, 3, 1, 0, device, flush, False, c2,
+                                                              rect=rk)
             ck2 = c2.stop()
             m2 = sum(ms2) / len(ms2)
-            f2 = pe.pe_flops(sh, T, DEGREE)
+            f2 = alg4_flops(sh, T, rk) if rk else pe.pe_flops(sh, T, DEGREE)
             extras[name] = {"matrices": len(sh), "value": round(len(sh) / (m2 * 1e-3), 3), "unit": UNIT,
                             "ms_per_step": round(m2, 3), "steps": st2, "warmup": 3,
                             "tflops": round(f2 / (m2 * 1e-3) / 1e12, 2),
                             "frac_of_bf16_peak_sustained": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
                             "frac_of_bf16_peak_burst": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
-                            "roofline": roofline(prof2, sh, T, m2, peaks, src, name),
+                            "roofline": None if rk else roofline(prof2, sh, T, m2, peaks, src, name),
+                            "method": (f"App. H Alg. 4 (restart {rk}, shift 1e-3) on the matrices with aspect "
+                                       f"> 1.5 T / (T - 1); tflops from its own algorithmic count" if rk
+                                       else "Listing 2"),
                             "per_kernel_ms_per_step": {k: round(v[0] / st2, 4) for k, v in prof2.items()},
                             "clocks": ck2}
             del xs2, ys2

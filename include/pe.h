@@ -262,13 +262,15 @@ pe_status pe_polar_split(pe_ctx ctx, const void* in, void* out, int64_t rows, in
  * inputs with one large outlying singular value.  power_iters > 0 turns it
  * on for the context's later bf16 pe_polar / pe_polar_ex / pe_polar_host
  * calls (0 = off, the default): after Listing 2's normalisation X_0 = M / s,
- * power_iters steps of the power method on A_0 = X_0 X_0^T (deterministic
- * start vector v0_i = frac((i+1)/phi) + 0.5) give the Rayleigh quotient
- * lambda <= sigma_1(X_0)^2 and z = sqrt(lambda) / ||X_0||_F; when
+ * power_iters steps of the power method on A_0 = X_0 X_0^T in fp32
+ * (deterministic start vector v0_i = frac((i+1)/phi) + 0.5) give the
+ * Rayleigh quotient lambda <= sigma_1(X_0)^2 and z = sqrt(lambda) / ||X_0||_F;
+ * when
  * 1/sqrt(2) <= z <= 1 - 1e-6 the odd cubic p(x) = a x + b x^3 of
  * eq. (init_poly) (p(sqrt(1-z^2)) = p(z) = 1 on the unit-norm
  * scale) is applied before the T iterations, else the step is the identity.
- * Costs one extra Gram + update (+ power_iters passes over A_0); matrices run
+ * Costs two extra Grams (one stores the fp32 accumulator for the power
+ * method) + one update (+ power_iters passes over A_0); matrices run
  * on the large path (the small-matrix path is bypassed).  fp32 calls and
  * pe_muon_step ignore it.  Errors: PE_ERR_INVALID_ARG (NULL, power_iters < 0
  * or > 1000).
@@ -278,10 +280,13 @@ pe_status pe_set_spectrum_init(pe_ctx ctx, int power_iters);
 /*
  * Same, with the bf16 stabilisation margin of reading R17 made explicit: the
  * cubic of eq. (init_poly) is divided by 1 + |b| * margin.  margin = 0 applies
- * eq. (init_poly) exactly as P:1256-1263 states it (what the oracle computes);
- * pe_set_spectrum_init uses margin = 2^-7, which keeps p(sigma_1) <= 1.01
- * under the bf16 error (~|b| 2^-8) of the cancellation a s + b s^3 when z is
- * close to 1 (margin 0 diverges to NaN at z = 0.9995 in bf16).  Errors:
+ * eq. (init_poly) exactly as P:1256-1263 states it (what the oracle computes)
+ * and is what pe_set_spectrum_init uses.  z comes from the power method on
+ * the fp32 Gram of the first iteration (a second Gram launch that stores the
+ * raw accumulator): on the bf16 Gram the Rayleigh quotient can exceed
+ * sigma_1^2 by ~2^-9 relative, which breaks z <= sigma_1, lets
+ * the tail bound sqrt(1 - z^2) fall below sigma_2 and lifted sigma_2 past 1
+ * (NaN two iterations later); a margin > 0 is then a user choice.  Errors:
  * PE_ERR_INVALID_ARG (NULL, power_iters outside 0..1000, margin outside
  * [0, 1] or NaN).
  */
@@ -395,6 +400,16 @@ pe_status pe_attach_comm(pe_ctx ctx, const char id[128], int rank, int world);
 pe_status pe_comm_info(pe_ctx ctx, int* rank, int* world);
 pe_status pe_polar_sharded(pe_ctx ctx, const void* const* in, void* const* out, const int64_t* shapes,
                            int count, int iters, pe_dtype dtype, void* stream);
+
+/*
+ * The exchange step of pe_polar_sharded alone: every rank's out[i] for the
+ * matrices it owns (pe_shard_plan) already hold their results; the same
+ * buckets, collectives (all-gather over the pe_shard_layout buffer, else
+ * per-matrix broadcasts) and stream ordering bring every out[i] to every
+ * rank.  No compute.  Errors as pe_polar_sharded.
+ */
+pe_status pe_sharded_exchange(pe_ctx ctx, void* const* out, const int64_t* shapes, int count, pe_dtype dtype,
+                              void* stream);
 
 /*
  * Caller-supplied exchange instead of NCCL (virtual ranks, other transports).

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
     "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
-    "pe_set_rect_iteration",
+    "pe_set_rect_iteration", "pe_sharded_exchange",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -80,6 +80,7 @@ def lib():
         "pe_set_spectrum_init": (I, [P, I]),
         "pe_set_spectrum_init_ex": (I, [P, I, D]),
         "pe_set_rect_iteration": (I, [P, I, D, D]),
+        "pe_sharded_exchange": (I, [P, ctypes.POINTER(P), I64P, I, I, P]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -455,6 +456,25 @@ class Context:
             errs.clear()
             raise e
         _check(status, "pe_polar_sharded")
+        return outputs
+
+    def sharded_exchange(self, outputs, stream=None):
+        """pe_sharded_exchange: pe_polar_sharded's exchange step alone (the
+        owned outputs already hold their results)."""
+        import torch
+        n = len(outputs)
+        outs = (ctypes.c_void_p * max(n, 1))(*[y.data_ptr() for y in outputs])
+        shp = _shapes_arr([tuple(y.shape) for y in outputs])
+        if stream is None:
+            stream = torch.cuda.current_stream(outputs[0].device)
+        status = lib().pe_sharded_exchange(self._h, outs, shp, n, _dtype_code(outputs[0]),
+                                           ctypes.c_void_p(stream.cuda_stream))
+        errs = getattr(self, "_x_errors", None)
+        if errs:
+            e = errs[0]
+            errs.clear()
+            raise e
+        _check(status, "pe_sharded_exchange")
         return outputs
 
     def polar_host(self, inputs, outputs, iters=5, stream=None):

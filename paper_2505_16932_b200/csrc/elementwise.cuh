@@ -712,11 +712,11 @@ __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const 
     const double den = z * t * (2.0 * z * z - 1.0);
     const double F = sqrt(f2);
     const double a = (z * z * (z + t) - t) / den, b = (t - z) / den;
-    // reading R17 (product-side stabilisation, not part of eq. (init_poly)):
-    // divide by 1 + |b| * margin (default 2^-7) -- p(sigma_1) = a s + b s^3
-    // cancels (|a| ~ |b| ~ 1/t as z -> 1), and its bf16 error ~ |b| 2^-8 must
-    // not push sigma_1 past the table's 1.01 margin (margin 0: NaN at
-    // z = 0.9995); margin = 0 is the paper's step exactly
+    // optional margin (pe_set_spectrum_init_ex; default 0 = eq. (init_poly)
+    // exactly): divide by 1 + |b| * margin.  With z from the fp32 Gram the
+    // paper's step stays finite on every input tried (R17); an earlier z from
+    // the bf16 Gram overestimated sigma_1, lifted the tail past 1 and needed
+    // a 2^-7 margin to avoid NaN
     const double sc = 1.0 / (1.0 + fabs(b) * margin);
     ca = (float)(a * sc / F);
     cb = (float)(b * sc / (F * F * F));

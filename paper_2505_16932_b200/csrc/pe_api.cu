@@ -241,7 +241,7 @@ struct pe_ctx_s {
 
   PeDist* dist = nullptr;       // pe_attach_comm (pe_dist.cpp)
   int init_iters = 0;           // pe_set_spectrum_init: power iterations of App. G's first step (0 = off)
-  double init_margin = 0.0078125;  // pe_set_spectrum_init_ex: R17's 1 / (1 + |b| margin) (0 = eq. (init_poly) exactly)
+  double init_margin = 0.0;     // pe_set_spectrum_init_ex: 1 / (1 + |b| margin) (0 = eq. (init_poly) exactly, R17)
   // pe_set_rect_iteration (App. H, Alg. 4): iterations per application (0 = off)
   int rect_restart = 0;
   double rect_min_aspect = 0.0;  // <= 0: the paper's rule alpha > 1.5 T / (T - 1)
@@ -430,7 +430,7 @@ extern "C" pe_status pe_set_coeffs(pe_ctx c, const double* coeffs, int ntuples, 
 extern "C" pe_status pe_set_spectrum_init(pe_ctx c, int power_iters) {
   if (!c || power_iters < 0 || power_iters > 1000) return PE_ERR_INVALID_ARG;
   c->init_iters = power_iters;
-  c->init_margin = 0.0078125;
+  c->init_margin = 0.0;
   return PE_OK;
 }
 
@@ -955,7 +955,9 @@ extern "C" pe_status pe_reserve(pe_ctx c, const int64_t* shapes, int count, pe_d
   if (s != PE_OK) return s;
   PE_CUDA(cudaSetDevice(c->device));
   Plan* P = nullptr;
-  if ((s = build_plan(c, shapes, count, dtype, &P)) != PE_OK) return s;
+  // the plan a later call will look up (App. G plans carry the fp32 Gram)
+  const bool init = c->init_iters > 0 && dtype == PE_BF16;
+  if ((s = build_plan(c, shapes, count, dtype, &P, false, 0, false, false, init)) != PE_OK) return s;
   if (dtype == PE_FP32 && !c->scratch) {
     const size_t sb = (size_t)c->num_sms * (kBM / 2) * kBN * sizeof(float);
     if (cudaMalloc(&c->scratch, sb) != cudaSuccess) { cudaGetLastError(); return PE_ERR_WORKSPACE; }

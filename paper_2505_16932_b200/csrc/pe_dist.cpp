@@ -358,10 +358,10 @@ extern "C" pe_status pe_shard_buckets(const int64_t* shapes, int count, int nbuc
   return PE_OK;
 }
 
-extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
-                                      int count, int iters, pe_dtype dtype, void* stream_) {
+static pe_status sharded_impl(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
+                              int iters, pe_dtype dtype, void* stream_, bool compute) {
   if (!c || count < 0 || iters < 1 || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
-  if (count > 0 && (!in || !out || !shapes)) return PE_ERR_INVALID_ARG;
+  if (count > 0 && ((compute && !in) || !out || !shapes)) return PE_ERR_INVALID_ARG;
   PeDist* d = pe_ctx_dist(c);
   if (!d) {
     pe_set_error("pe_polar_sharded: no communicator (call pe_attach_comm or pe_attach_exchange first)");
@@ -379,7 +379,7 @@ extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* con
   if (s != PE_OK) return s;
   const std::vector<int>& owner = L.owner;
   for (int i = 0; i < count; ++i)
-    if (!out[i] || (owner[i] == d->rank && !in[i])) return PE_ERR_INVALID_ARG;
+    if (!out[i] || (compute && owner[i] == d->rank && !in[i])) return PE_ERR_INVALID_ARG;
   // zero-copy all-gather when out[] is the pe_shard_layout of one buffer
   uint8_t* flat = reinterpret_cast<uint8_t*>(out[0]) - L.off[0];
   bool gather = d->world > 1 && !getenv("PE_SHARD_BROADCAST");
@@ -429,7 +429,7 @@ extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* con
         shp.push_back(shapes[2 * i]);
         shp.push_back(shapes[2 * i + 1]);
       }
-    if (!outs.empty()) {
+    if (!outs.empty() && compute) {
       s = pe_polar(c, ins.data(), outs.data(), shp.data(), (int)outs.size(), iters, dtype, stream_);
       if (s != PE_OK) return fail(s);
       int l = 0;
@@ -479,6 +479,19 @@ extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* con
   if ((s = join()) != PE_OK) return s;
   pe_ctx_set_launches(c, launches);
   return PE_OK;
+}
+
+extern "C" pe_status pe_polar_sharded(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
+                                      int count, int iters, pe_dtype dtype, void* stream) {
+  return sharded_impl(c, in, out, shapes, count, iters, dtype, stream, true);
+}
+
+// The exchange of pe_polar_sharded alone (each rank's owned out[i] already
+// hold its results): the same buckets, collectives and stream ordering, no
+// compute.  The benchmark times it to report the exchange span in isolation.
+extern "C" pe_status pe_sharded_exchange(pe_ctx c, void* const* out, const int64_t* shapes, int count,
+                                         pe_dtype dtype, void* stream) {
+  return sharded_impl(c, nullptr, out, shapes, count, 1, dtype, stream, false);
 }
 
 // pe_polar_split's all-reduce when the caller passes none: an in-place
