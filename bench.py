@@ -569,6 +569,7 @@ def main():
     if world == 1 and args.extra:
         del xs, ys, hin, hout
         for name in [s for s in args.extra.split(",") if s and s != args.workload]:
+            time.sleep(3.0)        # let the power limiter recover after the previous (long) workload
             sh = layer_set(name)
             ctx2 = pe.Context(local_rank)
             c2 = ClockSampler(local_rank)

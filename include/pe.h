@@ -49,7 +49,8 @@ typedef enum {
   PE_ERR_NO_CONVERGENCE = 3,  /* Remez exceeded 50 iterations (reading R6)    */
   PE_ERR_CUDA = 4,            /* CUDA runtime/driver error (sticky errors too) */
   PE_ERR_NCCL = 5,            /* NCCL missing or failed (multi-GPU calls)     */
-  PE_ERR_WORKSPACE = 6        /* device allocation failed                     */
+  PE_ERR_WORKSPACE = 6,       /* device allocation failed                     */
+  PE_ERR_NONFINITE = 7        /* PE_DEBUG_CHECK_FINITE found NaN / Inf        */
 } pe_status;
 
 typedef enum { PE_BF16 = 0, PE_FP32 = 1 } pe_dtype;
@@ -313,6 +314,24 @@ pe_status pe_set_spectrum_init_ex(pe_ctx ctx, int power_iters, double margin);
  * outside [0, 1), NaN min_aspect).
  */
 pe_status pe_set_rect_iteration(pe_ctx ctx, int restart, double min_aspect, double shift);
+
+/*
+ * Debug aids (never on the hot path).
+ * pe_count_nonfinite: *nonfinite = number of NaN / Inf elements over the
+ *   `count` device buffers (rows x cols of `dtype` each); synchronises
+ *   `stream`; PE_ERR_UNSUPPORTED under graph capture.
+ * pe_set_debug(ctx, PE_DEBUG_CHECK_FINITE): later pe_polar / pe_polar_ex
+ *   calls scan their inputs before launching anything (non-finite inputs:
+ *   PE_ERR_NONFINITE, nothing computed) and their outputs after the call
+ *   (non-finite outputs of finite inputs: PE_ERR_NONFINITE); both scans
+ *   synchronise the stream.  0 turns it off (the default: non-finite inputs
+ *   then propagate, reading R9's contract).
+ * Errors: PE_ERR_INVALID_ARG (NULL, unknown flag bits), PE_ERR_CUDA.
+ */
+#define PE_DEBUG_CHECK_FINITE 1
+pe_status pe_count_nonfinite(pe_ctx ctx, const void* const* bufs, const int64_t* shapes, int count, pe_dtype dtype,
+                             int64_t* nonfinite, void* stream);
+pe_status pe_set_debug(pe_ctx ctx, int flags);
 
 /* Number of kernel launches the last pe_polar / pe_polar_host enqueued (for
  * the benchmark's gpu_launches accounting). */

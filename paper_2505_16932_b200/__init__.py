@@ -27,7 +27,8 @@ PE_SAFETY_NOT_FINAL = 2
 PE_NO_RECENTER = 4
 
 _STATUS = {0: "PE_OK", 1: "PE_ERR_INVALID_ARG", 2: "PE_ERR_UNSUPPORTED", 3: "PE_ERR_NO_CONVERGENCE",
-           4: "PE_ERR_CUDA", 5: "PE_ERR_NCCL", 6: "PE_ERR_WORKSPACE"}
+           4: "PE_ERR_CUDA", 5: "PE_ERR_NCCL", 6: "PE_ERR_WORKSPACE",
+           7: "PE_ERR_NONFINITE"}
 
 EXPORTED_SYMBOLS = [
     "pe_status_string", "pe_version", "pe_last_error_message", "pe_coeffs", "pe_coeffs_ex",
@@ -36,7 +37,7 @@ EXPORTED_SYMBOLS = [
     "pe_muon_step", "pe_polar_split", "pe_shard_buckets", "pe_nccl_unique_id", "pe_attach_comm",
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
     "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
-    "pe_set_rect_iteration", "pe_sharded_exchange",
+    "pe_set_rect_iteration", "pe_sharded_exchange", "pe_count_nonfinite", "pe_set_debug",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -81,6 +82,8 @@ def lib():
         "pe_set_spectrum_init_ex": (I, [P, I, D]),
         "pe_set_rect_iteration": (I, [P, I, D, D]),
         "pe_sharded_exchange": (I, [P, ctypes.POINTER(P), I64P, I, I, P]),
+        "pe_count_nonfinite": (I, [P, ctypes.POINTER(P), I64P, I, I, ctypes.POINTER(ctypes.c_int64), P]),
+        "pe_set_debug": (I, [P, I]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -256,6 +259,23 @@ class Context:
         else:
             _check(lib().pe_set_spectrum_init_ex(self._h, int(power_iters), float(margin)),
                    "pe_set_spectrum_init_ex")
+
+    def count_nonfinite(self, tensors, stream=None):
+        """pe_count_nonfinite: NaN / Inf elements over CUDA tensors of one dtype."""
+        import torch
+        n = len(tensors)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in tensors])
+        out = ctypes.c_int64()
+        if stream is None:
+            stream = torch.cuda.current_stream(tensors[0].device)
+        _check(lib().pe_count_nonfinite(self._h, ptrs, _shapes_arr([tuple(t.shape) for t in tensors]), n,
+                                        _dtype_code(tensors[0]), ctypes.byref(out),
+                                        ctypes.c_void_p(stream.cuda_stream)), "pe_count_nonfinite")
+        return out.value
+
+    def set_debug(self, flags):
+        """pe_set_debug (PE_DEBUG_CHECK_FINITE = 1)."""
+        _check(lib().pe_set_debug(self._h, int(flags)), "pe_set_debug")
 
     def set_rect_iteration(self, restart, min_aspect=0.0, shift=1e-3):
         """pe_set_rect_iteration: App. H's Alg. 4 for matrices with aspect

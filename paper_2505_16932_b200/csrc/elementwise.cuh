@@ -465,6 +465,30 @@ __global__ void __launch_bounds__(256) pe_upload_kernel(const uint4* __restrict_
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
+// ---------------------------------------------------------------- debug scan
+// Count the non-finite elements (NaN / Inf: all exponent bits set) of one
+// buffer of n elements (bf16 or fp32) into *count (pe_count_nonfinite,
+// PE_DEBUG_CHECK_FINITE; off the hot path).
+template <typename T>
+__global__ void __launch_bounds__(256) pe_nonfinite_kernel(const T* __restrict__ x, int64_t n,
+                                                           unsigned long long* count) {
+  pdl_trigger();
+  pdl_wait();
+  unsigned long long k = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (sizeof(T) == 2) {
+      const uint16_t u = reinterpret_cast<const uint16_t*>(x)[i];
+      k += (u & 0x7F80u) == 0x7F80u;
+    } else {
+      const uint32_t u = reinterpret_cast<const uint32_t*>(x)[i];
+      k += (u & 0x7F800000u) == 0x7F800000u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  if ((threadIdx.x & 31) == 0 && k) atomicAdd(count, k);
+}
+
 // ---------------------------------------------------------------- App. H
 // Fast rectangular iteration (Alg. 4): with Q_0 = I the first
 // iteration of an application is R_1 = Y and Q_1 = h_1(Y) = a_1 I + H_1,
@@ -482,7 +506,10 @@ struct ExpandArgs {
 __global__ void __launch_bounds__(256) pe_expand_kernel(const ExpandArgs e) {
   pdl_trigger();
   pdl_wait();
-  __shared__ __nv_bfloat16 t[64][66];
+  // [64][64 + 8] bf16: row pitch 144 bytes keeps 16-byte row segments aligned
+  // and spreads the column gathers of the transposed tiles over the banks
+  __shared__ __align__(16) __nv_bfloat16 t[64][72];
+  const int tid = threadIdx.x;
   for (int it = blockIdx.x; it < e.nitems; it += gridDim.x) {
     const CopyItem ci = e.items[it];
     const MatDev md = e.mats[ci.mat];
@@ -491,18 +518,42 @@ __global__ void __launch_bounds__(256) pe_expand_kernel(const ExpandArgs e) {
     const int sr0 = upper ? r0 : c0, sc0 = upper ? c0 : r0;
     const __nv_bfloat16* H = reinterpret_cast<const __nv_bfloat16*>(md.B);
     __nv_bfloat16* Q = reinterpret_cast<__nv_bfloat16*>(md.E[0]);
+    const bool vec = (md.ldm % 8 == 0) && (sr0 + 64 <= md.m) && (sc0 + 64 <= md.m) && (r0 + 64 <= md.m) &&
+                     (c0 + 64 <= md.m);
     __syncthreads();                                   // previous tile's reads of t are done
-    for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
-      const int i = k >> 6, j = k & 63, gr = sr0 + i, gc = sc0 + j;
-      t[i][j] = (gr < md.m && gc < md.m) ? H[(int64_t)gr * md.ldm + gc] : __float2bfloat16_rn(0.f);
+    if (vec) {
+      // 512 16-byte units (row i, columns 8u .. 8u+7), two per thread
+      for (int k = tid; k < 512; k += 256) {
+        const int i = k >> 3, u = k & 7;
+        *reinterpret_cast<uint4*>(&t[i][8 * u]) =
+            *reinterpret_cast<const uint4*>(H + (int64_t)(sr0 + i) * md.ldm + sc0 + 8 * u);
+      }
+    } else {
+      for (int k = tid; k < 64 * 64; k += 256) {
+        const int i = k >> 6, j = k & 63, gr = sr0 + i, gc = sc0 + j;
+        t[i][j] = (gr < md.m && gc < md.m) ? H[(int64_t)gr * md.ldm + gc] : __float2bfloat16_rn(0.f);
+      }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 64 * 64; k += blockDim.x) {
-      const int i = k >> 6, j = k & 63, gr = r0 + i, gc = c0 + j;
-      if (gr >= md.m || gc >= md.m) continue;
-      __nv_bfloat16 v = upper ? t[i][j] : t[j][i];
-      if (gr == gc) v = __float2bfloat16_rn(__fadd_rn(__bfloat162float(v), e.a));
-      Q[(int64_t)gr * md.ldm + gc] = v;
+    if (vec) {
+      for (int k = tid; k < 512; k += 256) {
+        const int i = k >> 3, u = k & 7, gr = r0 + i;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          v[q] = upper ? t[i][8 * u + q] : t[8 * u + q][i];
+          if (gr == c0 + 8 * u + q) v[q] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(v[q]), e.a));
+        }
+        *reinterpret_cast<uint4*>(Q + (int64_t)gr * md.ldm + c0 + 8 * u) = *reinterpret_cast<const uint4*>(v);
+      }
+    } else {
+      for (int k = tid; k < 64 * 64; k += 256) {
+        const int i = k >> 6, j = k & 63, gr = r0 + i, gc = c0 + j;
+        if (gr >= md.m || gc >= md.m) continue;
+        __nv_bfloat16 v = upper ? t[i][j] : t[j][i];
+        if (gr == gc) v = __float2bfloat16_rn(__fadd_rn(__bfloat162float(v), e.a));
+        Q[(int64_t)gr * md.ldm + gc] = v;
+      }
     }
   }
 }

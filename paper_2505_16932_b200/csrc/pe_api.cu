@@ -247,6 +247,8 @@ struct pe_ctx_s {
   double rect_min_aspect = 0.0;  // <= 0: the paper's rule alpha > 1.5 T / (T - 1)
   double rect_shift = 1e-3;      // added to Y's diagonal in the first application
   int rect_mode = 0;             // internal: 0 = split the batch by aspect, 1 = Listing 2 only, 2 = Alg. 4 only
+  int debug = 0;                 // pe_set_debug flags (PE_DEBUG_CHECK_FINITE)
+  unsigned long long* nf = nullptr;   // device counter of pe_count_nonfinite
 };
 
 PeDist*& pe_ctx_dist(pe_ctx c) { return c->dist; }
@@ -324,6 +326,7 @@ extern "C" const char* pe_status_string(pe_status s) {
     case PE_ERR_CUDA: return "PE_ERR_CUDA";
     case PE_ERR_NCCL: return "PE_ERR_NCCL";
     case PE_ERR_WORKSPACE: return "PE_ERR_WORKSPACE";
+    case PE_ERR_NONFINITE: return "PE_ERR_NONFINITE";
   }
   return "PE_ERR_UNKNOWN";
 }
@@ -387,6 +390,7 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   if (c->ws) cudaFree(c->ws);
+  if (c->nf) cudaFree(c->nf);
   for (Plan* p : c->plans) free_plan(p);
   for (Plan* p : c->retired_plans) free_plan(p);
   for (void* w : c->retired_ws) cudaFree(w);
@@ -1708,9 +1712,80 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
   return PE_OK;
 }
 
+extern "C" pe_status pe_count_nonfinite(pe_ctx c, const void* const* bufs, const int64_t* shapes, int count,
+                                        pe_dtype dtype, int64_t* nonfinite, void* stream) {
+  if (!c || !nonfinite || (dtype != PE_BF16 && dtype != PE_FP32)) return PE_ERR_INVALID_ARG;
+  pe_status s = validate_shapes(shapes, count);
+  if (s != PE_OK) return s;
+  for (int i = 0; i < count; ++i)
+    if (!bufs || !bufs[i]) return PE_ERR_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  PE_CUDA(cudaSetDevice(c->device));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  PE_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    g_last_error = "pe_count_nonfinite synchronises: not under graph capture";
+    return PE_ERR_UNSUPPORTED;
+  }
+  if (!c->nf && cudaMalloc(&c->nf, sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return PE_ERR_WORKSPACE;
+  }
+  PE_CUDA(cudaMemsetAsync(c->nf, 0, sizeof(unsigned long long), st));
+  for (int i = 0; i < count; ++i) {
+    const int64_t n = shapes[2 * i] * shapes[2 * i + 1];
+    const int grid = (int)std::min<int64_t>(cdiv(n, 256 * 8), c->num_sms * 8);
+    if (dtype == PE_BF16)
+      launch(pe_nonfinite_kernel<__nv_bfloat16>, grid, 256, 0, st, (const __nv_bfloat16*)bufs[i], n, c->nf);
+    else
+      launch(pe_nonfinite_kernel<float>, grid, 256, 0, st, (const float*)bufs[i], n, c->nf);
+  }
+  unsigned long long h = 0;
+  PE_CUDA(cudaMemcpyAsync(&h, c->nf, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PE_CUDA(cudaStreamSynchronize(st));
+  *nonfinite = (int64_t)h;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_set_debug(pe_ctx c, int flags) {
+  if (!c || (flags & ~PE_DEBUG_CHECK_FINITE)) return PE_ERR_INVALID_ARG;
+  c->debug = flags;
+  return PE_OK;
+}
+
+// PE_DEBUG_CHECK_FINITE around a pe_polar / pe_polar_ex call: non-finite
+// inputs are refused before anything is launched, non-finite outputs of
+// finite inputs are reported after the call (both synchronise the stream).
+template <typename F>
+static pe_status checked_call(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes, int count,
+                              pe_dtype in_t, pe_dtype out_t, void* stream, F&& call) {
+  if (!c || !(c->debug & PE_DEBUG_CHECK_FINITE) || count <= 0 || !in || !out) return call();
+  int64_t k = 0;
+  pe_status s = pe_count_nonfinite(c, in, shapes, count, in_t, &k, stream);
+  if (s != PE_OK) return s;
+  if (k > 0) {
+    static thread_local std::string msg;
+    msg = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite input values";
+    g_last_error = msg.c_str();
+    return PE_ERR_NONFINITE;
+  }
+  if ((s = call()) != PE_OK) return s;
+  if ((s = pe_count_nonfinite(c, const_cast<const void* const*>(out), shapes, count, out_t, &k, stream)) != PE_OK)
+    return s;
+  if (k > 0) {
+    static thread_local std::string msg;
+    msg = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite outputs from finite inputs";
+    g_last_error = msg.c_str();
+    return PE_ERR_NONFINITE;
+  }
+  return PE_OK;
+}
+
 extern "C" pe_status pe_polar(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
                               int count, int iters, pe_dtype dtype, void* stream) {
-  return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
+  return checked_call(c, in, out, shapes, count, dtype, dtype, stream, [&] {
+    return polar_impl(c, in, out, nullptr, shapes, count, iters, dtype, stream, 0.0, 0.0);
+  });
 }
 
 extern "C" pe_status pe_polar_ex(pe_ctx c, const void* const* in, void* const* out, const int64_t* shapes,
@@ -1723,10 +1798,14 @@ extern "C" pe_status pe_polar_ex(pe_ctx c, const void* const* in, void* const* o
       g_last_error = "pe_polar_ex: fp32 compute takes fp32 input and output";
       return PE_ERR_UNSUPPORTED;
     }
-    return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_FP32, stream, 0.0, 0.0);
+    return checked_call(c, in, out, shapes, count, PE_FP32, PE_FP32, stream, [&] {
+      return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_FP32, stream, 0.0, 0.0);
+    });
   }
   const int io = (in_dtype == PE_FP32 ? 1 : 0) | (out_dtype == PE_FP32 ? 2 : 0);
-  return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_BF16, stream, 0.0, 0.0, nullptr, nullptr, io);
+  return checked_call(c, in, out, shapes, count, in_dtype, out_dtype, stream, [&] {
+    return polar_impl(c, in, out, nullptr, shapes, count, iters, PE_BF16, stream, 0.0, 0.0, nullptr, nullptr, io);
+  });
 }
 
 extern "C" pe_status pe_polar_split(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,

@@ -422,7 +422,7 @@ static pe_status sharded_impl(pe_ctx c, const void* const* in, void* const* out,
     ins.clear();
     outs.clear();
     shp.clear();
-    for (int i = L.beg[b]; i < L.beg[b + 1]; ++i)
+    for (int i = L.beg[b]; i < L.beg[b + 1] && compute; ++i)
       if (owner[i] == d->rank) {
         ins.push_back(in[i]);
         outs.push_back(out[i]);

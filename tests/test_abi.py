@@ -198,6 +198,8 @@ def test_shard_layout_chunks_hold_each_owners_matrices():
     assert L.pe_attach_exchange(None, 0, 1, pe.EXCHANGE_FN(), None) == 1
     assert L.pe_sharded_exchange(None, None, None, 1, 0, None) == 1
     assert L.pe_set_rect_iteration(None, 2, 0.0, 1e-3) == 1
+    assert L.pe_set_debug(None, 1) == 1
+    assert L.pe_count_nonfinite(None, None, None, 0, 0, None, None) == 1
 
 
 def test_nccl_entry_points_validate_without_a_gpu():

@@ -1677,3 +1677,38 @@ def test_alg4_hadamard_closed_form(shape):
     Y = y[::61].float().cpu().numpy().astype(np.float64)
     assert np.all(np.isfinite(Y))
     assert om.rel_frobenius(Y, s * H[::61].astype(np.float64) / math.sqrt(n)) <= 2e-2
+
+
+def test_debug_nonfinite_scan():
+    """SURVEY §5 / §8(b) debug aid: pe_count_nonfinite counts NaN / Inf in
+    bf16 and fp32 buffers exactly; with PE_DEBUG_CHECK_FINITE a non-finite
+    input is refused before anything runs (output untouched) and non-finite
+    outputs of finite inputs are reported (folded bf16 entries of 1e30
+    overflow the first Gram's fp32 accumulator, reading R18); off again, the
+    same calls run and propagate as documented."""
+    c = pe.Context(0)
+    x = to_dev_bf16(bf16_values(syn.gaussian(256, 512, seed=5, std=0.02)))
+    y32 = torch.randn(300, 130, device="cuda")
+    assert c.count_nonfinite([x]) == 0 and c.count_nonfinite([y32]) == 0
+    xb = x.clone()
+    xb[3, 7] = float("nan")
+    xb[100, 500] = float("inf")
+    xb[255, 0] = float("-inf")
+    y32[0, 0] = float("nan")
+    assert c.count_nonfinite([x, xb]) == 3 and c.count_nonfinite([y32]) == 1
+    c.set_debug(pe.PE_DEBUG_CHECK_FINITE)
+    out = torch.zeros_like(xb)
+    with pytest.raises(pe.PeError) as ei:
+        c.polar([xb], [out], iters=5)
+    assert ei.value.status == 7 and torch.count_nonzero(out) == 0
+    ok = c.polar([x], iters=5)[0]
+    big = torch.full((256, 512), 1e30, device="cuda").to(torch.bfloat16)
+    with pytest.raises(pe.PeError) as ei:
+        c.polar([big], iters=5)
+    assert ei.value.status == 7
+    c.set_debug(0)
+    again = c.polar([x], iters=5)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(ok.view(torch.int16), again.view(torch.int16))
+    assert c.count_nonfinite(c.polar([xb], iters=5)) > 0          # propagates when off
+    c.close()
