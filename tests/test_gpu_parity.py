@@ -1712,3 +1712,43 @@ def test_debug_nonfinite_scan():
     assert torch.equal(ok.view(torch.int16), again.view(torch.int16))
     assert c.count_nonfinite(c.polar([xb], iters=5)) > 0          # propagates when off
     c.close()
+
+
+@pytest.mark.slow
+def test_alg4_random_calls_fuzz():
+    """Alg. 4 fuzz: 40 random calls (1-4 matrices, sides around the tile and
+    256-block boundaries, both orientations, aspect ratios 1-6, T = 2..8,
+    restart 1..T+1, shift 0 or 1e-3): every matrix is finite; Alg. 4 ones
+    meet G3 against the fp64 Alg. 4 oracle (the design's G1 spread at
+    T > 5 and small m is wider than the T = 5 gates, so G1 is gated at 1e-1
+    here), the others equal a plain pe_polar call bit for bit."""
+    from oracle import alg4 as a4
+    rng = np.random.default_rng(4242)
+    c = pe.Context(0)
+    plain = pe.Context(0)
+    for call in range(40):
+        T = int(rng.integers(2, 9))
+        restart = int(rng.integers(1, T + 2))
+        shift = float(rng.choice([0.0, 1e-3]))
+        c.set_rect_iteration(restart, 0.0, shift)
+        shapes = []
+        for _ in range(int(rng.integers(1, 5))):
+            m = int(rng.choice([129, 200, 255, 256, 257, 300, 384, 511, 513]))
+            n = int(m * rng.uniform(1.0, 6.0))
+            shapes.append((m, n) if rng.random() < 0.5 else (n, m))
+        mats = [bf16_values(syn.gaussian(r, cc, seed=50000 + 10 * call + i, std=0.02)) for i, (r, cc) in enumerate(shapes)]
+        outs = run(c, mats, T=T)
+        ref_plain = run(plain, mats, T=T)
+        thr = 1.5 * T / (T - 1)
+        for X, M, Y in zip(outs, mats, ref_plain):
+            assert np.all(np.isfinite(X)), (call, M.shape)
+            m, n = min(M.shape), max(M.shape)
+            if n > thr * m:
+                ref = a4.alg4(M, TABLE, T, restart=restart, shift=shift)
+                P = oi.exact_polar(M)
+                assert om.rel_frobenius(X, ref) <= 1e-1, (call, M.shape, T, restart)
+                assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2, (call, M.shape, T, restart)
+            else:
+                assert np.array_equal(X, Y), (call, M.shape)
+    c.close()
+    plain.close()
