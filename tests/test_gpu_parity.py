@@ -1497,21 +1497,26 @@ def test_muon_optimizer_wrapper():
 def test_power_law_spectrum(ctx, shape):
     """sigma_j = j^-5 (App. G's example spectrum): one dominant
     direction, the rest far below ell.  The directions the iteration
-    resolves (sigma >= 0.1 sigma_max) match the oracle to 2e-2 and the error
-    to polar(M) is no worse than the oracle's + max(1e-2, 2 S) (G3 with the
-    oracle's own bf16-input sensitivity S), on the small and the large path."""
+    resolves (sigma >= 3 ell sigma_max: sigma_1..sigma_3, App. E.1's
+    truncation P:1036 at gamma = 3e-3) match the oracle to 2e-2, and the error
+    to polar(M) is no worse than the oracle's + min(max(1e-2, 2 S), 0.05):
+    G3 with the oracle's own bf16-input sensitivity S (0.6-0.66 here, so the
+    slack is capped; the R8 emulation's excess is <= 1.1e-2 on these
+    shapes), on the small and the large path."""
     M = _spiked(*shape, seed=sum(shape), law=5.0)
     Mb = bf16_values(M)
     X = run(ctx, [Mb])[0]
     ref = oi.polar_express(Mb, TABLE, 5)
     P = oi.exact_polar(Mb)
     assert np.all(np.isfinite(X))
-    assert om.truncated_rel_frobenius(X, Mb, 0.1, reference=ref) <= 2e-2
+    assert om.truncated_rel_frobenius(X, Mb, 3e-3, reference=ref) <= 2e-2
     # the unresolved directions (sigma << ell) carry the bf16 rounding noise
     # of the input itself: G3 with the oracle's own sensitivity S to that
-    # rounding (as G2 does for prescribed spectra)
+    # rounding (as G2 does for prescribed spectra), bounded
     S = om.rel_frobenius(oi.polar_express(M, TABLE, 5), ref)
-    assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + max(1e-2, 2 * S)
+    slack = min(max(1e-2, 2 * S), 0.05)
+    print(f"power law {shape}: S = {S:.3f}, G3 slack {slack:.3f}")
+    assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + slack
 
 
 @pytest.mark.parametrize("shape", [(768, 768), (4096, 4096), (1024, 3072), (3072, 1024)])
