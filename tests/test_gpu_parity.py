@@ -1757,3 +1757,33 @@ def test_alg4_random_calls_fuzz():
                 assert np.array_equal(X, Y), (call, M.shape)
     c.close()
     plain.close()
+
+
+def test_alg4_with_polar_ex_and_host_entry():
+    """Alg. 4 composes with pe_polar_ex (fp32 momentum in, R16's explicit
+    X_0, bf16 or fp32 out) -- G3 against the fp64 Alg. 4 oracle on the fp32
+    values -- and with pe_polar_host (pinned host buffers, in place on the
+    staging buffer): bit-identical to the device entry point, one and
+    several applications (restart 5 and 2 at T = 5)."""
+    from oracle import alg4 as a4
+    M = syn.gaussian(256, 1024, seed=4300, std=0.02).astype(np.float32)
+    for restart in (2, 5):
+        c = _alg4_ctx(restart)
+        y = c.polar_ex([torch.from_numpy(M).cuda()], [torch.empty(M.shape, dtype=torch.bfloat16, device="cuda")],
+                       iters=5)[0]
+        torch.cuda.synchronize()
+        X = y.float().cpu().numpy().astype(np.float64)
+        ref = a4.alg4(M.astype(np.float64), TABLE, 5, restart=restart, shift=1e-3)
+        P = oi.exact_polar(M.astype(np.float64))
+        assert np.all(np.isfinite(X)) and om.rel_frobenius(X, ref) <= ALG4_G1[restart if restart < 5 else None]
+        assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
+        shapes = [(256, 1024), (1024, 300), (512, 512)]
+        mats = [bf16_values(syn.gaussian(r, cc, seed=4310 + i, std=0.02)) for i, (r, cc) in enumerate(shapes)]
+        dev = run(c, mats, T=5)
+        hin = [torch.from_numpy(syn.f32_to_bf16_bits(np.asarray(Mi, np.float32)).view(np.int16).copy())
+               .view(torch.bfloat16).pin_memory() for Mi in mats]
+        hout = [torch.empty_like(h).pin_memory() for h in hin]
+        c.polar_host(hin, hout, iters=5)
+        for h, d in zip(hout, dev):
+            assert np.array_equal(h.float().numpy().astype(np.float64), d)
+        c.close()
