@@ -118,7 +118,9 @@ def r19_alg4(M_bf16, table, T, restart=None, shift=1e-3, folded=True):
         then per further iteration t of the application:
         T   = bf16(acc)   acc = Y Q
         R   = bf16(acc)   acc = Q T   (upper blocks stored, symmetrised)
-        H   = bf16(fp32(b R) + fp32(c acc))       acc = R R
+        H   = bf16(fp32(b R) + fp32(c acc))       acc = R R (the true product:
+              R is not symmetric inside its diagonal blocks; upper blocks
+              stored, symmetrised)
         Q   = bf16(fp32(a Q) + acc)               acc = H Q
         X'  = bf16(acc [* inv])                   acc = Q X
     An application of one iteration is Listing 2's step (r8).  Equal to the
@@ -158,7 +160,7 @@ def r19_alg4(M_bf16, table, T, restart=None, shift=1e-3, folded=True):
             a, bb, c = (np.float32(v) for v in tup)
             Tm = _bf16(mm(Y, Q))
             R = _sym_upper(_bf16(mm(Q, Tm)))
-            H = _bf16(np.float32(bb * R) + np.float32(c * mm(R, R)))
+            H = _sym_upper(_bf16(np.float32(bb * R) + np.float32(c * mm(R, R))))
             Q = _bf16(np.float32(a * Q) + mm(H, Q))
         acc = mm(Q, X)
         X = _bf16(np.float32(acc * inv) if scaled else acc)

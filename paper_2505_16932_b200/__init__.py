@@ -117,6 +117,7 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                ctypes.c_void_p, ctypes.c_void_p)
 PE_EXCHANGE_ALLGATHER, PE_EXCHANGE_BROADCAST = 0, 1
+PE_DEBUG_CHECK_FINITE = 1
 
 
 class _DevBuf:

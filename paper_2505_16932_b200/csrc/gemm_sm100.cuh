@@ -145,6 +145,9 @@ struct TileCfg {
   bool scaled;                 // first iteration of a folded matrix
   bool muon;                   // result chunk is a Muon weight update of the chunk already at eout
   bool lin;                    // update of a cubic step: left operand A, epilogue a X + b acc
+  bool rr;                     // poly of Alg. 4's R: the true product R R, not R R^T -- R = Q T is not
+                               // symmetric inside its diagonal blocks, so the right operand's diagonal
+                               // K block is read transposed (MN-major) and diagonal tiles share nothing
   bool has_ein;                // the epilogue reads an operand chunk (poly: A/R, update: X/Q)
   int ncols;                   // result columns (n for X-shaped results, m for square ones)
   float shift;                 // Gram: diagonal shift
@@ -198,6 +201,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   c.scaled = fold;
   c.muon = false;
   c.lin = false;
+  c.rr = false;
   c.shift = 0.f;
   c.a_wide = c.b_wide = false;
   c.Amn = c.Bmn = nullptr;
@@ -214,6 +218,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
     c.shift = g.nphase == 0 ? g.shift : 0.f;
   } else if (c.mode == kModePoly) {
     const bool r = g.nphase == 0 && g.psrc != 0;      // Alg. 4: h(R) from R (maps 9 / 10, emap 7)
+    c.rr = r;
     c.A = c.B = maps + (r ? 9 : 2);
     c.Amn = c.Bmn = maps + (r ? 10 : 4);
     c.a_mn = c.b_mn = false;
@@ -266,7 +271,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   }
   c.has_ein = c.mode != kModeGram && c.ein != nullptr;
   c.ncols = (c.mode == kModeUpdate && !(g.nphase == 0 && g.gen != 0 && !g.g_wide)) ? md.n : md.m;
-  c.diag = (kP == 1) && (c.mode != kModeUpdate) && (tl.tm == tl.tn);
+  c.diag = (kP == 1) && (c.mode != kModeUpdate) && (tl.tm == tl.tn) && !c.rr;
   c.prow = (kP == 1) ? 0 : md.m;
   c.row_a = tl.tm * kBM + (int)rank * (kBM / 2);
   c.col_b = tl.tn * kBN + (int)rank * (kBN / 2);
@@ -669,7 +674,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, o.row_a + 64, k0);
           }
           if (!skip_b) {          // diagonal tiles: the right operand is the left one
-            if (o.b_wide && (kb >> 2) < o.pan_b) {
+            if (o.b_wide && ((kb >> 2) < o.pan_b || (o.rr && (kb >> 2) == o.pan_b))) {
               tma_load_2d_pair(b_dst, o.Bmn, bar, o.col_b, k0 + pb);
               tma_load_2d_pair(b_dst + kBoxBytes, o.Bmn, bar, o.col_b + 64, k0 + pb);
             } else if (o.b_wide) {
@@ -719,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           // per k-block operand layout: blocks of a symmetric buffer below
           // the diagonal arrive transposed (MN-major)
           const bool amn = o.a_mn || (o.a_wide && (kin >> 2) < o.pan_a);
-          const bool bmn = o.b_mn || (o.b_wide && (kin >> 2) < o.pan_b);
+          const bool bmn = o.b_mn || (o.b_wide && ((kin >> 2) < o.pan_b || (o.rr && (kin >> 2) == o.pan_b)));
           const uint32_t idesc = idesc_bf16(kBM, kBN, amn, bmn);
           if (++kin == o.nk && kb < n_small) kin = 0;
           long long t1 = clock64();

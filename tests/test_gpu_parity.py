@@ -1587,7 +1587,7 @@ def _alg4_ctx(restart, shift=1e-3, min_aspect=0.0):
 
 
 @pytest.mark.parametrize("restart", [2, 3, None])
-@pytest.mark.parametrize("shape", [(256, 1024), (1024, 256), (300, 1100), (192, 768), (520, 2080)])
+@pytest.mark.parametrize("shape", [(256, 1024), (1024, 256), (300, 1100), (192, 768), (520, 2080), (129, 244)])
 def test_alg4_parity(shape, restart):
     """pe_set_rect_iteration (App. H, Alg. 4; restart P:1337-1341,
     shift P:1344) against the fp64 oracle's Alg. 4 (oracle/alg4.py, same
@@ -1724,9 +1724,11 @@ def test_alg4_random_calls_fuzz():
     """Alg. 4 fuzz: 40 random calls (1-4 matrices, sides around the tile and
     256-block boundaries, both orientations, aspect ratios 1-6, T = 2..8,
     restart 1..T+1, shift 0 or 1e-3): every matrix is finite; Alg. 4 ones
-    meet G3 against the fp64 Alg. 4 oracle (the design's G1 spread at
+    meet G3 against the fp64 Alg. 4 oracle, or the bf16 design's own excess
+    (R19 emulation) x 1.5 + 2e-3 where that is larger (converged bf16 Alg. 4
+    floors at ~1.3e-2 from polar(M) at m = 129); the design's G1 spread at
     T > 5 and small m is wider than the T = 5 gates, so G1 is gated at 1e-1
-    here), the others equal a plain pe_polar call bit for bit."""
+    here; the others equal a plain pe_polar call bit for bit."""
     from oracle import alg4 as a4
     rng = np.random.default_rng(4242)
     c = pe.Context(0)
@@ -1751,8 +1753,15 @@ def test_alg4_random_calls_fuzz():
             if n > thr * m:
                 ref = a4.alg4(M, TABLE, T, restart=restart, shift=shift)
                 P = oi.exact_polar(M)
+                # G3, or the bf16 design's own excess over the oracle (R19
+                # emulation) with headroom: converged bf16 Alg. 4 floors at
+                # ~1.3e-2 from polar(M) at m = 129 (Listing 2: 0.65e-2)
+                emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift,
+                                       folded=M.shape[1] % 8 == 0).astype(np.float64)
+                e_ref = om.rel_frobenius(ref, P)
+                g3 = max(1e-2, 1.5 * (om.rel_frobenius(emu, P) - e_ref) + 2e-3)
                 assert om.rel_frobenius(X, ref) <= 1e-1, (call, M.shape, T, restart)
-                assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2, (call, M.shape, T, restart)
+                assert om.rel_frobenius(X, P) <= e_ref + g3, (call, M.shape, T, restart)
             else:
                 assert np.array_equal(X, Y), (call, M.shape)
     c.close()
