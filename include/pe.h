@@ -316,6 +316,21 @@ pe_status pe_set_spectrum_init_ex(pe_ctx ctx, int power_iters, double margin);
 pe_status pe_set_rect_iteration(pe_ctx ctx, int restart, double min_aspect, double shift);
 
 /*
+ * Precision of the bf16 small-matrix path (one CTA per matrix, min side
+ * <= 128; R8p).  planes = 2 (opt-in; applies when every matrix of
+ * the call has max side <= 640): the Gram A and the polynomial B are kept as
+ * two bf16 planes (16 significand bits) -- their bf16 rounding dominates the
+ * R8 design's error at small m, and with two planes the small path meets
+ * north_star's 2e-2 from m = 32 (tests/test_r8_spread.py); X and X' stay
+ * bf16; the call takes ~1.4x longer (two MMA chains on the update).
+ * planes = 1 (the default): Listing 2's R8 rounding points, bit-identical to
+ * the large path, so a matrix's result does not depend on the batch it is
+ * computed in (two-plane results do: the variant only exists on the small
+ * path).  Errors: PE_ERR_INVALID_ARG (NULL, planes not 1 or 2).
+ */
+pe_status pe_set_small_planes(pe_ctx ctx, int planes);
+
+/*
  * Debug aids (never on the hot path).
  * pe_count_nonfinite: *nonfinite = number of NaN / Inf elements over the
  *   `count` device buffers (rows x cols of `dtype` each); synchronises

@@ -35,11 +35,21 @@ def _bf16(x):
     return u.astype(np.uint32).view(np.float32)
 
 
-def diagonal_bf16(sigmas_bf16, table, T, folded=True):
+def _split2(v):
+    """Two bf16 planes of fp32 values: (bf16(v), bf16(v - bf16(v)))."""
+    v = np.asarray(v, dtype=np.float32)
+    p0 = _bf16(v)
+    return p0, _bf16(np.float32(v - p0))
+
+
+def diagonal_bf16(sigmas_bf16, table, T, folded=True, ab_planes=1):
     """Diagonal of the GPU's bf16 result for M = diag(sigmas) (any padding).
     ``sigmas_bf16`` must already be bf16 values (the GPU input); ``folded``
     says whether the normalisation is folded into the first iteration (the
-    path the GPU takes when the caller's rows are 16-byte multiples)."""
+    path the GPU takes when the caller's rows are 16-byte multiples).
+    ``ab_planes = 2``: the small path's precise variant (reading R8p): A and
+    B kept as two bf16 planes; a product with a two-plane operand is its big
+    plane product plus the small ones, one fp32 add."""
     s = np.asarray(sigmas_bf16, dtype=np.float32)
     sumsq = float(np.sum(s.astype(np.float64) ** 2))
     nrm = np.sqrt(sumsq) * 1.01 + 1e-7
@@ -49,6 +59,22 @@ def diagonal_bf16(sigmas_bf16, table, T, folded=True):
         a = np.float32(tup[0])
         b = np.float32(tup[1])
         first = folded and it == 0
+        if ab_planes == 2:
+            acc = np.float32(np.float32(x * x) * np.float32(inv * inv)) if first else np.float32(x * x)
+            A0, A1 = _split2(acc)
+            Af = np.float32(A0 + A1)
+            if len(tup) == 3:
+                c = np.float32(tup[2])
+                w = np.float32(np.float32(A0 * A0) + np.float32(2.0 * np.float32(A1 * A0)))
+                B0, B1 = _split2(np.float32(b * Af) + np.float32(c * w))
+                BX = np.float32(np.float32(B0 * x) + np.float32(B1 * x))
+            else:
+                BX = np.float32(b * np.float32(np.float32(A0 * x) + np.float32(A1 * x)))
+            if first:
+                x = _bf16(np.float32(np.float32(a * x) + BX) * inv)
+            else:
+                x = _bf16(np.float32(a * x) + BX)
+            continue
         A = _bf16(np.float32(x * x) * np.float32(inv * inv)) if first else _bf16(x * x)
         if len(tup) == 3:
             c = np.float32(tup[2])
@@ -63,7 +89,7 @@ def diagonal_bf16(sigmas_bf16, table, T, folded=True):
     return x
 
 
-def r8_polar_express(M_bf16, table, T, folded=True):
+def r8_polar_express(M_bf16, table, T, folded=True, ab_planes=1):
     """The bf16 design of reading R8 on a general matrix: bf16 operands and an
     exact-products accumulation rounded once to fp32 (fp64 matmul of the
     bf16-valued operands, then fp32 -- the tensor cores' fp32 accumulation
@@ -72,7 +98,8 @@ def r8_polar_express(M_bf16, table, T, folded=True):
     bit on diagonal inputs -- its pin).  Listing 2's orientation (P:493,
     P:501).  Used to measure how widely the design's own rounding points
     spread against the fp64 oracle (tests/test_r8_spread.py), i.e. what a
-    bf16 gate can demand of the GPU at a given size."""
+    bf16 gate can demand of the GPU at a given size.  ``ab_planes = 2`` is
+    the small path's precise variant (R8p, as ``diagonal_bf16``)."""
     def mm(P, Q):
         return (P.astype(np.float64) @ Q.astype(np.float64)).astype(np.float32)
 
@@ -87,6 +114,18 @@ def r8_polar_express(M_bf16, table, T, folded=True):
         a, b = np.float32(tup[0]), np.float32(tup[1])
         first = folded and it == 0
         acc = mm(X, X.T)
+        if ab_planes == 2:
+            A0, A1 = _split2(np.float32(acc * np.float32(inv * inv)) if first else acc)
+            Af = np.float32(A0 + A1)
+            if len(tup) == 3:
+                c = np.float32(tup[2])
+                w = np.float32(mm(A0, A0.T) + (mm(A1, A0.T) + mm(A0, A1.T)).astype(np.float32))
+                B0, B1 = _split2(np.float32(b * Af) + np.float32(c * w))
+                BX = np.float32(mm(B0, X) + mm(B1, X))
+            else:
+                BX = np.float32(b * np.float32(mm(A0, X) + mm(A1, X)))
+            X = _bf16(np.float32(np.float32(a * X) + BX) * inv) if first else _bf16(np.float32(a * X) + BX)
+            continue
         A = _bf16(acc * np.float32(inv * inv)) if first else _bf16(acc)
         if len(tup) == 3:
             c = np.float32(tup[2])

@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = [
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
     "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
     "pe_set_rect_iteration", "pe_sharded_exchange", "pe_count_nonfinite", "pe_set_debug",
+    "pe_set_small_planes",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -84,6 +85,7 @@ def lib():
         "pe_sharded_exchange": (I, [P, ctypes.POINTER(P), I64P, I, I, P]),
         "pe_count_nonfinite": (I, [P, ctypes.POINTER(P), I64P, I, I, ctypes.POINTER(ctypes.c_int64), P]),
         "pe_set_debug": (I, [P, I]),
+        "pe_set_small_planes": (I, [P, I]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -273,6 +275,12 @@ class Context:
                                         _dtype_code(tensors[0]), ctypes.byref(out),
                                         ctypes.c_void_p(stream.cuda_stream)), "pe_count_nonfinite")
         return out.value
+
+    def set_small_planes(self, planes):
+        """pe_set_small_planes: 2 (default) keeps A and B of the bf16 small
+        path as two bf16 planes (reading R8p); 1 = R8, bit-identical to the
+        large path."""
+        _check(lib().pe_set_small_planes(self._h, int(planes)), "pe_set_small_planes")
 
     def set_debug(self, flags):
         """pe_set_debug (PE_DEBUG_CHECK_FINITE = 1)."""

@@ -248,6 +248,7 @@ struct pe_ctx_s {
   double rect_shift = 1e-3;      // added to Y's diagonal in the first application
   int rect_mode = 0;             // internal: 0 = split the batch by aspect, 1 = Listing 2 only, 2 = Alg. 4 only
   int debug = 0;                 // pe_set_debug flags (PE_DEBUG_CHECK_FINITE)
+  int small_planes = 1;          // pe_set_small_planes: A / B planes of the bf16 small path (1 = R8, 2 = R8p)
   unsigned long long* nf = nullptr;   // device counter of pe_count_nonfinite
 };
 
@@ -362,6 +363,8 @@ extern "C" pe_status pe_create(pe_ctx* out, int device) {
                                (int)small_smem_bytes<1>(kSmallMaxNpadBf16)));
   PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)small_smem_bytes<3>(128)));
+  PE_CUDA(cudaFuncSetAttribute(pe_small_sm100<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)small_smem_bytes<1, 2>(kSmallMaxNpadPrecise)));
   if (!get_encode_fn()) {
     g_last_error = "cuTensorMapEncodeTiled unavailable";
     return PE_ERR_CUDA;
@@ -1149,7 +1152,10 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     a.coef = reinterpret_cast<const float*>(d + mats_bytes + cta_bytes);
   }
   { ProfScope ps(c, 7, st);
-    if (dtype == PE_BF16) launch(pe_small_sm100<1>, nctas, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
+    if (dtype == PE_BF16 && c->small_planes == 2 && max_npad <= kSmallMaxNpadPrecise)
+      launch(pe_small_sm100<1, 2>, nctas, kSmallThreads, small_smem_bytes<1, 2>(max_npad), st, a);
+    else if (dtype == PE_BF16)
+      launch(pe_small_sm100<1>, nctas, kSmallThreads, small_smem_bytes<1>(max_npad), st, a);
     else launch(pe_small_sm100<3>, nctas, kSmallThreads, small_smem_bytes<3>(max_npad), st, a); }
   PE_CUDA(cudaGetLastError());
   c->last_launches = 1 + c->uploads;
@@ -1744,6 +1750,12 @@ extern "C" pe_status pe_count_nonfinite(pe_ctx c, const void* const* bufs, const
   PE_CUDA(cudaMemcpyAsync(&h, c->nf, sizeof(h), cudaMemcpyDeviceToHost, st));
   PE_CUDA(cudaStreamSynchronize(st));
   *nonfinite = (int64_t)h;
+  return PE_OK;
+}
+
+extern "C" pe_status pe_set_small_planes(pe_ctx c, int planes) {
+  if (!c || (planes != 1 && planes != 2)) return PE_ERR_INVALID_ARG;
+  c->small_planes = planes;
   return PE_OK;
 }
 

@@ -15,6 +15,15 @@
 //   fp32 (kP = 3): three bf16 planes per buffer, the six plane products small
 //     terms first, the big p0 q0 chain split over two TMEM buffers at the
 //     same K block, X_0 = split3(fp32(m inv)), result = (p0 + p1) + p2.
+//   bf16, precise A/B (kP = 1, kQ = 2; the default for bf16 calls with
+//     n <= 640, pe_set_small_planes): X and X' as above, but A and B are kept
+//     as two bf16 planes (16 significand bits): A = split2(fp32 acc [* inv^2]),
+//     B = split2(fp32(b (A0 + A1)) + fp32(c acc)), acc = A A; the products
+//     with a two-plane operand accumulate the big p0 chain in TMEM buffer 0
+//     and the small plane products in buffer 1, summed by the epilogue with
+//     one fp32 add (reading R8p).  The bf16 rounding of A and B dominates the
+//     design's error at small m (tests/test_r8_spread.py); this variant meets
+//     north_star's 2e-2 from m = 16.
 //
 // Shared memory (one CTA per matrix, 128 threads = 4 warps; thread r owns
 // TMEM lane / row r): X as kP planes of [128 rows][n_pad/64 blocks of 64
@@ -79,10 +88,11 @@ __device__ __forceinline__ uint32_t small_unit(int r, int u) {
   return (uint32_t)((u >> 3) * 16384 + r * 128 + (((u & 7) ^ (r & 7)) << 4));
 }
 
-template <int kP>
+template <int kP, int kQ = kP>
 __host__ __device__ constexpr size_t small_smem_bytes(int n_pad) {
-  return 1024 + (size_t)kP * 128 * n_pad * 2 + (size_t)kP * 128 * 128 * 2 + 64;
+  return 1024 + (size_t)kP * 128 * n_pad * 2 + (size_t)kQ * 128 * 128 * 2 + 64;
 }
+constexpr int kSmallMaxNpadPrecise = 640;   // bf16 X (128 x 640) + two A planes = 224 KB
 
 // 8 consecutive values of one row (one 16-byte unit per plane): kP = 1 the
 // bf16 value, kP = 3 (p0 + p1) + p2
@@ -96,6 +106,15 @@ __device__ __forceinline__ void small_load8(const uint8_t* buf, size_t plane, ui
       const float2 f = __bfloat1622float2(h0[q]);
       v[2 * q] = f.x;
       v[2 * q + 1] = f.y;
+    }
+  } else if (kP == 2) {
+    const uint4 u1 = *reinterpret_cast<const uint4*>(buf + plane + off);
+    const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = __bfloat1622float2(h0[q]), b = __bfloat1622float2(h1[q]);
+      v[2 * q] = __fadd_rn(a.x, b.x);
+      v[2 * q + 1] = __fadd_rn(a.y, b.y);
     }
   } else {
     const uint4 u1 = *reinterpret_cast<const uint4*>(buf + plane + off);
@@ -121,6 +140,15 @@ __device__ __forceinline__ void small_store8(uint8_t* buf, size_t plane, uint32_
   for (int q = 0; q < 4; ++q) {
     if (kP == 1) {
       h0[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    } else if (kP == 2) {
+      float p0[2], p1[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        p0[e] = __bfloat162float(__float2bfloat16_rn(v[2 * q + e]));
+        p1[e] = __fsub_rn(v[2 * q + e], p0[e]);
+      }
+      h0[q] = __floats2bfloat162_rn(p0[0], p0[1]);
+      h1[q] = __floats2bfloat162_rn(p1[0], p1[1]);
     } else {
       float p0[2], p1[2], p2[2];
 #pragma unroll
@@ -136,6 +164,7 @@ __device__ __forceinline__ void small_store8(uint8_t* buf, size_t plane, uint32_
     }
   }
   *reinterpret_cast<uint4*>(buf + off) = u0;
+  if (kP == 2) *reinterpret_cast<uint4*>(buf + plane + off) = u1;
   if (kP == 3) {
     *reinterpret_cast<uint4*>(buf + plane + off) = u1;
     *reinterpret_cast<uint4*>(buf + 2 * plane + off) = u2;
@@ -147,7 +176,7 @@ __device__ __forceinline__ void small_store8(uint8_t* buf, size_t plane, uint32_
 template <int kP>
 __device__ __forceinline__ void small_acc32(uint32_t taddr, bool b1, float (&w)[32]) {
   tmem_ld32(taddr, w);
-  if (kP == 3 && b1) {
+  if ((kP == 3 || kP == 2) && b1) {
     float w2[32];
     tmem_ld32(taddr + 128, w2);
 #pragma unroll
@@ -186,8 +215,41 @@ __device__ __forceinline__ void small_mma(uint32_t d, uint32_t p_base, size_t p_
   }
 }
 
-template <int kP>
+// Two-plane products of the precise bf16 variant: P has kPa planes, Q kPb
+// (one of them 2, the other 1 or 2); the big p0 q0 chain accumulates in d,
+// the small plane products (p1 q0, p0 q1) in d + 128, summed by the
+// epilogue (small_acc32<2>).
+template <int kPa, int kPb, bool kQmn>
+__device__ __forceinline__ void small_mma_2p(uint32_t d, uint32_t p_base, size_t p_plane, uint32_t q_base,
+                                             size_t q_plane, int q_col0, int N, int nkb) {
+  const uint32_t idesc = idesc_bf16(128, N, 0, kQmn ? 1 : 0);
+  // segments: (1, 0) and (0, 1) into d + 128, then (0, 0) into d
+  const int segs[3][2] = {{1, 0}, {0, 1}, {0, 0}};
+  bool first_small = true;
+  for (int sg = 0; sg < 3; ++sg) {
+    const int pa = segs[sg][0], pb = segs[sg][1];
+    if (pa >= kPa || pb >= kPb) continue;
+    const bool big = (sg == 2);
+    const uint32_t dd = big ? d : d + 128;
+    for (int kb = 0; kb < nkb; ++kb) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t adesc = smem_desc_sw128(p_base + (uint32_t)(pa * p_plane) + kb * 16384 + k * 32, 16, 1024);
+        const uint64_t bdesc =
+            kQmn ? smem_desc_sw128(q_base + (uint32_t)(pb * q_plane) + (q_col0 >> 6) * 16384 + kb * 8192 + k * 2048,
+                                   16384, 1024)
+                 : smem_desc_sw128(q_base + (uint32_t)(pb * q_plane) + kb * 16384 + k * 32, 16, 1024);
+        const uint32_t acc = big ? (kb > 0 || k > 0) : !(first_small && kb == 0 && k == 0);
+        umma_bf16(dd, adesc, bdesc, idesc, acc);
+      }
+    }
+    if (!big) first_small = false;
+  }
+}
+
+template <int kP, int kQ = kP>
 __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_constant__ SmallArgs args) {
+  static_assert((kP == 1 && (kQ == 1 || kQ == 2)) || (kP == 3 && kQ == 3), "plane combinations");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_s;
@@ -219,7 +281,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
   const size_t xplane = (size_t)128 * n_pad * 2;
   const size_t aplane = (size_t)128 * 128 * 2;
   uint8_t* X = smem;
-  uint8_t* A = smem + kP * xplane;
+  uint8_t* A = smem + kP * xplane;                 // kQ planes
 
   // ---- norm (fp64 sum of exact squares, as pe_norm_kernel) and load, per
   // matrix of the CTA (slot s at X rows 64 s ..).  The caller matrix is
@@ -232,7 +294,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
   {
     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int u = 0; u < n_pad / 8; ++u) small_store8<kP>(X, xplane, small_unit(tid, u), z);
-    for (int u = 0; u < 16; ++u) small_store8<kP>(A, aplane, small_unit(tid, u), z);
+    for (int u = 0; u < 16; ++u) small_store8<kQ>(A, aplane, small_unit(tid, u), z);
   }
   float inv_s[2] = {1.f, 1.f};
   bool fold_s[2] = {false, false};
@@ -436,38 +498,40 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
       // packed: only the own diagonal block (columns 64 my ..) is written
       if (!packed || (g >> 1) == my) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) small_store8<kP>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
+        for (int q = 0; q < 4; ++q) small_store8<kQ>(A, aplane, small_unit(r, 4 * g + q), w + 8 * q);
       }
     }
     // ---- B = b A + c A A, in place over A (cubic: not formed)
     if (!args.lin) {
       sync_for_mma();
-      run_and_wait([&] { small_mma<kP, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
+      if (kQ == 2) run_and_wait([&] { small_mma_2p<2, 2, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
+      else run_and_wait([&] { small_mma<kP, false>(tmem, as, aplane, as, aplane, 0, 128, 2); });
 #pragma unroll 1
       for (int g = 0; g < 4; ++g) {
         float w[32];
-        small_acc32<kP>(trow + 32 * g, true, w);
+        small_acc32<kQ>(trow + 32 * g, true, w);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float o[8];
           const uint32_t off = small_unit(r, 4 * g + q);
-          small_load8<kP>(A, aplane, off, o);
+          small_load8<kQ>(A, aplane, off, o);
 #pragma unroll
           for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(__fmul_rn(b, o[j]), __fmul_rn(cc3, w[8 * q + j]));
-          small_store8<kP>(A, aplane, off, o);
+          small_store8<kQ>(A, aplane, off, o);
         }
       }
     }
     // ---- X' = a X + B X, column chunks in place
     sync_for_mma();
-    const int chunk = (kP == 1) ? 256 : 128;
+    const int chunk = (kP == 1 && kQ == 1) ? 256 : 128;   // two-plane products use both TMEM halves
     for (int q0 = 0; q0 < n_pad; q0 += chunk) {
       const int N = min(chunk, n_pad - q0);
-      run_and_wait([&] { small_mma<kP, true>(tmem, as, aplane, xs, xplane, q0, N, 2); });
+      if (kQ == 2) run_and_wait([&] { small_mma_2p<2, 1, true>(tmem, as, aplane, xs, xplane, q0, N, 2); });
+      else run_and_wait([&] { small_mma<kP, true>(tmem, as, aplane, xs, xplane, q0, N, 2); });
 #pragma unroll 1
       for (int g = 0; g < N / 32; ++g) {
         float w[32];
-        small_acc32<kP>(trow + 32 * g, true, w);
+        small_acc32<kQ == 2 ? 2 : kP>(trow + 32 * g, true, w);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int u = (q0 + 32 * g) / 8 + q;

@@ -7,6 +7,8 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 import torch, paper_2505_16932_b200 as pe
 ctx = pe.Context(0)
 import os
+if os.environ.get("PE_SMALL_PLANES"):
+    ctx.set_small_planes(int(os.environ["PE_SMALL_PLANES"]))
 for dt in (torch.float32, torch.bfloat16):
     for shape in [(128, 128), (64, 64), (128, 512)]:
         x = (torch.randn(shape, device="cuda") * 0.02).to(dt)

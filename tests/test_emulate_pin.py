@@ -84,6 +84,44 @@ def sqrt64(x):
     return a
 
 
+def pin_trajectory_r8p(sig_bf16, tuples, folded):
+    """Reading R8p (the small path's two-plane A/B variant) on
+    M = diag(sig): A = split2(fp32 acc [* inv^2]); a product with a two-plane
+    operand = fp32(big plane product + fp32(sum of the small ones));
+    B = split2(fp32(b (A0 + A1)) + fp32(c (A A))); X' = bf16(fp32(a X) + B X)."""
+    xs = [Fr(float(v)) for v in sig_bf16]
+    sumsq = sum(x * x for x in xs)
+    s = f64(f64(sqrt64(sumsq) * Fr(1.01)) + Fr(1e-7))
+    inv = f32(f64(Fr(1) / s))
+    inv2 = f32(inv * inv)
+    x = list(xs) if folded else [bf16(f32(v * inv)) for v in xs]
+
+    def split2(v):
+        p0 = bf16(v)
+        return p0, bf16(f32(v - p0))
+
+    out = []
+    for it, tup in enumerate(tuples):
+        a, b = f32(Fr(tup[0])), f32(Fr(tup[1]))
+        c = f32(Fr(tup[2])) if len(tup) == 3 else None
+        first = folded and it == 0
+        nx = []
+        for v in x:
+            acc = v * v
+            A0, A1 = split2(f32(f32(acc) * inv2) if first else f32(acc))
+            if c is not None:
+                w = f32(A0 * A0 + f32(2 * A1 * A0))
+                B0, B1 = split2(f32(f32(b * f32(A0 + A1)) + f32(c * w)))
+                bx = f32(B0 * v + f32(B1 * v))
+            else:
+                bx = f32(b * f32(A0 * v + f32(A1 * v)))
+            y = bf16(f32(f32(f32(a * v) + bx) * inv)) if first else bf16(f32(f32(a * v) + bx))
+            nx.append(y)
+        x = nx
+        out.append(x)
+    return out
+
+
 def pin_trajectory(sig_bf16, tuples, folded, variant=None):
     """Reading R8 on M = diag(sig): the bf16 diagonal after each iteration
     (list of lists of Fractions).  ``variant`` plants one changed rounding
@@ -172,6 +210,21 @@ def test_emulation_bit_exact_against_fraction_pin(folded):
             emu = emulate.diagonal_bf16(sig, TABLE, T, folded=folded)
             pin = np.array([float(v) for v in traj[T - 1]], dtype=np.float32)
             assert np.array_equal(_bits(emu), _bits(pin)), (folded, T, np.flatnonzero(_bits(emu) != _bits(pin))[:5])
+
+
+@pytest.mark.parametrize("folded", [True, False])
+def test_r8p_emulation_bit_exact_against_fraction_pin(folded):
+    """The two-plane small-path variant (R8p): emulate.diagonal_bf16(...,
+    ab_planes=2) == its exact-rational pin bit for bit (256 sigma values,
+    T = 1..6, degree 5 and 3)."""
+    tab3, _ = oc.pe_coeffs(1e-3, 3, 8, 1.01)
+    for sig in _sigma_sets()[:2]:
+        for tab in (TABLE, tab3):
+            traj = pin_trajectory_r8p(sig, schedule(tab, 6), folded)
+            for T in range(1, 7):
+                emu = emulate.diagonal_bf16(sig, tab, T, folded=folded, ab_planes=2)
+                pin = np.array([float(v) for v in traj[T - 1]], dtype=np.float32)
+                assert np.array_equal(_bits(emu), _bits(pin)), (folded, T, len(tab[0]))
 
 
 def test_emulation_bit_exact_degree3_table():

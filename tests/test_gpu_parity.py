@@ -52,11 +52,21 @@ def run(ctx, mats, T=5, dtype="bf16"):
     return [y.float().cpu().numpy().astype(np.float64) for y in ys]
 
 
-def g1_gate(m):
+def small_precise(shapes):
+    """Does a bf16 call over these shapes take the small path's two-plane
+    variant (R8p: every matrix min side <= 128, max side <= 640)?"""
+    return all(min(s_) <= 128 and -(-max(s_) // 64) * 64 <= 640 for s_ in shapes)
+
+
+def g1_gate(m, precise=False):
     """G1 bound for a Gaussian input with min side m:
     2e-2 from m = 128; below that the R8 rounding points alone spread wider,
     with no kernel involved (tests/test_r8_spread.py, 16-24 seeds of the CPU
-    emulation: max 1.97e-2 at 71 x 547, 3.6e-2 at 16 x 40, 7.8e-2 at 8 x 8)."""
+    emulation: max 1.97e-2 at 71 x 547, 3.6e-2 at 16 x 40, 7.8e-2 at 8 x 8).
+    precise: the small path's two-plane A/B variant (R8p), 2e-2 from m = 32
+    (emulation max 1.16e-2 at 16 x 40, 3.5e-2 at 16 x 16, 2.1e-2 at 8 x 8)."""
+    if precise:
+        return 2e-2 if m >= 32 else (4e-2 if m >= 16 else 1e-1)
     return 2e-2 if m >= 128 else (2.5e-2 if m >= 64 else (4e-2 if m >= 16 else 1e-1))
 
 
@@ -153,7 +163,8 @@ def test_diagonal_bit_exact(ctx, shape):
     """Diagonal inputs: every product has one non-zero term, so the GPU must
     equal the R8 rounding-point emulation bit for bit.  Rows that are
     16-byte multiples take the folded-normalisation path, the others the
-    explicit X_0 path."""
+    explicit X_0 path; the small shapes are also run with the small path's
+    two-plane variant (pe_set_small_planes(2)) against its emulation (R8p)."""
     k = min(shape)
     folded = shape[1] % 8 == 0
     sig = syn.to_bf16_values(np.linspace(1.0, 0.02, k)).astype(np.float64)
@@ -165,6 +176,16 @@ def test_diagonal_bit_exact(ctx, shape):
         off = X.copy()
         off[np.arange(k), np.arange(k)] = 0
         assert np.all(off == 0)
+    if small_precise([shape]):
+        # the small path's two-plane variant (R8p) against its own emulation
+        ctx.set_small_planes(2)
+        try:
+            for T in (1, 3, 5, 8):
+                X = run(ctx, [M], T=T)[0]
+                emu = emulate.diagonal_bf16(sig, TABLE, T, folded=folded, ab_planes=2).astype(np.float64)
+                assert np.array_equal(np.diag(X)[:k], emu), ("planes 2", T)
+        finally:
+            ctx.set_small_planes(1)
 
 
 @pytest.mark.parametrize("shape", [(128, 128), (1024, 4096), (4096, 1024), (2048, 2048)])
@@ -713,12 +734,37 @@ def test_large_batch_of_small_random_shapes(ctx):
         assert np.array_equal(run(ctx, [mats[i]])[0], outs[i])
 
 
+@pytest.mark.parametrize("shape", [(32, 32), (37, 100), (48, 100), (64, 300), (71, 547), (100, 37), (127, 600),
+                                   (300, 64), (16, 40), (8, 8), (1, 64)])
+def test_small_path_two_plane_precision(shape):
+    """pe_set_small_planes(2) (reading R8p): the small path keeps A and B as
+    two bf16 planes and meets north_star's G1 2e-2 from m = 32 (the design's
+    own spread, tests/test_r8_spread.py), G3 everywhere; rank one within
+    2e-2 too (the R8 path needs 5e-2 there).  Also several seeds per shape."""
+    c = pe.Context(0)
+    c.set_small_planes(2)
+    m = min(shape)
+    for seed in range(3):
+        Mb = bf16_values(syn.gaussian(*shape, seed=7000 + 13 * seed + sum(shape), std=0.02))
+        X = run(c, [Mb])[0]
+        launches = c.last_launch_count()
+        if m == 1:
+            ref = oi.polar_express(Mb, TABLE, 5)
+            assert om.rel_frobenius(X, ref) <= 2e-2
+            assert om.rel_frobenius(X, oi.exact_polar(Mb)) <= om.rel_frobenius(ref, oi.exact_polar(Mb)) + 1e-2
+        else:
+            check_g1_g3(X, Mb, g1=g1_gate(m, precise=True))
+        assert launches <= 2           # the small path: one launch (+ upload)
+    c.close()
+
+
 _SMALL_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2505_16932_b200 as pe
 data = np.load(sys.argv[2])
 ctx = pe.Context(0)
+ctx.set_small_planes(1)          # R8 on the small path: bit-identical to the large path
 out = {}
 for key in sorted(data.files):
     dt, T = key.split("_")[0], int(key.split("_")[1])
@@ -734,7 +780,8 @@ np.savez(sys.argv[3], **out)
 
 def test_small_path_bit_identical_to_large_path(tmp_path):
     """The small-matrix fused path (one CTA per matrix, the whole call in one
-    launch) reproduces the large path bit for bit: bf16 folded (cols % 8 == 0)
+    launch; pe_set_small_planes(1), the R8 rounding points) reproduces the
+    large path bit for bit: bf16 folded (cols % 8 == 0)
     and unfolded shapes, both orientations, rank one; fp32 (three planes)
     including config 1 (128 x 128); T = 1, 3, 5.  PE_SMALL=0 forces the large
     path; the small path is a single launch."""
@@ -921,12 +968,13 @@ def test_back_to_back_async_calls_stress(ctx):
             assert np.array_equal(y.float().cpu().numpy().astype(np.float64), r)
 
 
-def _r8_emulated(M, T, f32_input=False):
+def _r8_emulated(M, T, f32_input=False, precise=False):
     """oracle.emulate.r8_polar_express on the path the library takes: folded
     for bf16 rows of 16-byte multiples, explicit X_0 = bf16(fp32(x) inv) for
-    the others and for fp32 input (pe_polar_ex, R16)."""
+    the others and for fp32 input (pe_polar_ex, R16); two-plane A/B when the
+    call ran on the small path's precise variant (R8p)."""
     fold = M.shape[1] % 8 == 0 and not f32_input
-    return emulate.r8_polar_express(M, TABLE, T, folded=fold).astype(np.float64)
+    return emulate.r8_polar_express(M, TABLE, T, folded=fold, ab_planes=2 if precise else 1).astype(np.float64)
 
 
 @pytest.mark.slow

@@ -26,11 +26,11 @@ def g1_gate(m):
     return 2e-2 if m >= 128 else (2.5e-2 if m >= 64 else (4e-2 if m >= 16 else 1e-1))
 
 
-def spread(shape, seeds, T=5):
+def spread(shape, seeds, T=5, ab_planes=1):
     out = []
     for seed in seeds:
         M = syn.to_bf16_values(syn.gaussian(*shape, seed=seed, std=0.02)).astype(np.float64)
-        E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0).astype(np.float64)
+        E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=ab_planes).astype(np.float64)
         out.append(om.rel_frobenius(E, oi.polar_express(M, TABLE, T)))
     return np.array(out)
 
@@ -62,6 +62,27 @@ def test_small_m_spread_exceeds_2e2_somewhere():
     widening below m = 128 is needed)."""
     for shape in ((8, 8), (16, 40), (37, 100)):
         assert spread(shape, range(24)).max() > 2e-2, shape
+
+
+@pytest.mark.parametrize("shape", [(32, 32), (32, 500), (37, 100), (48, 100), (64, 64), (64, 300), (71, 547),
+                                   (100, 37), (127, 600)])
+def test_two_plane_small_path_meets_2e2_from_m32(shape):
+    """The small path's precise variant (R8p: A and B as two bf16 planes,
+    pe_set_small_planes(2), max side <= 640) meets north_star's 2e-2 from
+    m = 32 on every seed (24 seeds; 16 x 40 reaches 1.16e-2, 16 x 16 3.5e-2,
+    8 x 8 2.1e-2 -- X's own rounding then dominates)."""
+    r = spread(shape, range(24), ab_planes=2)
+    assert r.max() <= 2e-2, (shape, r.max())
+
+
+def test_r8p_general_emulation_reduces_to_the_diagonal_one():
+    sig = syn.to_bf16_values(np.linspace(1.0, 0.03, 40)).astype(np.float64)
+    for shape in ((40, 96), (96, 40), (40, 61)):
+        M = syn.diagonal(*shape, sig)
+        for T in (1, 3, 5):
+            E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=2)
+            d = emulate.diagonal_bf16(sig, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=2)
+            assert np.array_equal(np.diag(E)[:40], d)
 
 
 @pytest.mark.parametrize("shape", [(128, 128), (128, 512), (200, 520)])
