@@ -1883,9 +1883,13 @@ extern "C" pe_status pe_polar_host(pe_ctx c, const void* const* in, void* const*
     PE_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
     PE_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
   }
-  // groups: contiguous index ranges of ~equal bytes, ~16 MB or more each, at
-  // most 8 (GPT-2 S set on B200 / PCIe 5: G=1 8.1 ms, G=4 7.2 ms, G=8 6.4 ms)
-  int G = (int)std::max<size_t>(1, std::min<size_t>({(size_t)count, (size_t)8, total / (16u << 20)}));
+  // groups: contiguous index ranges of ~equal bytes: up to 8 of >= 16 MB,
+  // more (up to 48, >= 256 MB each) for large sets, where the first group's
+  // H2D and the last group's D2H are the exposed fill and drain (GPT-2 S on
+  // B200 / PCIe 5: G=1 8.1 ms, G=4 7.2 ms, G=8 6.4 ms; Llama-3-8B set, 14 GB
+  // each way: G=8 417 ms, G=16 391, G=32 382, G=48 379, profiles/r2_e2e.txt)
+  const size_t g_small = std::min<size_t>(8, total / (16u << 20)), g_large = std::min<size_t>(48, total >> 28);
+  int G = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, std::max(g_small, g_large)));
   if (const char* gv = getenv("PE_HOST_GROUPS")) G = std::max(1, std::min(count, atoi(gv)));   // experiments
   const bool skip_compute = getenv("PE_HOST_NOCOMPUTE") != nullptr;                          // experiments
   std::vector<int> gbeg(G + 1, count);
