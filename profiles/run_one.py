@@ -24,6 +24,8 @@ def main():
         g.manual_seed(i)
         xs.append((torch.randn((r, c), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
     ctx = pe.Context(0)
+    if os.environ.get("PE_RUN_RECT"):            # App. H Alg. 4 with this restart interval
+        ctx.set_rect_iteration(int(os.environ["PE_RUN_RECT"]), 0.0, 1e-3)
     ys = [torch.empty_like(x) for x in xs]
     for _ in range(calls):
         ctx.polar(xs, ys, iters=T)
