@@ -547,6 +547,10 @@ def main():
                    "parallelism": f"dp{world} (pe_polar_sharded: bucket-balanced LPT shard + per-bucket in-place "
                                   f"NCCL all-gather)" if world > 1 else "single GPU"},
         "tflops": round(tflops, 2), "tflops_unit": "TFLOP/s (algorithmic, symmetric-aware)",
+        "tflops_dense": round(sum(T * (4.0 * min(s_) ** 2 * max(s_) + 2.0 * min(s_) ** 3) for s_ in shapes)
+                              / (mean_ms * 1e-3) / 1e12, 2),
+        "tflops_dense_unit": "TFLOP/s counting every product dense (the paper's MAC model x 2, SURVEY §8d); "
+                             "not comparable with `tflops`",
         "frac_of_bf16_peak": round(tflops / peaks[peak_key], 4),
         "frac_of_bf16_peak_sustained": round(tflops / peaks["bf16_tflops_sustained"], 4),
         "layer_sets_per_s": round(1e3 / mean_ms, 3),

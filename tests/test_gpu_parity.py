@@ -1844,3 +1844,41 @@ def test_alg4_with_polar_ex_and_host_entry():
         for h, d in zip(hout, dev):
             assert np.array_equal(h.float().numpy().astype(np.float64), d)
         c.close()
+
+
+@pytest.mark.slow
+def test_full_llama_set_alg4_sampled():
+    """The bench's Alg. 4 line (llama3-8b:alg4r3) in its launch
+    configuration: all 224 Llama-3-8B matrices in one call with
+    pe_set_rect_iteration(3); the 96 MLP matrices (alpha = 3.5 > 1.875) take
+    Alg. 4, the others Listing 2.  Layer 0's q_proj must equal a plain call
+    bit for bit; its gate_proj (14336 x 4096) and down_proj (4096 x 14336)
+    meet the Alg. 4 G1 gate against the fp64 Alg. 4 oracle and G3."""
+    from oracle import alg4 as a4
+    shapes = syn.layer_set_shapes("llama3-8b")
+    xs, checks = [], {}
+    for i, (r, c) in enumerate(shapes):
+        if i in (0, 4, 6):
+            M = bf16_values(syn.gaussian(r, c, seed=3100 + i, std=0.02))
+            checks[i] = M
+            xs.append(to_dev_bf16(M))
+        else:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(i)
+            xs.append((torch.randn((r, c), generator=g, device="cuda") * 0.02).to(torch.bfloat16))
+    c = _alg4_ctx(3)
+    ys = c.polar(xs, iters=5)
+    torch.cuda.synchronize()
+    c.close()
+    plain = pe.Context(0)
+    q0 = plain.polar([xs[0]], iters=5)[0]
+    torch.cuda.synchronize()
+    plain.close()
+    assert torch.equal(ys[0].view(torch.int16), q0.view(torch.int16))
+    for i in (4, 6):
+        M = checks[i]
+        X = ys[i].float().cpu().numpy().astype(np.float64)
+        ref = a4.alg4(M, TABLE, 5, restart=3, shift=1e-3)
+        P = oi.exact_polar(M)
+        assert np.all(np.isfinite(X)) and om.rel_frobenius(X, ref) <= ALG4_G1[3]
+        assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
