@@ -1089,9 +1089,10 @@ class _VirtualRanks:
         return ex
 
 
-@pytest.mark.parametrize("W,layout,nb", [(2, True, "3"), (3, True, None), (4, True, "2"), (2, False, "2"),
-                                         (4, False, None)])
-def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
+@pytest.mark.parametrize("W,layout,nb,dt", [(2, True, "3", "bf16"), (3, True, None, "bf16"), (4, True, "2", "bf16"),
+                                            (2, False, "2", "bf16"), (4, False, None, "bf16"), (3, True, "2", "fp32"),
+                                            (2, False, None, "fp32")])
+def test_polar_sharded_virtual_ranks(W, layout, nb, dt, monkeypatch):
     """pe_polar_sharded's exchange path at world > 1 (2-4 virtual ranks in
     threads on one GPU, each with its own context, stream and exchange
     function): with outputs in the pe_shard_layout buffer the exchange is one
@@ -1104,7 +1105,13 @@ def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
     if nb:
         monkeypatch.setenv("PE_SHARD_BUCKETS", nb)
     shapes = syn.layer_set_shapes("gpt2-small", layers=2) + [(130, 1000), (1000, 130), (64, 96), (300, 520)]
-    xs = [to_dev_bf16(bf16_values(syn.gaussian(r, c, seed=900 + i, std=0.02))) for i, (r, c) in enumerate(shapes)]
+    if dt == "fp32":
+        shapes = shapes[:4] + shapes[-4:]
+        xs = [torch.from_numpy(syn.gaussian(r, c, seed=900 + i).astype(np.float32)).cuda()
+              for i, (r, c) in enumerate(shapes)]
+    else:
+        xs = [to_dev_bf16(bf16_values(syn.gaussian(r, c, seed=900 + i, std=0.02))) for i, (r, c) in enumerate(shapes)]
+    tdt = torch.float32 if dt == "fp32" else torch.bfloat16
     c0 = pe.Context(0)
     ref = c0.polar(xs, iters=5)
     torch.cuda.synchronize()
@@ -1120,7 +1127,7 @@ def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
                 if layout:
-                    _, ys = pdist.sharded_outputs(shapes, W, torch.bfloat16, "cuda")
+                    _, ys = pdist.sharded_outputs(shapes, W, tdt, "cuda")
                 else:
                     ys = [torch.empty_like(x) for x in xs]
                 c.polar_sharded(xs, ys, iters=5, stream=st)
@@ -1130,6 +1137,7 @@ def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
                 # other ranks own, exchange again, same bytes
                 own = pe.pe_shard_plan(shapes, W)
                 snap = [y.clone() for y in ys]
+                assert all(y.dtype == tdt for y in ys)
                 with torch.cuda.stream(st):
                     for i, y in enumerate(ys):
                         if own[i] != r:
@@ -1153,7 +1161,7 @@ def test_polar_sharded_virtual_ranks(W, layout, nb, monkeypatch):
     nbk = pe.pe_shard_nbuckets(shapes, W)
     for r in range(W):
         for y, z in zip(outs[r], ref):
-            assert torch.equal(y.view(torch.int16), z.view(torch.int16))
+            assert torch.equal(y, z)
         ops = [op for op, _, _ in vr.calls[r]]
         if layout:
             assert ops == [pe.PE_EXCHANGE_ALLGATHER] * (2 * nbk)
