@@ -254,7 +254,8 @@ static int default_nbuckets(const int64_t* shapes, int count, int world) {
 
 extern "C" pe_status pe_shard_nbuckets(const int64_t* shapes, int count, int world, int* nbuckets) {
   if (count < 0 || world < 1 || (count > 0 && !shapes) || !nbuckets) return PE_ERR_INVALID_ARG;
-  *nbuckets = std::min(default_nbuckets(shapes, count, world), std::max(1, count));
+  // the buckets cost_buckets actually forms (skewed costs can leave fewer)
+  *nbuckets = count == 0 ? 1 : (int)cost_buckets(shapes, count, default_nbuckets(shapes, count, world)).size() - 1;
   return PE_OK;
 }
 

@@ -192,6 +192,15 @@ def test_shard_layout_chunks_hold_each_owners_matrices():
         assert total < 1.12 * sum(2 * r * c for r, c in shapes)       # padding of the per-rank chunks
     llama = syn.layer_set_shapes("llama3-8b")
     assert pe.pe_shard_nbuckets(llama, 1) == 1 and pe.pe_shard_nbuckets(llama, 8) == 8
+    # skewed costs: fewer buckets form than the work rule asks for; the count
+    # reported, the bucket boundaries and the layout's chunks agree
+    skew = [(10, 10)] * 5 + [(8192, 8192)] + [(64, 700)] * 3
+    for world in (2, 3):
+        nb = pe.pe_shard_nbuckets(skew, world)
+        beg = pe.pe_shard_buckets(skew, nb)
+        offs, chunks, total = pe.pe_shard_layout(skew, world, pe.PE_BF16, chunks=True)
+        assert len(chunks) == nb and beg[-1] == len(skew) and all(ch >= 256 for ch in chunks)
+        assert total == world * sum(chunks)
     assert pe.pe_shard_nbuckets(syn.layer_set_shapes("gpt2-small"), 8) == 1
     L = pe.lib()
     assert L.pe_shard_layout(None, 0, 1, 0, None, None, None) == 1
