@@ -307,11 +307,13 @@ pe_status pe_set_spectrum_init_ex(pe_ctx ctx, int power_iters, double margin);
  * of 2 per iteration; per further iteration four m x m products.  Other
  * matrices of the call run Listing 2 (a mixed call becomes two grouped
  * calls).  Rounding points (R19): Y, T = Y Q, R, H = b R + c R^2,
- * Q and X' each rounded once to bf16 from fp32 accumulators.  Not with
- * pe_set_spectrum_init, degree-3 tables, fp32, pe_muon_step, pe_polar_split
- * or under graph capture (PE_ERR_UNSUPPORTED).  restart = 0 turns it off
- * (the default).  Errors: PE_ERR_INVALID_ARG (NULL, restart < 0, shift
- * outside [0, 1), NaN min_aspect).
+ * Q and X' each rounded once to bf16 from fp32 accumulators (R² is the
+ * true product R R).  fp32 calls, degree-3 tables, pe_muon_step,
+ * pe_polar_split and calls with the App. G step (pe_set_spectrum_init) run
+ * Listing 2 as if it were off; a call under graph capture with a qualifying
+ * matrix returns PE_ERR_UNSUPPORTED.  restart = 0 turns it off (the
+ * default).  Errors: PE_ERR_INVALID_ARG (NULL, restart < 0, shift outside
+ * [0, 1), NaN min_aspect).
  */
 pe_status pe_set_rect_iteration(pe_ctx ctx, int restart, double min_aspect, double shift);
 
