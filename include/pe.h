@@ -259,6 +259,29 @@ pe_status pe_polar_split(pe_ctx ctx, const void* in, void* out, int64_t rows, in
                            pe_allreduce_fn allreduce, void* user, void* stream);
 
 /*
+ * pe_polar_split with the cross-rank sums done by the library's own kernels
+ * over peer-visible memory instead of an all-reduce call.
+ * slots[r] (r = 0..world-1, 256-byte aligned, pe_split_slot_bytes(rows, cols)
+ * bytes each) is rank r's slot, readable by every rank: on several GPUs a
+ * P2P-mapped (cudaIpc / symmetric-memory) allocation over NVLink, on one GPU
+ * plain device memory.  Rank r's kernels write its partial results straight
+ * into slots[rank] -- ||M_r||^2 from the norm pass, the partial Gram from the
+ * Gram epilogue (double-buffered by iteration parity) -- and after the
+ * barrier the next kernel sums all slots in rank order (bit-identical on every
+ * rank) and rounds A once to bf16 (R8).  barrier(user, stream) is called on
+ * the host: it must return once the work enqueued on `stream` so far is
+ * complete on this rank and every rank has reached the same barrier (one per
+ * iteration plus one for the norm).  Errors: PE_ERR_INVALID_ARG (NULL,
+ * misaligned slot, rank outside [0, world)), the barrier's status, and
+ * pe_polar_split's.
+ */
+typedef pe_status (*pe_barrier_fn)(void* user, void* stream);
+pe_status pe_split_slot_bytes(int64_t rows, int64_t cols, int64_t* bytes);
+pe_status pe_polar_split_peers(pe_ctx ctx, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+                               void* const* slots, int rank, int world, pe_barrier_fn barrier, void* user,
+                               void* stream);
+
+/*
  * Spectrum-aware first step (App. G, k = 1; reading R17), for
  * inputs with one large outlying singular value.  power_iters > 0 turns it
  * on for the context's later bf16 pe_polar / pe_polar_ex / pe_polar_host

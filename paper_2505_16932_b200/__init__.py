@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = [
     "pe_comm_info", "pe_polar_sharded", "pe_polar_ex", "pe_set_spectrum_init",
     "pe_set_spectrum_init_ex", "pe_attach_exchange", "pe_shard_nbuckets", "pe_shard_layout",
     "pe_set_rect_iteration", "pe_sharded_exchange", "pe_count_nonfinite", "pe_set_debug",
-    "pe_set_small_planes",
+    "pe_set_small_planes", "pe_split_slot_bytes", "pe_polar_split_peers",
 ]
 PROFILE_KINDS = ["norm", "scale", "gram", "poly", "update", "transpose_back", "fused", "small"]
 
@@ -86,6 +86,9 @@ def lib():
         "pe_count_nonfinite": (I, [P, ctypes.POINTER(P), I64P, I, I, ctypes.POINTER(ctypes.c_int64), P]),
         "pe_set_debug": (I, [P, I]),
         "pe_set_small_planes": (I, [P, I]),
+        "pe_split_slot_bytes": (I, [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
+        "pe_polar_split_peers": (I, [P, P, P, ctypes.c_int64, ctypes.c_int64, I, ctypes.POINTER(P), I, I,
+                                     BARRIER_FN, P, P]),
         "pe_last_launch_count": (I, [P, ctypes.POINTER(I)]),
         "pe_shard_plan": (I, [I64P, I, I, ctypes.POINTER(I)]),
         "pe_flops": (I, [I64P, I, I, I, DP]),
@@ -119,6 +122,8 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                ctypes.c_void_p, ctypes.c_void_p)
 PE_EXCHANGE_ALLGATHER, PE_EXCHANGE_BROADCAST = 0, 1
+# pe_barrier_fn (include/pe.h): (user, stream) -> pe_status
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
 PE_DEBUG_CHECK_FINITE = 1
 
 
@@ -201,6 +206,13 @@ def pe_shard_layout(shapes, world, dtype=PE_BF16, chunks=False):
     if chunks:
         return list(offs[:n]), list(ch[:nb]), tot.value
     return list(offs[:n]), tot.value
+
+
+def pe_split_slot_bytes(rows, cols):
+    """pe.h pe_split_slot_bytes: bytes of one rank's slot for pe_polar_split_peers."""
+    out = ctypes.c_int64()
+    _check(lib().pe_split_slot_bytes(int(rows), int(cols), ctypes.byref(out)), "pe_split_slot_bytes")
+    return out.value
 
 
 def pe_nccl_unique_id():
@@ -420,6 +432,39 @@ class Context:
         if errors:
             raise errors[0]
         _check(status, "pe_polar_split")
+        return out
+
+    def polar_split_peers(self, shard, slots, rank, barrier, out=None, iters=5, stream=None):
+        """pe_polar_split_peers: this rank's column block of one wide matrix;
+        `slots` are every rank's slot (device pointers or uint8 CUDA tensors
+        of pe_split_slot_bytes bytes, 256-byte aligned, readable by every
+        rank), `barrier(stream_handle)` must return once this rank's work on
+        the stream is complete and every rank has reached it."""
+        import torch
+        if shard.dim() != 2 or not shard.is_contiguous() or not shard.is_cuda or shard.dtype != torch.bfloat16:
+            raise ValueError("polar_split_peers takes a contiguous 2-D bf16 CUDA tensor")
+        if out is None:
+            out = torch.empty_like(shard)
+        if stream is None:
+            stream = torch.cuda.current_stream(shard.device)
+        ptrs = [s_.data_ptr() if hasattr(s_, "data_ptr") else int(s_) for s_ in slots]
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        errors = []
+
+        def cb(user, st):
+            try:
+                barrier(int(st or 0))
+                return 0
+            except Exception as e:          # reported after the call returns
+                errors.append(e)
+                return 5
+        fn = BARRIER_FN(cb)
+        status = lib().pe_polar_split_peers(self._h, ctypes.c_void_p(shard.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            int(shard.shape[0]), int(shard.shape[1]), int(iters), arr, int(rank),
+                                            len(ptrs), fn, None, ctypes.c_void_p(stream.cuda_stream))
+        if errors:
+            raise errors[0]
+        _check(status, "pe_polar_split_peers")
         return out
 
     def attach_comm(self, unique_id, rank, world):

@@ -451,6 +451,38 @@ __global__ void __launch_bounds__(256) pe_round_gram_kernel(const float* a32, __
     a[i] = __float2bfloat16_rn(first ? __fmul_rn(a32[i], sc) : a32[i]);
 }
 
+// pe_polar_split_peers: the cross-rank sums over peer-visible slots (slot r =
+// rank r's partial results, written by its own kernels; on several GPUs a
+// P2P-mapped or NVLS buffer, read here with plain loads), in rank order so
+// every rank forms bit-identical sums.  Slot layout: double ||M_r||^2 at byte
+// 0, partial Gram of parity p at byte 256 + p * gbytes.
+struct PeerSlots {
+  const uint8_t* const* slots;   // [world] device pointers
+  int world;
+  int64_t gbytes;                // bytes of one partial Gram (m * ldm fp32, 256-byte padded)
+};
+__global__ void pe_inv_peers_kernel(const PeerSlots ps, float* inv) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int r = 0; r < ps.world; ++r) s += *reinterpret_cast<const volatile double*>(ps.slots[r]);
+    inv[0] = (float)(1.0 / (sqrt(s) * 1.01 + 1e-7));
+  }
+}
+__global__ void __launch_bounds__(256) pe_round_peers_kernel(const PeerSlots ps, int parity, __nv_bfloat16* a,
+                                                             int64_t n, const float* inv, int first) {
+  pdl_trigger();
+  pdl_wait();
+  const float sc = first ? __fmul_rn(inv[0], inv[0]) : 1.0f;
+  const int64_t off = 256 + parity * ps.gbytes;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int r = 0; r < ps.world; ++r) v = __fadd_rn(v, __ldcg(reinterpret_cast<const float*>(ps.slots[r] + off) + i));
+    a[i] = __float2bfloat16_rn(first ? __fmul_rn(v, sc) : v);
+  }
+}
+
 // Per-call upload of a pe_polar call (pointers, caller tensor maps,
 // coefficients) from its mapped pinned host buffer, read over PCIe by the
 // SMs: it never waits in the copy engines behind unrelated bulk transfers.

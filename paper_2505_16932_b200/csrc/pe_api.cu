@@ -228,6 +228,11 @@ struct pe_ctx_s {
   size_t sh_cap = 0;
   float** sh_ptr = nullptr;
   double* sh_sum = nullptr;
+  // pe_polar_split_peers: device copies of the slot pointers, and of this
+  // rank's two partial-Gram destinations (by iteration parity)
+  uint8_t** peer_slots = nullptr;
+  int peer_cap = 0;
+  float** peer_out = nullptr;
   size_t done_cap = 0;
   int dbg = 0;   // PE_DEBUG_GEMM (timing experiments only; results are wrong when bits 0/1/3 are set)
   long long* stats = nullptr;   // PE_DEBUG_GEMM bit 2: per-CTA wait counters of the last launch per mode
@@ -417,6 +422,8 @@ extern "C" pe_status pe_destroy(pe_ctx c) {
   if (c->sh_a32) cudaFree(c->sh_a32);
   if (c->sh_ptr) cudaFree(c->sh_ptr);
   if (c->sh_sum) cudaFree(c->sh_sum);
+  if (c->peer_slots) cudaFree(c->peer_slots);
+  if (c->peer_out) cudaFree(c->peer_out);
   if (c->dist) pe_dist_free(c->dist);
   delete c;
   return PE_OK;
@@ -1185,8 +1192,13 @@ static bool outputs_overlap_inputs(const void* const* in, void* const* out, cons
 
 // pe_polar_split: the all-reduce hook of one call
 struct SplitCtx {
-  pe_allreduce_fn fn;
+  pe_allreduce_fn fn;            // all-reduce hook (pe_polar_split), or
   void* user;
+  // pe_polar_split_peers: every rank's partials in peer-visible slots, a
+  // barrier between writing and summing them (fn == nullptr)
+  void* const* slots = nullptr;
+  int rank = 0, world = 1;
+  pe_barrier_fn barrier = nullptr;
 };
 
 // pe_polar and pe_muon_step.  Muon (grads != nullptr, bf16): `in` are the
@@ -1399,18 +1411,58 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       PE_CUDA(cudaMemcpy(c->sh_ptr, &c->sh_a32, sizeof(float*), cudaMemcpyHostToDevice));
     }
     na.sums = c->sh_sum;
+    if (sh->slots) {
+      // the local ||M_r||^2 goes straight into this rank's slot; the slot
+      // pointers (and this rank's two Gram destinations) to the device
+      if (sh->world > c->peer_cap) {
+        PE_CUDA(cudaDeviceSynchronize());
+        if (c->peer_slots) cudaFree(c->peer_slots);
+        c->peer_slots = nullptr;
+        c->peer_cap = 0;
+        if (cudaMalloc(&c->peer_slots, sizeof(uint8_t*) * sh->world) != cudaSuccess) {
+          cudaGetLastError();
+          return PE_ERR_WORKSPACE;
+        }
+        c->peer_cap = sh->world;
+      }
+      if (!c->peer_out && cudaMalloc(&c->peer_out, 2 * sizeof(float*)) != cudaSuccess) {
+        cudaGetLastError();
+        return PE_ERR_WORKSPACE;
+      }
+      const int64_t gbytes = (int64_t)rup(need * sizeof(float), 256);
+      uint8_t* mine = reinterpret_cast<uint8_t*>(sh->slots[sh->rank]);
+      float* outs2[2] = {reinterpret_cast<float*>(mine + 256), reinterpret_cast<float*>(mine + 256 + gbytes)};
+      PE_CUDA(cudaMemcpy(c->peer_slots, sh->slots, sizeof(uint8_t*) * sh->world, cudaMemcpyHostToDevice));
+      PE_CUDA(cudaMemcpy(c->peer_out, outs2, sizeof(outs2), cudaMemcpyHostToDevice));
+      na.sums = reinterpret_cast<double*>(mine);
+    }
   }
   { ProfScope ps(c, 0, st);
     launch(pe_norm_kernel, PE_NORM_PERSIST ? std::min(P->n_chunks, c->norm_blocks) : P->n_chunks, kNormThreads, 0,
            st, na); }
   ++launches;
+  PeerSlots peers{};
+  if (sh && sh->slots) {
+    const MatDev& md0 = P->mats[0];
+    peers.slots = c->peer_slots;
+    peers.world = sh->world;
+    peers.gbytes = (int64_t)rup((size_t)md0.m * md0.ldm * sizeof(float), 256);
+  }
   if (sh) {
     // ||M||_F^2 over every rank's columns, then inv on the device
-    if ((s = sh->fn(c->sh_sum, 1, 1, sh->user, stream_)) != PE_OK) {
-      g_last_error = "pe_polar_split: the all-reduce callback failed";
-      return s;
+    if (sh->slots) {
+      if ((s = sh->barrier(sh->user, stream_)) != PE_OK) {
+        g_last_error = "pe_polar_split_peers: the barrier failed";
+        return s;
+      }
+      launch(pe_inv_peers_kernel, 1, 32, 0, st, peers, at<float>(P, P->o_inv));
+    } else {
+      if ((s = sh->fn(c->sh_sum, 1, 1, sh->user, stream_)) != PE_OK) {
+        g_last_error = "pe_polar_split: the all-reduce callback failed";
+        return s;
+      }
+      launch(pe_inv_kernel, 1, 32, 0, st, (const double*)c->sh_sum, at<float>(P, P->o_inv));
     }
-    launch(pe_inv_kernel, 1, 32, 0, st, (const double*)c->sh_sum, at<float>(P, P->o_inv));
     ++launches;
   }
 
@@ -1634,7 +1686,8 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         g.stats = c->stats + (size_t)mode * 2048;
       }
       const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
-      if (sh && mode == kModeGram) g.out32 = c->sh_ptr;         // partial Gram in fp32
+      if (sh && mode == kModeGram)                               // partial Gram in fp32: own buffer, or
+        g.out32 = sh->slots ? c->peer_out + (t & 1) : c->sh_ptr;  // this rank's peer-visible slot
       if (istep && mode == kModeGram) {
         // App. G: the Gram once more with its raw fp32 accumulator stored, for
         // the power method (its Rayleigh quotient on bf16(A_0) can exceed
@@ -1698,13 +1751,25 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
         // matrix), then rounded once to bf16 (R8; iteration 1 also scales)
         const MatDev& md = P->mats[0];
         const int64_t na32 = (int64_t)md.m * md.ldm;
-        if ((s = sh->fn(c->sh_a32, na32, 0, sh->user, stream_)) != PE_OK) {
-          g_last_error = "pe_polar_split: the all-reduce callback failed";
-          return s;
+        const int grid = (int)std::min<int64_t>(cdiv(na32, 256), c->num_sms * 4);
+        if (sh->slots) {
+          // every rank's partial is in its slot once all ranks pass the
+          // barrier; the sum over the slots (rank order) and the rounding
+          // are one kernel reading peer memory -- no collective call
+          if ((s = sh->barrier(sh->user, stream_)) != PE_OK) {
+            g_last_error = "pe_polar_split_peers: the barrier failed";
+            return s;
+          }
+          launch(pe_round_peers_kernel, grid, 256, 0, st, peers, t & 1, reinterpret_cast<__nv_bfloat16*>(md.A),
+                 na32, (const float*)at<float>(P, P->o_inv), t == 0 ? 1 : 0);
+        } else {
+          if ((s = sh->fn(c->sh_a32, na32, 0, sh->user, stream_)) != PE_OK) {
+            g_last_error = "pe_polar_split: the all-reduce callback failed";
+            return s;
+          }
+          launch(pe_round_gram_kernel, grid, 256, 0, st, (const float*)c->sh_a32,
+                 reinterpret_cast<__nv_bfloat16*>(md.A), na32, (const float*)at<float>(P, P->o_inv), t == 0 ? 1 : 0);
         }
-        launch(pe_round_gram_kernel, std::min<int64_t>(cdiv(na32, 256), c->num_sms * 4), 256, 0, st,
-               (const float*)c->sh_a32, reinterpret_cast<__nv_bfloat16*>(md.A), na32,
-               (const float*)at<float>(P, P->o_inv), t == 0 ? 1 : 0);
         ++launches;
       }
     }
@@ -1835,6 +1900,34 @@ extern "C" pe_status pe_polar_split(pe_ctx c, const void* in, void* out, int64_t
   const void* ins[1] = {in};
   void* outs[1] = {out};
   SplitCtx sh{allreduce, user};
+  return polar_impl(c, ins, outs, nullptr, shp, 1, iters, PE_BF16, stream, 0.0, 0.0, nullptr, &sh);
+}
+
+extern "C" pe_status pe_split_slot_bytes(int64_t rows, int64_t cols, int64_t* bytes) {
+  if (rows < 1 || cols < 1 || !bytes) return PE_ERR_INVALID_ARG;
+  const size_t g = rup((size_t)rows * rup((size_t)rows, 8) * sizeof(float), 256);
+  *bytes = (int64_t)(256 + 2 * g);
+  return PE_OK;
+}
+
+extern "C" pe_status pe_polar_split_peers(pe_ctx c, const void* in, void* out, int64_t rows, int64_t cols, int iters,
+                                          void* const* slots, int rank, int world, pe_barrier_fn barrier, void* user,
+                                          void* stream) {
+  if (!c || !in || !out || iters < 1 || !slots || !barrier || world < 1 || rank < 0 || rank >= world)
+    return PE_ERR_INVALID_ARG;
+  for (int r = 0; r < world; ++r)
+    if (!slots[r] || (reinterpret_cast<uintptr_t>(slots[r]) & 255)) {
+      g_last_error = "pe_polar_split_peers: every slot must be a 256-byte aligned device pointer";
+      return PE_ERR_INVALID_ARG;
+    }
+  const int64_t shp[2] = {rows, cols};
+  const void* ins[1] = {in};
+  void* outs[1] = {out};
+  SplitCtx sh{nullptr, user};
+  sh.slots = slots;
+  sh.rank = rank;
+  sh.world = world;
+  sh.barrier = barrier;
   return polar_impl(c, ins, outs, nullptr, shp, 1, iters, PE_BF16, stream, 0.0, 0.0, nullptr, &sh);
 }
 

@@ -860,6 +860,69 @@ def _virtual_ranks_sharded(shards, T=5):
     return outs
 
 
+def _virtual_ranks_peers(shards, T=5):
+    """pe_polar_split_peers for every column block in its own host thread
+    (one context and stream each, one GPU): the slots are plain device
+    buffers every thread can read; the barrier synchronises this rank's
+    stream and meets the other threads (no kernel waits on another)."""
+    import threading
+    W = len(shards)
+    bar = threading.Barrier(W, timeout=120)
+    nbytes = pe.pe_split_slot_bytes(*shards[0].shape)
+    slots = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(W)]
+    assert all(sl.data_ptr() % 256 == 0 for sl in slots)
+    outs, errs, nbar = [None] * W, [], [0] * W
+
+    def run(r):
+        try:
+            c = pe.Context(0)
+            st = torch.cuda.Stream()
+
+            def barrier(handle):
+                torch.cuda.ExternalStream(handle, device=0).synchronize()
+                nbar[r] += 1
+                bar.wait()
+
+            with torch.cuda.stream(st):
+                outs[r] = c.polar_split_peers(shards[r], slots, r, barrier, iters=T)
+            st.synchronize()
+            c.close()
+        except Exception as e:                                # pragma: no cover
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    return outs, nbar
+
+
+@pytest.mark.parametrize("shape,W", [((768, 3072), 2), ((512, 4096), 4), ((300, 1600), 2), ((1024, 1024), 2)])
+def test_polar_split_peers_virtual_ranks(ctx, shape, W):
+    """pe_polar_split_peers (SURVEY §8f NEXT 2 without a collective call):
+    every rank's norm pass and Gram epilogue write their partials straight
+    into its peer-visible slot, and after a barrier one library kernel sums
+    the slots in rank order and rounds A.  W virtual ranks on one GPU: the
+    result equals the all-reduce-hook path (the same sums, rank order) bit
+    for bit, the joined matrix passes G1 / G3 against the oracle on the whole
+    matrix, and the barrier is called once for the norm plus once per
+    iteration."""
+    M = bf16_values(syn.gaussian(*shape, seed=shape[1] + W, std=0.02))
+    cols = shape[1] // W
+    shards = [to_dev_bf16(M[:, r * cols:(r + 1) * cols]) for r in range(W)]
+    peers, nbar = _virtual_ranks_peers(shards, T=5)
+    hook = _virtual_ranks_sharded(shards, T=5)
+    torch.cuda.synchronize()
+    for a, b in zip(peers, hook):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert nbar == [1 + 5] * W
+    X = np.concatenate([p.float().cpu().numpy().astype(np.float64) for p in peers], axis=1)
+    check_g1_g3(X, M)
+
+
 @pytest.mark.parametrize("shape,W", [((768, 3072), 2), ((512, 4096), 4), ((300, 1600), 2), ((1024, 1024), 2)])
 def test_polar_split_virtual_ranks(ctx, shape, W):
     """NEXT row 2 (intra-matrix sharding): the column blocks of one matrix,
