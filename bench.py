@@ -478,7 +478,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama3-8b")
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--extra", default="gpt2-small,gpt2-large,llama3-8b-literal,llama3-8b:alg4r3",
+    ap.add_argument("--extra", default="gpt2-small,gpt2-large,llama3-8b-literal,llama3-8b:alg4r3,gpt2-large:alg4r3,gpt2-small:alg4r3",
                     help="comma list of extra layer sets (N=1 only; '<set>:alg4r<k>' = with App. H Alg. 4), or ''")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
