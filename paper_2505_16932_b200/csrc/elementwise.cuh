@@ -55,13 +55,26 @@ struct NormArgs {
   double* ssq;                 // spectrum-aware init: per matrix sum of squares, or nullptr
 };
 
+// |x| of a bf16 (bit pattern in the low 16 bits of h) as an fp64 value built
+// with integer ops: exponent e + (1023 - 127), the 7 mantissa bits on top of
+// the fp64 mantissa.  The F2F.F64.F32 conversion it replaces runs at a
+// quarter of the issue rate and made the norm pass issue-bound (71 % of HBM)
+// when the power cap pulled the SM clock to ~1.1 GHz.  Exact for normal bf16
+// values; zero and subnormals become ~2^-127 (their squares, <= 2^-252, vanish
+// in any sum of a non-negligible matrix, and a matrix of only such values has
+// s = 1e-7 either way); Inf / NaN become 2^128 (the iteration still
+// propagates them: X_0 = M inv).
+__device__ __forceinline__ double bf16_abs_f64(uint32_t h) {
+  return __hiloint2double((int)(((h & 0x7FFFu) << 13) + 0x38000000u), 0);
+}
+
 __device__ __forceinline__ double sumsq8_bf16(uint4 u) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
   double acc = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float2 f = __bfloat1622float2(h[q]);
-    acc += (double)f.x * f.x + (double)f.y * f.y;   // exact in fp64 (an fp32 square overflows past |x| ~ 1.8e19)
+    const double a = bf16_abs_f64(w[q]), b = bf16_abs_f64(w[q] >> 16);
+    acc += a * a + b * b;   // exact squares in fp64 (an fp32 square overflows past |x| ~ 1.8e19)
   }
   return acc;
 }
