@@ -208,6 +208,11 @@ def test_shard_layout_chunks_hold_each_owners_matrices():
     assert L.pe_sharded_exchange(None, None, None, 1, 0, None) == 1
     assert L.pe_set_rect_iteration(None, 2, 0.0, 1e-3) == 1
     assert L.pe_set_debug(None, 1) == 1
+    assert L.pe_set_small_planes(None, 2) == 1
+    assert L.pe_polar_split_peers(None, None, None, 1, 1, 5, None, 0, 1, pe.BARRIER_FN(), None, None) == 1
+    n = ctypes.c_int64()
+    assert L.pe_split_slot_bytes(0, 8, ctypes.byref(n)) == 1
+    assert L.pe_split_slot_bytes(768, 1536, ctypes.byref(n)) == 0 and n.value == 256 + 2 * 768 * 768 * 4
     assert L.pe_count_nonfinite(None, None, None, 0, 0, None, None) == 1
 
 

@@ -1775,6 +1775,19 @@ def test_alg4_restart_one_is_listing2_and_mixed_batches():
     c.set_rect_iteration(0)
     for X, Y in zip(run(c, mats, T=5), ref):
         assert np.array_equal(X, Y)
+    # under CUDA-graph capture a qualifying matrix is refused (PE_ERR_UNSUPPORTED)
+    c.set_rect_iteration(2, 0.0, 1e-3)
+    xs = [to_dev_bf16(mats[1])]
+    ys = [torch.empty_like(xs[0])]
+    c.reserve([shapes[1]], pe.PE_BF16)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(pe.PeError) as ei:
+        with torch.cuda.graph(g):
+            c.polar(xs, ys, iters=5)
+    assert ei.value.status == 2
+    del g
+    torch.cuda.synchronize()
     c.close()
     base.close()
 
