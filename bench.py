@@ -557,7 +557,11 @@ def main():
         "peak_used": f"{peaks[peak_key]} TFLOP/s ({src} {'sustained' if peak_key.endswith('sustained') else 'burst'})",
         "e2e": {"value": round(len(shapes) / (e2e_mean * 1e-3), 3), "unit": UNIT,
                 "ms_per_step": round(e2e_mean, 3),
-                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes},
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+                "note": "pe_polar_host on pinned host tensors, wall clock per call (host->device copies, compute, "
+                        "device->host copies; synchronises): the batch is pipelined in groups so the PCIe transfers "
+                        "(both directions concurrently) hide behind the compute except the first group's H2D and "
+                        "the last group's D2H; no L2 flush between calls"},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
