@@ -359,7 +359,9 @@ pe_status pe_set_small_planes(pe_ctx ctx, int planes);
  * Debug aids (never on the hot path).
  * pe_count_nonfinite: *nonfinite = number of NaN / Inf elements over the
  *   `count` device buffers (rows x cols of `dtype` each); synchronises
- *   `stream`; PE_ERR_UNSUPPORTED under graph capture.
+ *   `stream`; PE_ERR_UNSUPPORTED under graph capture.  Uses a counter owned
+ *   by the context: like every call on a context, not from two host threads
+ *   at once.
  * pe_set_debug(ctx, PE_DEBUG_CHECK_FINITE): later pe_polar / pe_polar_ex
  *   calls scan their inputs before launching anything (non-finite inputs:
  *   PE_ERR_NONFINITE, nothing computed) and their outputs after the call
