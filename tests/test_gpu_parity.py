@@ -1966,3 +1966,23 @@ def test_full_llama_set_alg4_sampled():
         P = oi.exact_polar(M)
         assert np.all(np.isfinite(X)) and om.rel_frobenius(X, ref) <= ALG4_G1[3]
         assert om.rel_frobenius(X, P) <= om.rel_frobenius(ref, P) + 1e-2
+
+
+@pytest.mark.slow
+def test_polar_split_peers_max_size_hadamard():
+    """The sweep's largest matrix (16384^2, BASELINE configs[4]) split by
+    columns over 4 virtual ranks through pe_polar_split_peers: the joined
+    result follows the equal-sigma closed form X_T = p*(sigma_hat) H / sqrt(n)
+     within the bf16 gate on every 97th row."""
+    n, W = 16384, 4
+    H = syn.hadamard_rows(n, n, dtype=np.float32)
+    cols = n // W
+    shards = [to_dev_bf16(H[:, r * cols:(r + 1) * cols]) for r in range(W)]
+    outs, nbar = _virtual_ranks_peers(shards, T=5)
+    torch.cuda.synchronize()
+    assert nbar == [6] * W
+    sh = math.sqrt(n) / (1.01 * n + 1e-7)
+    s = float(oi.composite(sh, TABLE, 5))
+    Y = np.concatenate([o[::97].float().cpu().numpy().astype(np.float64) for o in outs], axis=1)
+    assert np.all(np.isfinite(Y))
+    assert om.rel_frobenius(Y, s * H[::97].astype(np.float64) / math.sqrt(n)) <= 2e-2
