@@ -1841,18 +1841,14 @@ static pe_status checked_call(pe_ctx c, const void* const* in, void* const* out,
   pe_status s = pe_count_nonfinite(c, in, shapes, count, in_t, &k, stream);
   if (s != PE_OK) return s;
   if (k > 0) {
-    static thread_local std::string msg;
-    msg = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite input values";
-    g_last_error = msg.c_str();
+    g_last_error = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite input values";
     return PE_ERR_NONFINITE;
   }
   if ((s = call()) != PE_OK) return s;
   if ((s = pe_count_nonfinite(c, const_cast<const void* const*>(out), shapes, count, out_t, &k, stream)) != PE_OK)
     return s;
   if (k > 0) {
-    static thread_local std::string msg;
-    msg = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite outputs from finite inputs";
-    g_last_error = msg.c_str();
+    g_last_error = "PE_DEBUG_CHECK_FINITE: " + std::to_string(k) + " non-finite outputs from finite inputs";
     return PE_ERR_NONFINITE;
   }
   return PE_OK;
