@@ -217,13 +217,14 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
     tot, cnt = prof[kind]
     per_launch_ms = tot / max(cnt, 1)
     sustained = step_ms > 50.0
-    traffic, traffic_src = None, None
+    traffic, traffic_src, ncu_kind = None, None, None
     try:
         # written by profiles/ncu_traffic.py from an `ncu --set full` capture
         # (dram__bytes_read.sum + dram__bytes_write.sum of that kernel)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(workload or "", {})
             traffic, traffic_src = tj.get(kind), tj.get("_source")
+            ncu_kind = tj.get(kind + "_ncu")
     except Exception:
         pass
     if kind in fl:
@@ -237,6 +238,7 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
     out.update({"kernel": f"pe_gemm_sm100[{kind}]" if kind in fl else kind, "achieved": round(achieved, 2),
                 "peak": peak, "peak_source": f"{src} {'sustained' if (sustained and kind in fl) else 'burst'}",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "ncu": ncu_kind,
                 "algorithmic_per_launch": (fl[kind] if kind in fl else by[kind]),
                 "launch_ms": round(per_launch_ms, 4),
                 "timing": "CUDA events around each launch of this kernel, on its stream, in a second pass of the same K steps",
