@@ -9,10 +9,13 @@ the reading, not from the kernels (the two share no code):
 
   R2/R8 normalisation: s = sqrt(sum x^2) * 1.01 + 1e-7 in fp64,
         inv = fp32(1/s)
-  folded inputs (rows of 16-byte multiples; X_0 = M/s is never rounded):
+  bf16 inputs (``folded=True``; X_0 = M/s is never rounded -- rows of
+  16-byte multiples are read in place, others through an exact copy
+  M 2^e with 1/s 2^-e applied below, which is bit-identical):
         Gram 1:    A = bf16(fp32(x*x) * fp32(inv*inv))
         update 1:  X_1 = bf16(fp32(fp32(a*x) + B*x) * inv)
-  other inputs: X_0 = bf16(fp32(x) * inv), then the generic steps
+  fp32 inputs of pe_polar_ex (``folded=False``): X_0 = bf16(fp32(x) * inv),
+  then the generic steps
   Gram (P:498):      A = bf16(x*x)
   poly:      B = bf16(fp32(b*A) + fp32(c*(A*A)))   (no FMA contraction)
   update:    X' = bf16(fp32(a*X) + (B*X))          (no FMA contraction)
@@ -46,7 +49,8 @@ def diagonal_bf16(sigmas_bf16, table, T, folded=True, ab_planes=1):
     """Diagonal of the GPU's bf16 result for M = diag(sigmas) (any padding).
     ``sigmas_bf16`` must already be bf16 values (the GPU input); ``folded``
     says whether the normalisation is folded into the first iteration (the
-    path the GPU takes when the caller's rows are 16-byte multiples).
+    path the GPU takes for every bf16 input; ``False``: an explicit rounded
+    X_0, the fp32-input path).
     ``ab_planes = 2``: the small path's precise variant (reading R8p): A and
     B kept as two bf16 planes; a product with a two-plane operand is its big
     plane product plus the small ones, one fp32 add."""
@@ -204,3 +208,65 @@ def r19_alg4(M_bf16, table, T, restart=None, shift=1e-3, folded=True):
         acc = mm(Q, X)
         X = _bf16(np.float32(acc * inv) if scaled else acc)
     return X.T if tall else X
+
+
+def r17_init_polar_express(M_bf16, table, T, power_iters, folded=True):
+    """App. G's first step at the GPU design's rounding points
+    (reading R17), then ``T`` iterations as ``r8_polar_express``:
+        acc = X X^T  (exact, rounded once to fp32; X = M when folded, else
+                      X_0 = bf16(M inv))
+        z   = sqrt(lambda / d): lambda the Rayleigh quotient of ``power_iters``
+              power steps on the fp32 acc (start vector of iteration.power_start),
+              d = ||M||^2 (folded) or ||M||^2 inv^2
+        (a, b) = eq. (init_poly) at z when 1/sqrt(2) <= z <= 1 - 1e-6,
+              else (1, 0); F^2 = ||M||^2 inv^2; a' = fp32(a / F), b' = fp32(b / F^3)
+        A_0 = bf16(acc [* inv^2])
+        X_1 = bf16(fp32(fp32(a' X) + fp32(b' (A_0 X))) [* inv])
+    Used to measure how far the bf16 design's own rounding of this step
+    (the b / F^3 ~ 1 / sqrt(1 - z^2) amplification of A_0's rounding as
+    z -> 1) moves the result from the fp64 step.  Returns (X_T, z, applied)."""
+    from .iteration import power_start, init_cubic, INIT_Z_MIN, INIT_Z_MAX
+
+    def mm(P, Q):
+        return (P.astype(np.float64) @ Q.astype(np.float64)).astype(np.float32)
+
+    M = np.asarray(M_bf16, dtype=np.float32)
+    tall = M.shape[0] > M.shape[1]
+    X = (M.T if tall else M).copy()
+    ssq = float(np.sum(X.astype(np.float64) ** 2))
+    nrm = np.sqrt(ssq) * 1.01 + 1e-7
+    inv = np.float32(1.0 / nrm)
+    if not folded:
+        X = _bf16(X * inv)
+    acc = mm(X, X.T)
+    f2 = ssq * float(inv) * float(inv)
+    d = ssq if folded else f2
+    A64 = acc.astype(np.float64)
+    v = power_start(A64.shape[0])
+    lam = 0.0
+    for _ in range(power_iters):
+        w = A64 @ v
+        lam = float(v @ w) / float(v @ v)
+        v = w / np.sqrt(float(w @ w))
+    z = np.sqrt(lam / d) if d > 0 and lam > 0 else 0.0
+    applied = INIT_Z_MIN <= z <= INIT_Z_MAX
+    if applied:
+        a, b = init_cubic(z)
+        F = np.sqrt(f2)
+        ca, cb = np.float32(a / F), np.float32(b / F ** 3)
+    else:
+        ca, cb = np.float32(1.0), np.float32(0.0)
+    A0 = _bf16(np.float32(acc * np.float32(inv * inv))) if folded else _bf16(acc)
+    X1 = np.float32(np.float32(ca * X) + np.float32(cb * mm(A0, X)))
+    X = _bf16(np.float32(X1 * inv)) if folded else _bf16(X1)
+    for tup in schedule(table, T):
+        a, b = np.float32(tup[0]), np.float32(tup[1])
+        A = _bf16(mm(X, X.T))
+        if len(tup) == 3:
+            c = np.float32(tup[2])
+            B = _bf16(np.float32(b * A) + np.float32(c * mm(A, A)))
+            BX = mm(B, X)
+        else:
+            BX = np.float32(b * mm(A, X))
+        X = _bf16(np.float32(a * X) + BX)
+    return (X.T if tall else X), z, applied

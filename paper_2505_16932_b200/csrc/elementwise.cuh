@@ -221,6 +221,7 @@ struct CopyArgs {
   const void* const* srcs;     // per matrix source
   void* const* dsts;           // per matrix destination
   const float* scale;          // per matrix multiplier or nullptr
+  int pow2;                    // multiply by the power-of-two part of scale only (pow2_part, exact)
   int muon;                    // finalize of pe_muon_step: dst = bf16(dst - lr * src) (Muon W update)
   float lr;
 };
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(256) pe_rows_kernel(const CopyArgs a) {
     const CopyMat cm = a.mats[ci.mat];
     const S* src = reinterpret_cast<const S*>(a.srcs[ci.mat]);
     D* dst = reinterpret_cast<D*>(a.dsts[ci.mat]);
-    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const float sc = a.scale ? (a.pow2 ? pow2_part(a.scale[ci.mat]) : a.scale[ci.mat]) : 1.0f;
     const bool vec = (cm.cols % V == 0) && (cm.sld % V == 0) && (cm.dld % V == 0) &&
                      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     if (vec) {
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(256) pe_transpose_kernel(const CopyArgs a) {
     const CopyMat cm = a.mats[ci.mat];
     const S* src = reinterpret_cast<const S*>(a.srcs[ci.mat]);
     D* dst = reinterpret_cast<D*>(a.dsts[ci.mat]);
-    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const float sc = a.scale ? (a.pow2 ? pow2_part(a.scale[ci.mat]) : a.scale[ci.mat]) : 1.0f;
     const int r0 = ci.a * 64, c0 = ci.b * 64;
     const bool vin = (cm.sld % V == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
     const bool vout = (cm.dld % W == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) pe_planes_kernel(const CopyArgs a) {
   for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
     const CopyItem ci = a.items[it];
     const CopyMat cm = a.mats[ci.mat];
-    const float sc = a.scale ? a.scale[ci.mat] : 1.0f;
+    const float sc = a.scale ? (a.pow2 ? pow2_part(a.scale[ci.mat]) : a.scale[ci.mat]) : 1.0f;
     const int r0 = ci.a * 64, c0 = ci.b * 64;
     auto put = [&](int dr, int dc, float f) {
       if (kSplit) {
@@ -797,10 +798,13 @@ __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   // lam is the Rayleigh quotient of the fp32 Gram the iteration-1 GEMM
-  // accumulated: of M M^T (unscaled) for folded matrices, of X_0 X_0^T for
-  // the others; z = sigma_1 / ||.||_F on the same scale
+  // accumulated: of M M^T for folded bf16 input (flags 8 | 1), of 4^e M M^T
+  // for copied bf16 input (flag 8), of X_0 X_0^T = (M/s)(M/s)^T for fp32
+  // input; z = sigma_1 / ||.||_F on the same scale
   const double f2 = ssq[i] * (double)inv[i] * (double)inv[i];
-  const double den2 = (mflags[i] & 1) ? ssq[i] : f2;
+  // bf16 copies hold M * 2^e (pow2_part): their Gram is 4^e M M^T
+  const double p2 = (double)pow2_part(inv[i]);
+  const double den2 = (mflags[i] & 8) ? ((mflags[i] & 1) ? ssq[i] : ssq[i] * p2 * p2) : f2;
   const double z = (den2 > 0.0 && lam[i] > 0.0) ? sqrt(lam[i] / den2) : 0.0;
   float ca = 1.f, cb = 0.f;
   if (z >= 0.70710678118654752 && z <= 1.0 - 1e-6) {

@@ -67,6 +67,8 @@ namespace pe {
 constexpr int kFlagFolded = 1;   // iteration 1 reads the caller's M (no X_0 buffer)
 constexpr int kFlagTall = 2;     // caller matrix is rows > cols (iterate on M^T)
 constexpr int kFlagDirect = 4;   // last update writes the caller's output buffer
+constexpr int kFlagScaled = 8;   // iteration 1 reads the unscaled bf16 M (the caller's, or an exact
+                                 // oriented copy) and applies 1/s in its epilogues (reading R8)
 
 struct GemmArgs {
   const Tile* tiles;
@@ -142,7 +144,8 @@ struct TileCfg {
   bool ein_tr;                 // operand chunk is M^T of a tall caller matrix
   const CUtensorMap* eout;     // result chunk map
   bool eout_tr;                // result chunk is stored transposed (tall caller output)
-  bool scaled;                 // first iteration of a folded matrix
+  bool scaled;                 // first iteration of a bf16-input matrix: 1/s in the epilogue
+  bool pre;                    // ... whose X_0 is the copy M * 2^e: the epilogue applies 1/s * 2^-e
   bool muon;                   // result chunk is a Muon weight update of the chunk already at eout
   bool lin;                    // update of a cubic step: left operand A, epilogue a X + b acc
   bool rr;                     // poly of Alg. 4's R: the true product R R, not R R^T -- R = Q T is not
@@ -198,7 +201,9 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   const int fl = kEdge ? g.mflags[tl.mat] : 0;
   const bool fold = kEdge && c.first && (fl & kFlagFolded);
   const bool tall = kEdge && (fl & kFlagTall) != 0;
-  c.scaled = fold;
+  const bool scl = kEdge && c.first && (fl & kFlagScaled);
+  c.scaled = scl;
+  c.pre = scl && !(fl & kFlagFolded);
   c.muon = false;
   c.lin = false;
   c.rr = false;
@@ -229,7 +234,7 @@ __device__ __forceinline__ TileCfg tile_cfg(const GemmArgs& g, const Tile& tl, u
   } else {
     const bool gen = g.nphase == 0 && g.gen != 0;
     const bool rx = !gen || g.g_rx != 0;             // right operand is the iterate
-    c.scaled = fold && rx;
+    c.scaled = scl && rx;
     c.lin = g.nphase == 0 && g.lin != 0;
     if (gen) {
       c.A = maps + g.g_l;
@@ -823,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         nnc = ncols_of(ntl, ncfg);
       }
       const bool need_load = needs_load(cfg);
-      const float inv = cfg.scaled ? args.inv[tl.mat] : 1.0f;
+      const float inv = !cfg.scaled ? 1.0f : cfg.pre ? pow2_residual(args.inv[tl.mat]) : args.inv[tl.mat];
       long long t2 = clock64();
       mbar_wait(&tfull[acc], acc_phase);
       st_wait_tfull += clock64() - t2;

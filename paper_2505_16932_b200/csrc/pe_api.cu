@@ -2,7 +2,8 @@
 // launch sequence of one Polar Express call (Listing 2):
 //
 //   pe_norm_kernel                       s = ||M||_F*1.01 + 1e-7
-//   copy pass (unfolded inputs only)     X_0 = M/s, wide orientation
+//   copy pass (unfolded inputs only)     X_0 = M 2^e, wide orientation; the
+//                                        rest of 1/s is applied by iteration 1 (fp32 input: X_0 = M/s)
 //   T x { pe_gemm_sm100 Gram            A = X X^T
 //         pe_gemm_sm100 Poly            B = b A + c A^2
 //         pe_gemm_sm100 Update          X = a X + B X }
@@ -731,7 +732,14 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     const bool foldable = (dtype == PE_BF16) && (md.cols % 8 == 0) && !getenv("PE_NO_FOLD");
     const bool folded = foldable && !(io & 1);
     const bool direct = foldable && !(io & 2) && !no_direct;
-    mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0);
+    // bf16 input: X_0 is never rounded -- the copy pass (if any) stores
+    // M * 2^e exactly (pow2_part of 1/s) and iteration 1 applies the residual
+    // 1/s * 2^-e, bit-identical to the folded path (R8, R18); rounding
+    // bf16(M/s) would add a second input-sized rounding noise that the
+    // iteration lifts as if it were spectrum
+    const bool scaled = (dtype == PE_BF16) && !(io & 1);
+    mflags[i] = (folded ? kFlagFolded : 0) | (md.tall ? kFlagTall : 0) | (direct ? kFlagDirect : 0) |
+                (scaled ? kFlagScaled : 0);
     x0[i] = md.X[0];
     const int64_t pst = (int64_t)md.m * md.ldx;
     smats[i] = {md.rows, md.cols, md.cols, md.ldx, pst};
@@ -1130,7 +1138,7 @@ static pe_status small_call(pe_ctx c, const void* const* in, void* const* out, c
     sm.m = sm.tall ? sm.cols : sm.rows;
     sm.n = sm.tall ? sm.rows : sm.cols;
     sm.n_pad = (int)rup(sm.n, 64);
-    sm.fold = (dtype == PE_BF16) && (sm.cols % 8 == 0) && !getenv("PE_NO_FOLD");   // as build_plan
+    sm.fold = (dtype == PE_BF16);   // X_0 = M exactly, 1/s in iteration 1 (kFlagScaled in build_plan)
     sm.pad = 0;
   }
   SmallCta* hct = inl ? a.inl_cta : reinterpret_cast<SmallCta*>(reinterpret_cast<uint8_t*>(cs->h) + mats_bytes);
@@ -1466,7 +1474,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     ++launches;
   }
 
-  // 2) X_0 = M / s (oriented)
+  // 2) X_0 = M 2^e (bf16, exact) or M / s (fp32 input), oriented
   auto copy_pass = [&](int k, bool scale, bool fin) {
     if (P->n_it[k] == 0) return;
     CopyArgs ca;
@@ -1476,6 +1484,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
     ca.srcs = fin ? d_fin_src : d_in;
     ca.dsts = fin ? d_out : at<void*>(P, P->o_x0);
     ca.scale = scale ? at<float>(P, P->o_inv) : nullptr;
+    ca.pow2 = (!fin && dtype == PE_BF16 && !(io & 1)) ? 1 : 0;    // kFlagScaled copies: X_0 = M * 2^e
     ca.muon = (muon && fin) ? 1 : 0;
     ca.lr = (float)lr;
     const int grid = std::min(P->n_it[k], c->num_sms * 8);

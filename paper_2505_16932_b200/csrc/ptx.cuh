@@ -268,4 +268,14 @@ __device__ __forceinline__ void acquire_counter(const int* ctr, int need) {
   fence_async_global();
 }
 
+
+// Exact power-of-two split of 1/s for bf16 inputs that go through an oriented
+// copy (reading R8/R18): the copy stores X_0 = M * 2^e (exact: an exponent
+// shift), iteration 1 applies the residual 1/s * 2^-e in [1, 2).  Every fp32
+// step commutes with the shift, so the result is bit-identical to reading M
+// and applying 1/s (the folded path), while the first Gram stays in range
+// for any finite input scale.
+__device__ __forceinline__ int pow2_exp(float inv) { return inv > 0.f ? ilogbf(inv) : 0; }
+__device__ __forceinline__ float pow2_part(float inv) { return scalbnf(1.0f, pow2_exp(inv)); }
+__device__ __forceinline__ float pow2_residual(float inv) { return scalbnf(inv, -pow2_exp(inv)); }
 }  // namespace pe

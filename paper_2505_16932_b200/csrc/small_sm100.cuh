@@ -9,8 +9,8 @@
 // The arithmetic is the large kernel's, step for step, so results are
 // bit-identical to it (tests/test_gpu_parity.py::test_small_path_*):
 //   bf16 (kP = 1): R8 rounding points, the folded first iteration
-//     (A = bf16(acc inv^2), X1 = bf16((a m + acc) inv)) exactly when the large
-//     path folds (cols % 8 == 0), else X_0 = bf16(m inv); K accumulated in
+//     (A = bf16(acc inv^2), X1 = bf16((a m + acc) inv)) on every bf16 input,
+//     as the large path (kFlagScaled: X_0 = M is never rounded); K accumulated in
 //     64-wide blocks of four K=16 steps in ascending order;
 //   fp32 (kP = 3): three bf16 planes per buffer, the six plane products small
 //     terms first, the big p0 q0 chain split over two TMEM buffers at the
@@ -55,7 +55,7 @@ struct SmallMat {
   int m, n;              // wide orientation (m <= n)
   int n_pad;             // n rounded up to 64
   int tall;
-  int fold;              // bf16 with cols % 8 == 0: the large path folds 1/s into iteration 1
+  int fold;              // bf16 input: X_0 = M exactly, 1/s applied by iteration 1 (as the large path)
   int pad;
 };
 
@@ -425,6 +425,22 @@ __global__ void __launch_bounds__(kSmallThreads, 1) pe_small_sm100(const __grid_
     __syncthreads();                                // red is reused by the next slot
     inv_s[sl] = inv;
     fold_s[sl] = fold;
+    if (fold && (pow2_exp(inv) < -60 || pow2_exp(inv) > 60)) {
+      // X holds M exactly; at extreme scales the first Gram M M^T would leave
+      // the fp32 range: X_0 = M 2^e in place (exact) and 1/s 2^-e in
+      // iteration 1, bit-identical to the unshifted arithmetic (R18)
+      __syncthreads();                              // the first pass's X writes
+      const float p2 = pow2_part(inv);
+      for (int q = tid; q < m * nu; q += kSmallThreads) {
+        const uint32_t off = small_unit(roff + q / nu, q % nu);
+        float f[8];
+        small_load8<1>(X, 0, off, f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(f[k], p2);
+        small_store8<1>(X, 0, off, f);
+      }
+      inv_s[sl] = pow2_residual(inv);
+    }
     if (!fold && md.tall) {                         // second (L2-hot) pass: X_0 = m * inv
       for (int u0 = 0; u0 < nu; u0 += 4) {
         float f[4][8];

@@ -31,7 +31,7 @@ def sweep():
             M = syn.to_bf16_values(syn.gaussian(*shape, seed=7, std=0.02)).astype(np.float64)
             X = c.polar([dev(M)], iters=T)[0].float().cpu().numpy().astype(np.float64)
             emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=0.0,
-                                   folded=shape[1] % 8 == 0).astype(np.float64)
+                                   folded=True).astype(np.float64)
             print(f"T={T} r={restart} {shape}: gpu-vs-emu {om.rel_frobenius(X, emu):.4f}", flush=True)
     c.close()
 
@@ -52,7 +52,7 @@ def main():
             X = y.float().cpu().numpy().astype(np.float64)
             M = mats[i]
             emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift,
-                                   folded=M.shape[1] % 8 == 0).astype(np.float64)
+                                   folded=True).astype(np.float64)
             ref = a4.alg4(M, TABLE, T, restart=restart, shift=shift)
             print(name, M.shape, f"gpu-vs-emu {om.rel_frobenius(X, emu):.4f}  gpu-vs-oracle {om.rel_frobenius(X, ref):.4f}"
                   f"  emu-vs-oracle {om.rel_frobenius(emu, ref):.4f}", flush=True)
@@ -64,7 +64,7 @@ def main():
         y = c.polar([dev(M)], iters=T)[0]
         torch.cuda.synchronize()
         X = y.float().cpu().numpy().astype(np.float64)
-        emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift, folded=shape[1] % 8 == 0)
+        emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift, folded=True)
         d = np.abs(X - emu)
         print("diag", shape, "max |gpu - emu|", d.max(), "at", np.unravel_index(np.argmax(d), d.shape), flush=True)
     c.close()

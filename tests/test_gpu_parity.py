@@ -162,11 +162,13 @@ def test_prescribed_spectrum(ctx, kappa, shape):
 def test_diagonal_bit_exact(ctx, shape):
     """Diagonal inputs: every product has one non-zero term, so the GPU must
     equal the R8 rounding-point emulation bit for bit.  Rows that are
-    16-byte multiples take the folded-normalisation path, the others the
-    explicit X_0 path; the small shapes are also run with the small path's
-    two-plane variant (pe_set_small_planes(2)) against its emulation (R8p)."""
+    16-byte multiples are read in place, the others through an exact oriented
+    copy; the small shapes are also run with the small path's
+    two-plane variant (pe_set_small_planes(2)) against its emulation (R8p).
+    Both paths scale in iteration 1 (X_0 = M is never rounded for bf16 input,
+    reading R8), so the emulation is the folded one on every shape."""
     k = min(shape)
-    folded = shape[1] % 8 == 0
+    folded = True
     sig = syn.to_bf16_values(np.linspace(1.0, 0.02, k)).astype(np.float64)
     M = syn.diagonal(*shape, sig)
     for T in (1, 3, 5, 8):
@@ -304,7 +306,7 @@ def test_degree3_table_skips_the_square(ctx, shape):
                 X = run(ctx, [M], T=T)[0]
                 launches[(deg, T)] = ctx.last_launch_count()
                 if deg == 3:
-                    emu = emulate.diagonal_bf16(sig, tab3, T, folded=shape[1] % 8 == 0).astype(np.float64)
+                    emu = emulate.diagonal_bf16(sig, tab3, T, folded=True).astype(np.float64)
                     assert np.array_equal(np.diag(X)[:k], emu), T
             if deg == 3:
                 X = run(ctx, [G], T=8)[0]
@@ -1032,11 +1034,11 @@ def test_back_to_back_async_calls_stress(ctx):
 
 
 def _r8_emulated(M, T, f32_input=False, precise=False):
-    """oracle.emulate.r8_polar_express on the path the library takes: folded
-    for bf16 rows of 16-byte multiples, explicit X_0 = bf16(fp32(x) inv) for
-    the others and for fp32 input (pe_polar_ex, R16); two-plane A/B when the
-    call ran on the small path's precise variant (R8p)."""
-    fold = M.shape[1] % 8 == 0 and not f32_input
+    """oracle.emulate.r8_polar_express on the path the library takes: 1/s
+    folded into iteration 1 for bf16 input (X_0 = M exactly, any shape),
+    explicit X_0 = bf16(fp32(x) inv) for fp32 input (pe_polar_ex, R16);
+    two-plane A/B when the call ran on the small path's precise variant (R8p)."""
+    fold = not f32_input
     return emulate.r8_polar_express(M, TABLE, T, folded=fold, ab_planes=2 if precise else 1).astype(np.float64)
 
 
@@ -1744,7 +1746,7 @@ def test_alg4_diagonal_bit_exact(shape, restart, shift):
     c = _alg4_ctx(restart, shift)
     for T in (2, 5):
         X = run(c, [M], T=T)[0]
-        emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift, folded=shape[1] % 8 == 0)
+        emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift, folded=True)
         assert np.array_equal(X, emu.astype(np.float64)), (T, np.abs(X - emu).max())
     c.close()
 
@@ -1889,7 +1891,7 @@ def test_alg4_random_calls_fuzz():
                 # emulation) with headroom: converged bf16 Alg. 4 floors at
                 # ~1.3e-2 from polar(M) at m = 129 (Listing 2: 0.65e-2)
                 emu = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=shift,
-                                       folded=M.shape[1] % 8 == 0).astype(np.float64)
+                                       folded=True).astype(np.float64)
                 e_ref = om.rel_frobenius(ref, P)
                 g3 = max(1e-2, 1.5 * (om.rel_frobenius(emu, P) - e_ref) + 2e-3)
                 assert om.rel_frobenius(X, ref) <= 1e-1, (call, M.shape, T, restart)
@@ -1986,3 +1988,75 @@ def test_polar_split_peers_max_size_hadamard():
     Y = np.concatenate([o[::97].float().cpu().numpy().astype(np.float64) for o in outs], axis=1)
     assert np.all(np.isfinite(Y))
     assert om.rel_frobenius(Y, s * H[::97].astype(np.float64) / math.sqrt(n)) <= 2e-2
+
+
+@pytest.mark.slow
+def test_spectrum_init_random_spikes_fuzz():
+    """App. G step fuzz: 24 random calls, one spiked matrix each (sigma_1 = 1
+    over a geometric tail drawn from [1e-4, 0.3], or a power law j^-p with p
+    in [2, 6]; sides 8..700, both orientations; T = 4..7; 2..12 power
+    iterations): finite, and the error to polar(M) within
+    max(1e-2, 2 S) (capped at 0.05) of the oracle's exact eq. (init_poly)
+    step, S the oracle's own sensitivity to rounding the input to bf16 --
+    or, where the bf16 design itself costs more (power laws, z -> 1: the
+    step's b / F^3 ~ 1 / sqrt(1 - z^2) amplifies A_0's rounding), within
+    1.5 x the excess of the design's emulation (oracle.emulate.
+    r17_init_polar_express, reading R17) + 2e-3: on call 12 (211 x 503,
+    j^-5.9, T = 7) the emulation's excess is 0.051, the GPU's 0.050."""
+    rng = np.random.default_rng(777)
+    c = pe.Context(0)
+    for call in range(24):
+        r = int(rng.integers(8, 701))
+        cc = int(rng.integers(8, 701))
+        T = int(rng.integers(4, 8))
+        q = int(rng.integers(2, 13))
+        if rng.random() < 0.5:
+            M = _spiked(r, cc, seed=8000 + call, tail=tuple(sorted(rng.uniform(1e-4, 0.3, 2))[::-1]))
+        else:
+            M = _spiked(r, cc, seed=8000 + call, law=float(rng.uniform(2.0, 6.0)))
+        Mb = bf16_values(M)
+        c.set_spectrum_init(q)
+        X = run(c, [Mb], T=T)[0]
+        ref, z, applied = oi.polar_express_init(Mb, TABLE, T, power_iters=q)
+        P = oi.exact_polar(Mb)
+        S = om.rel_frobenius(oi.polar_express_init(M, TABLE, T, power_iters=q)[0], ref)
+        assert np.all(np.isfinite(X)), (call, Mb.shape, T, q, z)
+        e_ref = om.rel_frobenius(ref, P)
+        emu = emulate.r17_init_polar_express(Mb, TABLE, T, q)[0].astype(np.float64)
+        excess = om.rel_frobenius(emu, P) - e_ref
+        slack = max(min(max(1e-2, 2 * S), 0.05), 1.5 * excess + 2e-3)
+        assert om.rel_frobenius(X, P) <= e_ref + slack, (call, Mb.shape, T, q, z, applied, excess)
+    c.close()
+
+
+@pytest.mark.parametrize("shape", [(64, 90), (90, 70), (300, 1100), (1100, 300), (700, 1261)])
+def test_unaligned_equals_zero_padded(shape):
+    """Readings R8/R18: a bf16 input whose rows are not 16-byte multiples goes
+    through an oriented copy X_0 = M 2^e (exact) with 1/s 2^-e applied in
+    iteration 1, so its result is bit-identical to the folded path's on the
+    same matrix zero-padded to an aligned width (zero columns add exact zeros
+    to every accumulation and nothing to the norm) -- on the small and the
+    large path, plain and with App. G's first step (there to 1e-6: the power
+    method's partial sums run over a different row count).  At entries of
+    ~1e30 (M 2^100, exact) the copy's exponent shift keeps the first Gram in
+    range: finite and within 2e-2 of the scale-1 result."""
+    r, cc = shape
+    pad = -(-cc // 8) * 8
+    c = pe.Context(0)
+    M = bf16_values(_spiked(r, cc, seed=r + cc, tail=(0.2, 1e-2)))
+    Mp = np.zeros((r, pad))
+    Mp[:, :cc] = M
+    for T in (1, 5):
+        X = run(c, [M], T=T)[0]
+        Xp = run(c, [Mp], T=T)[0]
+        assert np.array_equal(X, Xp[:, :cc]) and np.all(Xp[:, cc:] == 0), T
+        Xh = run(c, [M * 2.0 ** 100], T=T)[0]
+        assert np.all(np.isfinite(Xh)) and om.rel_frobenius(Xh, X) <= 2e-2, T
+    c.set_spectrum_init(8)
+    try:
+        X = run(c, [M], T=5)[0]
+        Xp = run(c, [Mp], T=5)[0]
+    finally:
+        c.set_spectrum_init(0)
+    assert np.all(np.isfinite(X)) and om.rel_frobenius(X, Xp[:, :cc]) <= 1e-6
+    c.close()

@@ -30,7 +30,7 @@ def spread(shape, seeds, T=5, ab_planes=1):
     out = []
     for seed in seeds:
         M = syn.to_bf16_values(syn.gaussian(*shape, seed=seed, std=0.02)).astype(np.float64)
-        E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=ab_planes).astype(np.float64)
+        E = emulate.r8_polar_express(M, TABLE, T, folded=True, ab_planes=ab_planes).astype(np.float64)
         out.append(om.rel_frobenius(E, oi.polar_express(M, TABLE, T)))
     return np.array(out)
 
@@ -42,8 +42,8 @@ def test_r8_emulation_equals_diagonal_pin():
     for shape in ((40, 96), (96, 40), (40, 61)):
         M = syn.diagonal(*shape, sig)
         for T in (1, 3, 5):
-            E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0)
-            d = emulate.diagonal_bf16(sig, TABLE, T, folded=shape[1] % 8 == 0)
+            E = emulate.r8_polar_express(M, TABLE, T, folded=True)
+            d = emulate.diagonal_bf16(sig, TABLE, T, folded=True)
             assert np.array_equal(np.diag(E)[:40], d)
 
 
@@ -80,8 +80,8 @@ def test_r8p_general_emulation_reduces_to_the_diagonal_one():
     for shape in ((40, 96), (96, 40), (40, 61)):
         M = syn.diagonal(*shape, sig)
         for T in (1, 3, 5):
-            E = emulate.r8_polar_express(M, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=2)
-            d = emulate.diagonal_bf16(sig, TABLE, T, folded=shape[1] % 8 == 0, ab_planes=2)
+            E = emulate.r8_polar_express(M, TABLE, T, folded=True, ab_planes=2)
+            d = emulate.diagonal_bf16(sig, TABLE, T, folded=True, ab_planes=2)
             assert np.array_equal(np.diag(E)[:40], d)
 
 
@@ -138,7 +138,7 @@ def alg4_spread(shape, seeds, restart, T=5, spectrum=None):
             M = syn.prescribed_spectrum(*shape, np.geomspace(1.0, 1.0 / spectrum, min(shape)), seed=seed) * 0.01
         M = syn.to_bf16_values(M).astype(np.float64)
         ref = a4.alg4(M, TABLE, T, restart=restart, shift=1e-3)
-        E = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=1e-3, folded=shape[1] % 8 == 0).astype(np.float64)
+        E = emulate.r19_alg4(M, TABLE, T, restart=restart, shift=1e-3, folded=True).astype(np.float64)
         P = oi.exact_polar(M)
         g1.append(om.rel_frobenius(E, ref))
         g3.append(om.rel_frobenius(E, P) - om.rel_frobenius(ref, P))
