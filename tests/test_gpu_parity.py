@@ -2036,8 +2036,8 @@ def test_unaligned_equals_zero_padded(shape):
     iteration 1, so its result is bit-identical to the folded path's on the
     same matrix zero-padded to an aligned width (zero columns add exact zeros
     to every accumulation and nothing to the norm) -- on the small and the
-    large path, plain and with App. G's first step (there to 1e-6: the power
-    method's partial sums run over a different row count).  At entries of
+    large path, plain, with Alg. 4 and with App. G's first step (there to
+    1e-6: the power method's partial sums run over a different row count).  At entries of
     ~1e30 (M 2^100, exact) the copy's exponent shift keeps the first Gram in
     range: finite and within 2e-2 of the scale-1 result."""
     r, cc = shape
@@ -2059,4 +2059,9 @@ def test_unaligned_equals_zero_padded(shape):
     finally:
         c.set_spectrum_init(0)
     assert np.all(np.isfinite(X)) and om.rel_frobenius(X, Xp[:, :cc]) <= 1e-6
+    # Alg. 4 (App. H) reads the same exact copy: bit-identical too
+    c.set_rect_iteration(3, 0.0, 1e-3)
+    X = run(c, [M], T=5)[0]
+    Xp = run(c, [Mp], T=5)[0]
+    assert np.array_equal(X, Xp[:, :cc]) and np.all(Xp[:, cc:] == 0)
     c.close()
