@@ -63,6 +63,13 @@
 
 namespace pe {
 
+// Timeline instrumentation (PE_DEBUG_GEMM bit 128, profiles/phase_timeline.py):
+// compiled in only with -DPE_GEMM_TIMELINE=1 (PE_NVCC_FLAGS at build time)
+#ifndef PE_GEMM_TIMELINE
+#define PE_GEMM_TIMELINE 0
+#endif
+constexpr bool kGemmTimeline = PE_GEMM_TIMELINE != 0;
+
 // per-call matrix flags
 constexpr int kFlagFolded = 1;   // iteration 1 reads the caller's M (no X_0 buffer)
 constexpr int kFlagTall = 2;     // caller matrix is rows > cols (iterate on M^T)
@@ -607,6 +614,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   long long st_wait_tempty = 0, st_wait_full = 0, st_wait_tfull = 0, st_lat = 0, st_nstage = 0;
   __shared__ long long st_issue[8];     // debug: producer issue time per stage (leader CTA)
   const long long st_begin = clock64();
+  // PE_DEBUG_GEMM bit 128: per-CTA %globaltimer timeline of the launch in the
+  // stats slots (0 entry, 1 after the PDL wait, 2 first operand stage landed,
+  // 3 last MMA committed, 4 last result store issued, 5 stores complete, 6 exit,
+  // 7 the last tile's accumulator ready in the epilogue)
+  const bool tl_on = kGemmTimeline && (args.dbg & 128) && args.stats != nullptr;
+  long long* tl_st = tl_on ? args.stats + blockIdx.x * 8 : nullptr;
+  // (bit 128, CTAs 0..63 of a phase-per-launch call: clock64 of the last tile's epilogue steps
+  // of warp 2 at stats + 6144 + 512 mode + 8 blockIdx: 0 accumulator ready, 1 first TMEM load,
+  // 2 first half computed, 3 chunk 0 computed, 4 its store issued, 5 chunk 1's slot free,
+  // 6 chunk 1 computed, 7 the tile's stores have left smem)
+  long long* tl_ep = (tl_on && blockIdx.x < 64 && args.nphase == 0)
+                         ? args.stats + (6144 - 2048 * args.mode) + 512 * args.mode + blockIdx.x * 8 : nullptr;
+  if (tl_on && threadIdx.x == 0) tl_st[0] = (long long)gtimer();
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kSt; ++s) {
@@ -629,6 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
   // dependent launch); nothing below may touch its outputs before this.
   pdl_trigger();
   pdl_wait();
+  if (tl_on && threadIdx.x == 0) tl_st[1] = (long long)gtimer();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -735,6 +756,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           long long t1 = clock64();
           mbar_wait(&full[stage], phase);
           const long long t1e = clock64();
+          if (tl_on && t == cid && kb == 0 && lane == 0) tl_st[2] = (long long)gtimer();
           st_wait_full += t1e - t1;
           if (args.stats != nullptr) { st_lat += t1e - *(volatile long long*)&st_issue[stage]; ++st_nstage; }
           tc_fence_after();
@@ -762,6 +784,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         }
         if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
+        if (tl_on && lane == 0) tl_st[3] = (long long)gtimer();
         if (kP == 3) {
           acc_phase ^= 1;          // both buffers belong to one pass
         } else {
@@ -832,6 +855,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
       long long t2 = clock64();
       mbar_wait(&tfull[acc], acc_phase);
       st_wait_tfull += clock64() - t2;
+      if (tl_on && ew == 0 && lane == 0) tl_st[7] = (long long)gtimer();
+      if (tl_ep != nullptr && ew == 0 && lane == 0) tl_ep[0] = clock64();
       tc_fence_after();
       const int r0 = tl.tm * kBM + row_off;
       const int r = r0 + lane;
@@ -843,6 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         if (c0 >= ncols || !do_work) break;                  // warp-uniform
         const int xb = (kSl == 1) ? 0 : k;                   // operand barrier / phase bit of this chunk
         uint8_t* slot = slots + (kSl == 1 ? 0 : k) * kEpiSlotBytes;
+        const bool tl_rec = tl_ep != nullptr && ew == 0 && lane == 0;
         if (kSl == 1 && need_load && k > 0) {
           // one slot: this chunk's operand is loaded once the previous chunk's
           // result has left the slot
@@ -889,6 +915,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
         }
+        if (tl_rec && k == 1) tl_ep[5] = clock64();
         if (kEdge && need_load && (cfg.ein_tr != cfg.eout_tr || cfg.muon)) {
           // operand and result layouts differ (tall caller matrix, first or
           // last iteration), or the result updates another chunk (Muon): read
@@ -928,9 +955,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             } else {
               tmem_ld32(t_row + k * kEpiCols + 32 * h, w);
             }
+            if (tl_rec && k == 0 && h == 0) tl_ep[1] = clock64();
             epilogue_math<kEdge>(args, cfg, inv, slot, lane, h, w, nullptr, r - (c0 + 32 * h));
+            if (tl_rec && k == 0 && h == 0) tl_ep[2] = clock64();
           }
         }
+        if (tl_rec) tl_ep[k == 0 ? 3 : 6] = clock64();
         {                                       // each chunk leaves as soon as it is done
                                                 // (measured: 2-4 % faster than one burst per tile)
           fence_async_smem();
@@ -941,6 +971,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
             bulk_commit();
           }
         }
+        if (tl_rec && k == 0) tl_ep[4] = clock64();
       }
       tc_fence_before();
       __syncwarp();
@@ -948,20 +979,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
         mbar_arrive_remote(tempty_leader0 + acc * sizeof(uint64_t));
         if (cfg.pub != nullptr) publish_stores(cfg.pub);   // fused: stores complete, counted
         else bulk_wait_read<0>();     // this tile's stores have left smem: slots are free
+        if (tl_ep != nullptr && ew == 0) tl_ep[7] = clock64();
         if (has_next && needs_load(ncfg)) issue_tile(ntl, ncfg, nnc);
       }
       __syncwarp();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (tl_on && ew == 0 && lane == 0) tl_st[4] = (long long)gtimer();
     if (lane == 0) bulk_wait<0>();
+    if (tl_on && ew == 0 && lane == 0) tl_st[5] = (long long)gtimer();
   }
 
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   if (warp == 1) tmem_dealloc_pair(tmem_base, kTmemCols);
-  if (args.stats != nullptr && lane == 0 && (warp == 1 || warp == 2)) {
+  if (tl_on) {
+    if (threadIdx.x == 0) tl_st[6] = (long long)gtimer();
+  } else if (args.stats != nullptr && lane == 0 && (warp == 1 || warp == 2)) {
     long long* st = args.stats + blockIdx.x * 8;
     if (warp == 1) {
       st[0] = clock64() - st_begin; st[1] = st_wait_tempty; st[2] = st_wait_full;

@@ -299,7 +299,7 @@ struct ProfScope {
 extern "C" pe_status pe_debug_stats(pe_ctx c, long long* out) {
   if (!c || !out || !c->stats) return PE_ERR_INVALID_ARG;
   PE_CUDA(cudaDeviceSynchronize());
-  PE_CUDA(cudaMemcpy(out, c->stats, 3 * 2048 * sizeof(long long), cudaMemcpyDeviceToHost));
+  PE_CUDA(cudaMemcpy(out, c->stats, 8 * 1024 * sizeof(long long), cudaMemcpyDeviceToHost));
   return PE_OK;
 }
 
@@ -1690,7 +1690,7 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       g.mode = mode; g.xin = xin; g.final_iter = fin;
       g.a = fa; g.b = fb; g.c = fc;
       if (istep && mode != kModeGram) g.mcoef = at<float>(P, P->o_smcoef);
-      if (c->dbg & 4) {
+      if (c->dbg & (4 | 128)) {
         if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
         g.stats = c->stats + (size_t)mode * 2048;
       }

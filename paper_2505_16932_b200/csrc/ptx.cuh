@@ -278,4 +278,11 @@ __device__ __forceinline__ void acquire_counter(const int* ctr, int need) {
 __device__ __forceinline__ int pow2_exp(float inv) { return inv > 0.f ? ilogbf(inv) : 0; }
 __device__ __forceinline__ float pow2_part(float inv) { return scalbnf(1.0f, pow2_exp(inv)); }
 __device__ __forceinline__ float pow2_residual(float inv) { return scalbnf(inv, -pow2_exp(inv)); }
+
+// %globaltimer (ns): timeline instrumentation of the debug builds of a launch
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 }  // namespace pe

@@ -24,9 +24,9 @@ for _ in range(2):
 torch.cuda.synchronize()
 L = pe.lib()
 L.pe_debug_stats.restype = ctypes.c_int
-buf = (ctypes.c_longlong * (3 * 2048))()
+buf = (ctypes.c_longlong * (8 * 1024))()
 assert L.pe_debug_stats(ctx._h, buf) == 0
-a = np.array(buf[:], dtype=np.int64).reshape(3, 256, 8)
+a = np.array(buf[:6144], dtype=np.int64).reshape(3, 256, 8)
 for mode, name in enumerate(["gram", "poly", "update"]):
     lead = a[mode, 0:148:2]          # leader CTAs
     tot = lead[:, 0].astype(float)

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+out=gpurun_out/r2z_timeline.txt
+: > $out
+for s in "1024 1024" "2048 2048" "4096 4096" "gpt2-small"; do PE_DEBUG_GEMM=128 timeout 300 python profiles/phase_timeline.py $s >> $out 2>&1; done
