@@ -1691,8 +1691,11 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       g.a = fa; g.b = fb; g.c = fc;
       if (istep && mode != kModeGram) g.mcoef = at<float>(P, P->o_smcoef);
       if (c->dbg & (4 | 128)) {
-        if (!c->stats) cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long));
-        g.stats = c->stats + (size_t)mode * 2048;
+        if (!c->stats && cudaMalloc(&c->stats, 8 * 1024 * sizeof(long long)) != cudaSuccess) {
+          cudaGetLastError();          // debug counters only: run without them
+          c->stats = nullptr;
+        }
+        if (c->stats) g.stats = c->stats + (size_t)mode * 2048;
       }
       const int grid = 2 * std::min(g.ntiles, c->num_sms / 2);   // CTA pairs
       if (sh && mode == kModeGram)                               // partial Gram in fp32: own buffer, or

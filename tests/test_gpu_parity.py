@@ -2065,3 +2065,20 @@ def test_unaligned_equals_zero_padded(shape):
     Xp = run(c, [Mp], T=5)[0]
     assert np.array_equal(X, Xp[:, :cc]) and np.all(Xp[:, cc:] == 0)
     c.close()
+
+
+def test_no_fold_copy_is_exact(monkeypatch):
+    """PE_NO_FOLD=1 sends aligned bf16 inputs through the oriented copy
+    (X_0 = M 2^e) and the transpose-back pass instead of reading / writing
+    the caller's buffers in the first / last GEMMs: bit-identical results
+    (reading R2), large path, both orientations."""
+    mats = [bf16_values(syn.gaussian(r, cc, seed=950 + r, std=0.02)) for r, cc in ((512, 1280), (1280, 512))]
+    c = pe.Context(0)
+    ref = run(c, mats, T=5)
+    c.close()
+    monkeypatch.setenv("PE_NO_FOLD", "1")
+    c = pe.Context(0)
+    got = run(c, mats, T=5)
+    c.close()
+    for X, Y in zip(got, ref):
+        assert np.array_equal(X, Y)
