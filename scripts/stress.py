@@ -75,10 +75,10 @@ def main():
             use_rect = rect > 0 and m > 128 and T > 1 and n > 1.5 * T / (T - 1) * m
             if use_rect:
                 ref = a4.alg4(M, TABLE, T, restart=rect, shift=1e-3)
-                emu = emulate.r19_alg4(M, TABLE, T, restart=rect, shift=1e-3, folded=s[1] % 8 == 0)
+                emu = emulate.r19_alg4(M, TABLE, T, restart=rect, shift=1e-3, folded=True)
             else:
                 ref = oi.polar_express(M, TABLE, T)
-                emu = emulate.r8_polar_express(M, TABLE, T, folded=s[1] % 8 == 0 and kind == "bf16",
+                emu = emulate.r8_polar_express(M, TABLE, T, folded=kind == "bf16",
                                                ab_planes=2 if (planes == 2 and small and kind == "bf16") else 1)
             emu = emu.astype(np.float64)
             e_ref = om.rel_frobenius(ref, P)
