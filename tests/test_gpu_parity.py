@@ -2082,3 +2082,34 @@ def test_no_fold_copy_is_exact(monkeypatch):
     c.close()
     for X, Y in zip(got, ref):
         assert np.array_equal(X, Y)
+
+
+@pytest.mark.parametrize("shape", [(256, 384), (300, 200), (200, 1000)])
+def test_spectrum_init_diagonal_emulation(shape):
+    """Reading R17 on hardware: on a diagonal input with one dominant sigma
+    (App. G's case) every product has one term, so the GPU's App. G step plus
+    T iterations equals the design's emulation (oracle.emulate.
+    r17_init_polar_express) up to the power method's own rounding: z comes
+    from an fp32 matrix-vector chain on the GPU and an fp64 one in the
+    emulation, which can move a' = fp32(a/F), b' = fp32(b/F^3) by an ulp.
+    Gate: every diagonal entry within 1 bf16 ulp, >= 95 % bit-identical,
+    off-diagonal exactly zero."""
+    k = min(shape)
+    sig = syn.to_bf16_values(np.concatenate([[1.0], np.geomspace(0.12, 0.01, k - 1)])).astype(np.float64)
+    M = syn.diagonal(*shape, sig)
+    c = pe.Context(0)
+    c.set_spectrum_init(8)
+    try:
+        for T in (1, 3):
+            X = run(c, [M], T=T)[0]
+            emu, z, applied = emulate.r17_init_polar_express(M, TABLE, T, 8)
+            assert applied
+            d = np.diag(X)[:k].astype(np.float32)
+            e = np.diag(emu.astype(np.float64))[:k].astype(np.float32)
+            ulp = np.abs(d.view(np.int32).astype(np.int64) - e.view(np.int32).astype(np.int64)) >> 16
+            assert ulp.max() <= 1 and np.mean(ulp == 0) >= 0.95, (T, z, int(ulp.max()), float(np.mean(ulp == 0)))
+            off = X.copy()
+            off[np.arange(k), np.arange(k)] = 0
+            assert np.all(off == 0)
+    finally:
+        c.close()
