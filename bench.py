@@ -204,8 +204,8 @@ def kind_work(shapes, T):
         fl["poly"] += m * m * (m + 1)
         fl["update"] += 2.0 * m * m * n
         by["norm"] += 2.0 * m * n
-        by["scale"] += 4.0 * m * n
-        if r > c:
+        if c % 8:                       # bf16 rows that are not 16-byte multiples: copy passes
+            by["scale"] += 4.0 * m * n
             by["transpose_back"] += 4.0 * m * n
     fl["fused"] = T * (fl["gram"] + fl["poly"] + fl["update"])    # one launch runs all 3T phases
     return fl, by
@@ -243,6 +243,29 @@ def roofline(prof, shapes, T, step_ms, peaks, src, workload=None):
                 "launch_ms": round(per_launch_ms, 4),
                 "timing": "CUDA events around each launch of this kernel, on its stream, in a second pass of the same K steps",
                 "share_of_step": round(tot / max(sum(v[0] for v in prof.values()), 1e-9), 4)})
+    return out
+
+
+def kernel_table(prof, shapes, T, step_ms, peaks):
+    """Every launched kernel kind against its own roofline (same event timing
+    and algorithmic counts as `roofline`, which reports the dominant one)."""
+    fl, by = kind_work(shapes, T)
+    sustained = step_ms > 50.0
+    out = {}
+    for kind, (tot, cnt) in prof.items():
+        if cnt <= 0 or tot <= 0 or (kind not in fl and kind not in by):
+            continue
+        per = tot / cnt
+        if kind in fl:
+            a = fl[kind] / (per * 1e-3) / 1e12
+            pk = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
+            out[kind] = {"bound": "tensor", "unit": "TFLOP/s", "achieved": round(a, 2), "peak": pk,
+                         "frac": round(a / pk, 4), "launch_ms": round(per, 4), "launches": cnt}
+        else:
+            a = by[kind] / (per * 1e-3) / 1e9
+            pk = peaks["hbm_gbs"]
+            out[kind] = {"bound": "hbm", "unit": "GB/s", "achieved": round(a, 1), "peak": pk,
+                         "frac": round(a / pk, 4), "launch_ms": round(per, 4), "launches": cnt}
     return out
 
 
@@ -567,6 +590,7 @@ def main():
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
+        "per_kernel_roofline": kernel_table(prof, [shapes[i] for i in idx], T, mean_ms, peaks),
         "per_kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
         "ms_per_step_stats": pctl(ms),
         "graph_replay": (pctl(graph_ms) if isinstance(graph_ms, list) else (None if world > 1 else graph_ms)),
@@ -597,6 +621,7 @@ def main():
                             "frac_of_bf16_peak_sustained": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
                             "frac_of_bf16_peak_burst": round(f2 / (m2 * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
                             "roofline": None if rk else roofline(prof2, sh, T, m2, peaks, src, name),
+                            "per_kernel_roofline": None if rk else kernel_table(prof2, sh, T, m2, peaks),
                             "method": (f"App. H Alg. 4 (restart {rk}, shift 1e-3) on the matrices with aspect "
                                        f"> 1.5 T / (T - 1); tflops from its own algorithmic count" if rk
                                        else "Listing 2"),
