@@ -548,12 +548,42 @@ def main():
     # e2e through the public API on pinned host buffers (H2D + D2H inside)
     hin = [x.cpu().pin_memory() for x in xs]
     hout = [torch.empty_like(h).pin_memory() for h in hin]
-    ctx.polar_host(hin, hout, iters=T)
     e2e_ms = []
-    for _ in range(max(3, min(args.steps, 10))):
-        t0 = time.perf_counter()
-        ctx.polar_host(hin, hout, iters=T)      # synchronises its stream
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    if not dist_on:
+        ctx.polar_host(hin, hout, iters=T)
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            ctx.polar_host(hin, hout, iters=T)      # synchronises its stream
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_note = ("pe_polar_host on pinned host tensors, wall clock per call (host->device copies, compute, "
+                    "device->host copies; synchronises): the batch is pipelined in groups so the PCIe transfers "
+                    "(both directions concurrently) hide behind the compute except the first group's H2D and "
+                    "the last group's D2H; no L2 flush between calls")
+    else:
+        # N ranks: each rank's owned inputs in from pinned host memory, the
+        # sharded call (compute + libpe's all-gather: every rank ends with every
+        # result), its owned results out to pinned host memory (the union over
+        # ranks is the whole set); wall clock between barriers, max over ranks
+        stream = torch.cuda.current_stream(device)
+        xin_e = [None] * len(shapes)
+        for i, x in zip(idx, xs):
+            xin_e[i] = x
+        ys_e = ys
+        for k in range(max(3, min(args.steps, 10)) + 1):
+            torch.distributed.barrier()
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            for x, h in zip(xs, hin):
+                x.copy_(h, non_blocking=True)
+            ctx.polar_sharded(xin_e, ys_e, iters=T, stream=stream)
+            for i, h in zip(idx, hout):
+                h.copy_(ys_e[i], non_blocking=True)
+            torch.cuda.synchronize(device)
+            if k > 0:                                   # the first pass is a warm-up
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_note = ("per rank: its owned inputs host->device from pinned memory, pe_polar_sharded (compute + "
+                    "libpe's per-bucket all-gather, every rank ends with every result), its owned results "
+                    "device->host into pinned memory; wall clock between barriers, max over ranks")
     e2e_mean = sum(e2e_ms) / len(e2e_ms)
     if dist_on:
         t = torch.tensor([e2e_mean], device=device)
@@ -582,11 +612,7 @@ def main():
         "peak_used": f"{peaks[peak_key]} TFLOP/s ({src} {'sustained' if peak_key.endswith('sustained') else 'burst'})",
         "e2e": {"value": round(len(shapes) / (e2e_mean * 1e-3), 3), "unit": UNIT,
                 "ms_per_step": round(e2e_mean, 3),
-                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
-                "note": "pe_polar_host on pinned host tensors, wall clock per call (host->device copies, compute, "
-                        "device->host copies; synchronises): the batch is pipelined in groups so the PCIe transfers "
-                        "(both directions concurrently) hide behind the compute except the first group's H2D and "
-                        "the last group's D2H; no L2 flush between calls"},
+                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes, "note": e2e_note},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "roofline": roofline(prof, [shapes[i] for i in idx], T, mean_ms, peaks, src, args.workload),
