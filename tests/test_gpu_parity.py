@@ -623,6 +623,28 @@ def test_muon_step_against_oracle(ctx):
         assert om.rel_frobenius(step, -W1 / lr) <= 3e-2
 
 
+def test_muon_step_unaligned_shapes(ctx):
+    """pe_muon_step on rows that are not 16-byte multiples (the momentum is
+    written by the norm pass, then copied exactly as M 2^e, reading R2; the
+    weight update goes through the finalize pass): G1 / G3 of the step
+    direction against oracle.muon_step, momentum to bf16 rounding."""
+    beta, lr = 0.95, 0.25
+    shapes = [(300, 130), (130, 301), (520, 203)]
+    Ms = [bf16_values(syn.gaussian(r, c, seed=140 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    Gs = [bf16_values(syn.gaussian(r, c, seed=150 + i, std=0.02)) for i, (r, c) in enumerate(shapes)]
+    w = [torch.zeros((r, c), dtype=torch.bfloat16, device="cuda") for r, c in shapes]
+    m = [to_dev_bf16(x) for x in Ms]
+    ctx.muon_step(w, m, [to_dev_bf16(x) for x in Gs], beta=beta, lr=lr, iters=5)
+    torch.cuda.synchronize()
+    for wi, mi, M, G in zip(w, m, Ms, Gs):
+        W1, Mt = oi.muon_step(np.zeros(M.shape), M, G, beta, lr, TABLE, 5)
+        m1 = mi.float().cpu().numpy().astype(np.float64)
+        assert om.rel_frobenius(m1, Mt) <= 2.0 ** -8
+        step = -wi.float().cpu().numpy().astype(np.float64) / lr
+        check_g1_g3(step, m1)
+        assert om.rel_frobenius(step, -W1 / lr) <= 3e-2
+
+
 def test_muon_step_rejects_aliasing(ctx):
     x = torch.zeros((64, 64), dtype=torch.bfloat16, device="cuda")
     y = torch.zeros_like(x)
