@@ -217,9 +217,10 @@ def r17_init_polar_express(M_bf16, table, T, power_iters, folded=True):
                       X_0 = bf16(M inv))
         z   = sqrt(lambda / d): lambda the Rayleigh quotient of ``power_iters``
               power steps on the fp32 acc (start vector of iteration.power_start),
-              d = ||M||^2 (folded) or ||M||^2 inv^2
+              d = ||M||^2 (folded) or trace(acc) = ||X_0||^2 of the rounded X_0
         (a, b) = eq. (init_poly) at z when 1/sqrt(2) <= z <= 1 - 1e-6,
-              else (1, 0); F^2 = ||M||^2 inv^2; a' = fp32(a / F), b' = fp32(b / F^3)
+              else (1, 0); F^2 = ||M||^2 inv^2 (folded) or trace(acc);
+              a' = fp32(a / F), b' = fp32(b / F^3)
         A_0 = bf16(acc [* inv^2])
         X_1 = bf16(fp32(fp32(a' X) + fp32(b' (A_0 X))) [* inv])
     Used to measure how far the bf16 design's own rounding of this step
@@ -239,8 +240,11 @@ def r17_init_polar_express(M_bf16, table, T, power_iters, folded=True):
     if not folded:
         X = _bf16(X * inv)
     acc = mm(X, X.T)
-    f2 = ssq * float(inv) * float(inv)
-    d = ssq if folded else f2
+    if folded:
+        f2 = ssq * float(inv) * float(inv)
+        d = ssq
+    else:                       # X_0 rounded: its norm from the same Gram (trace)
+        f2 = d = float(np.sum(np.diag(acc).astype(np.float64)))
     A64 = acc.astype(np.float64)
     v = power_start(A64.shape[0])
     lam = 0.0

@@ -791,8 +791,29 @@ __global__ void __launch_bounds__(kSymvThreads) pe_symv_kernel(const SymvArgs a)
 
 // Per matrix: z = sqrt(lambda / F^2), F^2 = ssq * inv^2 (= ||X_0||_F^2), and
 // the first step's (a/F, b/F^3) from eq. (init_poly), or (1, 0).
+// trace(A_0) of the raw fp32 Gram per matrix (one block each, fixed-order
+// reduction): ||X_0||_F^2 of the rounded X_0 = bf16(M inv) of fp32 inputs, the
+// scale the Rayleigh quotient of that Gram is on (App. G, reading R17)
+__global__ void __launch_bounds__(256) pe_trace_kernel(float* const* a32, const MatDev* mats, double* tr, int count) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double red[256];
+  const int i = blockIdx.x;
+  if (i >= count) return;
+  const MatDev md = mats[i];
+  double s = 0.0;
+  for (int j = threadIdx.x; j < md.m; j += blockDim.x) s += (double)a32[i][(size_t)j * md.ldm + j];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tr[i] = red[0];
+}
+
 __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const float* inv, float* mcoef,
-                                    int count, double margin, const int* mflags) {
+                                    int count, double margin, const int* mflags, const double* tr) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -801,10 +822,17 @@ __global__ void pe_init_coef_kernel(const double* lam, const double* ssq, const 
   // accumulated: of M M^T for folded bf16 input (flags 8 | 1), of 4^e M M^T
   // for copied bf16 input (flag 8), of X_0 X_0^T = (M/s)(M/s)^T for fp32
   // input; z = sigma_1 / ||.||_F on the same scale
-  const double f2 = ssq[i] * (double)inv[i] * (double)inv[i];
+  double f2 = ssq[i] * (double)inv[i] * (double)inv[i];
   // bf16 copies hold M * 2^e (pow2_part): their Gram is 4^e M M^T
   const double p2 = (double)pow2_part(inv[i]);
-  const double den2 = (mflags[i] & 8) ? ((mflags[i] & 1) ? ssq[i] : ssq[i] * p2 * p2) : f2;
+  double den2 = (mflags[i] & 8) ? ((mflags[i] & 1) ? ssq[i] : ssq[i] * p2 * p2) : f2;
+  if (!(mflags[i] & 8) && tr != nullptr) {
+    // fp32 input: X_0 = bf16(M inv) is rounded, so its norm is not ||M|| inv;
+    // z and F from the same Gram keep z <= sigma_1 / F (the lower bound the
+    // step's tail bound sqrt(1 - z^2) relies on)
+    f2 = tr[i];
+    den2 = tr[i];
+  }
   const double z = (den2 > 0.0 && lam[i] > 0.0) ? sqrt(lam[i] / den2) : 0.0;
   float ca = 1.f, cb = 0.f;
   if (z >= 0.70710678118654752 && z <= 1.0 - 1e-6) {

@@ -155,7 +155,7 @@ struct Plan {
   // work items (matrix, 32 rows), vectors (two ping-pong sets of sum m floats),
   // per-item partials, per-matrix counters / lambda / ||w||^2 (x2) / sum of squares / (a, b)
   size_t o_sitem_mat = 0, o_sitem_r0 = 0, o_sitem0 = 0, o_snitem = 0, o_svoff = 0, o_sv = 0, o_sv0 = 0, o_spart = 0;
-  size_t o_scnt = 0, o_slam = 0, o_snrm = 0, o_sssq = 0, o_smcoef = 0;
+  size_t o_scnt = 0, o_slam = 0, o_snrm = 0, o_sssq = 0, o_smcoef = 0, o_str = 0;
   size_t o_a32 = 0;             // per matrix fp32 Gram (App. G plans, `init`), device pointers
   bool init = false;
   int n_sitems = 0;
@@ -843,6 +843,7 @@ static pe_status build_plan(pe_ctx c, const int64_t* shapes, int count, pe_dtype
     P->o_slam = bl.add(std::vector<double>(count, 0.0));
     P->o_snrm = bl.add(std::vector<double>(2 * (size_t)count, 0.0));
     P->o_sssq = bl.add(std::vector<double>(count, 0.0));
+    P->o_str = bl.add(std::vector<double>(count, 0.0));
     P->o_smcoef = bl.add(std::vector<float>(2 * (size_t)count, 0.f));
     std::vector<float*> a32(count, nullptr);
     for (int i = 0; i < count && init; ++i) a32[i] = reinterpret_cast<float*>(ws + offs[9 * i + 8]);
@@ -1753,9 +1754,16 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
           launch(pe_symv_kernel<float>, sgrid, kSymvThreads, 0, st, sa);
           ++launches;
         }
+        const double* tr = nullptr;
+        if (io & 1) {                         // fp32 input: ||X_0||^2 of the rounded X_0
+          launch(pe_trace_kernel, count, 256, 0, st, (float* const*)sa.a32, (const MatDev*)sa.mats,
+                 at<double>(P, P->o_str), count);
+          ++launches;
+          tr = at<double>(P, P->o_str);
+        }
         launch(pe_init_coef_kernel, cdiv(count, 128), 128, 0, st, (const double*)sa.lam,
                (const double*)at<double>(P, P->o_sssq), (const float*)at<float>(P, P->o_inv),
-               at<float>(P, P->o_smcoef), count, c->init_margin, (const int*)at<int>(P, P->o_flags));
+               at<float>(P, P->o_smcoef), count, c->init_margin, (const int*)at<int>(P, P->o_flags), tr);
         ++launches;
       }
       if (sh && mode == kModeGram) {

@@ -95,3 +95,32 @@ def test_pow2_prescale_is_bit_identical_to_folding(scale):
         G = syn.to_bf16_values(syn.gaussian(*shape, seed=2, std=0.02) * scale).astype(np.float64)
         assert np.array_equal(emulate.r8_polar_express(G, TABLE, 2, folded=True).view(np.uint32),
                               _r8_prescaled(G, 2).view(np.uint32))
+
+
+def test_r17_explicit_x0_keeps_the_lower_bound():
+    """Reading R17 on the fp32-input path (X_0 = bf16(M inv) rounded): z and F
+    come from the same fp32 Gram (trace(acc) = ||X_0||^2), so z stays a lower
+    bound of sigma_1(X_0) / ||X_0||_F up to the fp32 Gram's own
+    rounding.  Taking F from the unrounded ||M|| inv instead overshoots it by
+    up to 1.3e-4 on these power laws (the planted variant below)."""
+    rng = np.random.default_rng(5)
+    over_fixed, over_planted = 0.0, 0.0
+    for _ in range(24):
+        r, c = int(rng.integers(32, 300)), int(rng.integers(32, 300))
+        k = min(r, c)
+        U, _ = np.linalg.qr(rng.standard_normal((r, k)))
+        V, _ = np.linalg.qr(rng.standard_normal((c, k)))
+        M = ((U * np.arange(1, k + 1) ** -rng.uniform(2, 6)) @ V.T * 0.01).astype(np.float32).astype(np.float64)
+        X = (M.T if r > c else M).astype(np.float32)
+        ssq = float(np.sum(X.astype(np.float64) ** 2))
+        inv = np.float32(1.0 / (np.sqrt(ssq) * 1.01 + 1e-7))
+        X0 = emulate._bf16(X * inv).astype(np.float64)
+        s = np.linalg.svd(X0, compute_uv=False)
+        z_true = s[0] / np.sqrt(np.sum(s * s))
+        _, z, _ = emulate.r17_init_polar_express(M, TABLE, 1, 12, folded=False)
+        over_fixed = max(over_fixed, z - z_true)
+        # planted: the Rayleigh quotient of the rounded X_0's Gram over ||M||^2 inv^2
+        lam = (z ** 2) * float(np.sum(np.diag((X0 @ X0.T).astype(np.float32)).astype(np.float64)))
+        over_planted = max(over_planted, np.sqrt(lam / (ssq * float(inv) ** 2)) - z_true)
+    assert over_fixed <= 2e-6, over_fixed
+    assert over_planted > 1e-5, over_planted

@@ -2133,5 +2133,20 @@ def test_spectrum_init_diagonal_emulation(shape):
             off = X.copy()
             off[np.arange(k), np.arange(k)] = 0
             assert np.all(off == 0)
+        # fp32 input (pe_polar_ex, bf16 arithmetic): X_0 = bf16(M inv) is
+        # rounded, F^2 and z's denominator are the fp32 Gram's trace (R17)
+        sig32 = np.concatenate([[1.0], np.geomspace(0.12, 0.01, k - 1)]).astype(np.float32).astype(np.float64)
+        M32 = syn.diagonal(*shape, sig32)
+        for T in (1, 3):
+            y = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+            c.polar_ex([torch.from_numpy(M32.astype(np.float32)).cuda()], [y], iters=T)
+            torch.cuda.synchronize()
+            X = y.float().cpu().numpy().astype(np.float64)
+            emu, z, applied = emulate.r17_init_polar_express(M32, TABLE, T, 8, folded=False)
+            assert applied
+            d = np.diag(X)[:k].astype(np.float32)
+            e = np.diag(emu.astype(np.float64))[:k].astype(np.float32)
+            ulp = np.abs(d.view(np.int32).astype(np.int64) - e.view(np.int32).astype(np.int64)) >> 16
+            assert ulp.max() <= 1 and np.mean(ulp == 0) >= 0.95, ("fp32 in", T, z, int(ulp.max()))
     finally:
         c.close()
