@@ -91,6 +91,7 @@ struct GemmArgs {
   float* scratch;              // kP = 3: 128 x 256 fp32 per CTA (running sum of the K passes)
   float* const* out32;         // sharded calls: the Gram writes its raw fp32 accumulator here (m x m,
                                // leading dim ldm, blocks on/above the diagonal), not bf16 A; else nullptr
+  int out32_both = 0;          // App. G step: the raw fp32 accumulator to out32 AND the usual bf16 A
   int muon;                    // pe_muon_step: the last update's direct output is the weight W,
   float lr;                    // updated to bf16(W - lr * bf16(X'))
   // one phase per launch (nphase == 0): the phase of every tile
@@ -907,7 +908,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
               }
             }
           }
-          continue;
+          if (!args.out32_both) continue;      // App. G: the bf16 A of the same accumulator too
         }
         if (kSl == 1 && k > 0 && !need_load) {
           // single staging slot (Gram: no epilogue operand): the previous

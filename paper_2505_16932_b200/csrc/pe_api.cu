@@ -1702,16 +1702,12 @@ static pe_status polar_impl(pe_ctx c, const void* const* in, void* const* out, c
       if (sh && mode == kModeGram)                               // partial Gram in fp32: own buffer, or
         g.out32 = sh->slots ? c->peer_out + (t & 1) : c->sh_ptr;  // this rank's peer-visible slot
       if (istep && mode == kModeGram) {
-        // App. G: the Gram once more with its raw fp32 accumulator stored, for
-        // the power method (its Rayleigh quotient on bf16(A_0) can exceed
+        // App. G: the same Gram launch also stores its raw fp32 accumulator,
+        // for the power method (the Rayleigh quotient of bf16(A_0) can exceed
         // sigma_1^2 by ~2^-9 relative, which breaks z <= sigma_1
         // and with it the tail bound sqrt(1 - z^2): R17)
-        GemmArgs g32 = g;
-        g32.out32 = at<float*>(P, P->o_a32);
-        ProfScope ps(c, 2, st);
-        const size_t sm = gemm_smem_bytes<kGramStages, 1>();
-        launch(pe_gemm_sm100<kGramStages, 1, true>, grid, kGemmThreads, sm, st, g32);
-        ++launches;
+        g.out32 = at<float*>(P, P->o_a32);
+        g.out32_both = 1;
       }
       {
       ProfScope ps(c, 2 + mode, st);
