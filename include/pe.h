@@ -169,7 +169,9 @@ pe_status pe_reserve(pe_ctx ctx, const int64_t* shapes, int count, pe_dtype dtyp
  *                  enqueued on it, the call does not synchronise.
  * Per matrix: s = ||M||_F * 1.01 + 1e-7 (reading R1; fp64 sum of
  * squares), X_0 = M / s, oriented so that the Gram is on the smaller side
- * (strict rows > cols, R10); then T x (Gram, b A + c A^2, a X + B X)
+ * (strict rows > cols, R10; bf16 X_0 is never rounded: 1/s is applied
+ * in the first Gram / update epilogues, on the caller's M or on an exact
+ * oriented copy M 2^e, R2); then T x (Gram, b A + c A^2, a X + B X)
  * on sm_100a tcgen05 tensor cores; the result is written to out[i] in the
  * caller's orientation.  A zero matrix gives zeros (R9).
  * Errors: PE_ERR_INVALID_ARG (count < 0, NULL pointer, rows/cols < 1 or
@@ -293,8 +295,10 @@ pe_status pe_polar_split_peers(pe_ctx ctx, const void* in, void* out, int64_t ro
  * 1/sqrt(2) <= z <= 1 - 1e-6 the odd cubic p(x) = a x + b x^3 of
  * eq. (init_poly) (p(sqrt(1-z^2)) = p(z) = 1 on the unit-norm
  * scale) is applied before the T iterations, else the step is the identity.
- * Costs two extra Grams (one stores the fp32 accumulator for the power
- * method) + one update (+ power_iters passes over A_0); matrices run
+ * Costs one extra Gram (which also stores its fp32 accumulator for the
+ * power method) + one update (+ power_iters passes over A_0; fp32 inputs also
+ * one pass over A_0's diagonal: ||X_0||_F^2 of the rounded X_0 as its trace);
+ * matrices run
  * on the large path (the small-matrix path is bypassed).  fp32 calls and
  * pe_muon_step ignore it.  Errors: PE_ERR_INVALID_ARG (NULL, power_iters < 0
  * or > 1000).
