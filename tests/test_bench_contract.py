@@ -42,3 +42,27 @@ def test_our_arm_line():
     assert d["roofline"]["bound"] == "tensor" and 0 < d["roofline"]["frac"] < 1
     assert d["clocks"]["sm_max_mhz"] and d["e2e"]["h2d_bytes_per_step"] > 0
     assert len(d["ms_per_step_stats"]["all_ms"]) == 2
+
+
+def test_kernel_accounting_helpers():
+    """bench.py's algorithmic counts: symmetric-aware GEMM flops
+    per launch, norm bytes, copy-pass bytes only for rows that are not 16-byte
+    multiples; every launched kind against its own roofline."""
+    sys.path.insert(0, ROOT)
+    import bench
+    shapes = [(768, 3072), (3072, 768), (100, 90)]
+    fl, by = bench.kind_work(shapes, 5)
+    m, n = 768, 3072
+    assert fl["gram"] == 2 * m * (m + 1) * n + 90 * 91 * 100
+    assert fl["poly"] == 2 * m * m * (m + 1) + 90 * 90 * 91
+    assert fl["update"] == 2 * (2.0 * m * m * n) + 2.0 * 90 * 90 * 100
+    assert by["norm"] == 2 * (2.0 * m * n) + 2.0 * 90 * 100
+    assert by["scale"] == 4.0 * 90 * 100 and by["transpose_back"] == 4.0 * 90 * 100   # only the unaligned one
+    peaks = {"bf16_tflops": 1000.0, "bf16_tflops_sustained": 800.0, "hbm_gbs": 5000.0}
+    prof = {"norm": (0.2, 2), "gram": (3.0, 10), "poly": (0.0, 0), "update": (5.0, 10)}
+    t = bench.kernel_table(prof, shapes, 5, 10.0, peaks)
+    assert set(t) == {"norm", "gram", "update"}
+    assert t["gram"]["bound"] == "tensor" and t["gram"]["peak"] == 1000.0       # short step: burst peak
+    assert abs(t["gram"]["achieved"] - fl["gram"] / 0.3e-3 / 1e12) < 0.01
+    assert t["norm"]["bound"] == "hbm" and abs(t["norm"]["achieved"] - by["norm"] / 0.1e-3 / 1e9) < 0.1
+    assert bench.kernel_table(prof, shapes, 5, 100.0, peaks)["update"]["peak"] == 800.0   # long step: sustained
