@@ -656,6 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
     // ------------------------------------------------------------ producer
     if (elect_one()) {
       const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
+      const uint64_t pol_keep = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       TileCfg nxt;
@@ -688,11 +689,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * kBBytes;
           const int k0 = (args.dbg & 8) ? 0 : kb * kBK;   // dbg 8: every load hits the same (L2-resident) boxes
+          // the update's left operand (B = b A + c A^2) is re-read by every
+          // column panel of X: keep it in L2 (evict_last); X streams through
+          const bool keep_a = kP == 1 && o.mode == kModeUpdate && !(args.dbg & 16384);
           if (o.a_wide && (kb >> 2) < o.pan_a) {                    // block below the diagonal
-            tma_load_2d_pair(a_dst, o.Amn, bar, o.row_a, k0 + pa);
-            tma_load_2d_pair(a_dst + kBoxBytes, o.Amn, bar, o.row_a + 64, k0 + pa);
+            if (keep_a) {
+              tma_load_2d_pair_hint(a_dst, o.Amn, bar, o.row_a, k0 + pa, pol_keep);
+              tma_load_2d_pair_hint(a_dst + kBoxBytes, o.Amn, bar, o.row_a + 64, k0 + pa, pol_keep);
+            } else {
+              tma_load_2d_pair(a_dst, o.Amn, bar, o.row_a, k0 + pa);
+              tma_load_2d_pair(a_dst + kBoxBytes, o.Amn, bar, o.row_a + 64, k0 + pa);
+            }
           } else if (o.a_wide) {
-            tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);      // one 64 x 128 box
+            if (keep_a) tma_load_2d_pair_hint(a_dst, o.A, bar, k0, o.row_a + pa, pol_keep);
+            else tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);      // one 64 x 128 box
           } else if (!o.a_mn) {
             tma_load_2d_pair(a_dst, o.A, bar, k0, o.row_a + pa);
             tma_load_2d_pair(a_dst + kBoxBytes, o.A, bar, k0, o.row_a + pa + 64);
@@ -967,8 +977,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1) pe_
           fence_async_smem();
           __syncwarp();
           if (lane == 0 && !(args.dbg & 32)) {
-            if (!(kEdge && cfg.eout_tr)) tma_store_2d(cfg.eout, slot, c0, r0);
-            else tma_store_2d(cfg.eout, slot, r0, c0);
+            if (cfg.mode == kModeUpdate && !(args.dbg & 16384)) {
+              // X' is not read again in this launch: first out of L2
+              const uint64_t pol = l2_policy_evict_first();
+              if (!(kEdge && cfg.eout_tr)) tma_store_2d_hint(cfg.eout, slot, c0, r0, pol);
+              else tma_store_2d_hint(cfg.eout, slot, r0, c0, pol);
+            } else if (!(kEdge && cfg.eout_tr)) {
+              tma_store_2d(cfg.eout, slot, c0, r0);
+            } else {
+              tma_store_2d(cfg.eout, slot, r0, c0);
+            }
             bulk_commit();
           }
         }
